@@ -1,0 +1,171 @@
+/*
+ * bd3mg_b200.h -- C ABI of the B200-native BD3MG hot path.
+ *
+ * Drop-in boundary for the reference package `bd3mg` (arXiv 2002.02328 CPU
+ * reference, /root/reference/pkg).  The reference binds its native core at
+ * import time in pkg/src/bd3mg/kernels.py:16-28 (`_core` or `_kernels_np`);
+ * a ctypes binding of this library replaces that module (see
+ * INTEGRATION.md).  Every entry point:
+ *   - takes plain pointers and sizes (no framework types),
+ *   - returns an int status (BD3MG_OK = 0); the message of the last failure on
+ *     the calling thread is available from bd3mg_last_error(),
+ *   - device-pointer variants are asynchronous on `stream` (a cudaStream_t
+ *     passed as void*, NULL = legacy default stream),
+ *   - *_host variants take host buffers and are synchronous (they stage
+ *     through device memory and return after the result is on the host).
+ * Volumes are C-contiguous (nz, ny, nx), x fastest; kernel stacks are
+ * (nz, kz, ky, kx) indexed by the OUTPUT depth (reference blur.py:5-12).
+ * Depth coordinates are global: fragment plane 0 is depth frag_z0.
+ */
+#ifndef BD3MG_B200_H
+#define BD3MG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BD3MG_OK = 0,
+  BD3MG_EINVAL = 1,      /* bad shape / range / coverage (reference: ValueError) */
+  BD3MG_ECUDA = 2,       /* CUDA runtime failure */
+  BD3MG_EWORKSPACE = 3,  /* workspace smaller than *_ws_bytes reported */
+  BD3MG_ENONFINITE = 4   /* non-finite gradient (directions.py:64-65) */
+};
+
+enum { BD3MG_F64 = 0, BD3MG_F32 = 1 };
+
+/* Problem geometry: volume (nz, ny, nx) and kernel extents (kz, ky, kx), odd. */
+typedef struct {
+  int64_t nx, ny, nz;
+  int32_t kx, ky, kz;
+  int32_t dtype; /* BD3MG_F64 or BD3MG_F32: element type of every array */
+} bd3mg_geom_t;
+
+/* Regulariser weights: reference objective.py:46-62 (RegParams). */
+typedef struct {
+  double lam, eta, kappa, delta, x_min, x_max;
+} bd3mg_reg_t;
+
+/* One block step of the memory-gradient solver (reference
+ * directions.py:89-94 mg_direction + scheduler.py:151-153 receive_update).
+ * `frag` is the anchor slab; it must cover [z_lo-kz, z_hi+kz] clamped to the
+ * volume (blur.py:190-198 slab_support).  Pointers are device pointers of
+ * the geometry's dtype. */
+typedef struct {
+  const void* frag;
+  int64_t frag_z0, nzf;
+  int64_t z_lo, z_hi;
+  const void* d_mem;  /* block rows of the memory direction, or NULL (= 0) */
+  void* inc_out;      /* block rows receiving the increment, or NULL */
+  void* x_rows;       /* block rows of an iterate updated in place, or NULL */
+  void* dmem_rows;    /* block rows of the memory store overwritten, or NULL */
+} bd3mg_task_t;
+
+/* Per-task StepInfo record (reference directions.py:29-40), 16 doubles:
+ * [0..2] gram (00,01,11 over the kept columns; one column -> [0]),
+ * [3..4] rhs, [5..6] coeffs, [7] ncols, [8] status (1 = non-finite g),
+ * [9] |g|, [10] coefficient of -g, [11] coefficient of d_mem,
+ * [12] kept-column mask (1 = -g, 2 = d_mem). */
+#define BD3MG_INFO_DOUBLES 16
+
+/* Objective terms written by bd3mg_eval_f (device, 7 doubles):
+ * [0] data, [1] box, [2] tv, [3] axial, [4] f, [5] |x-snap|^2, [6] |snap|^2 */
+#define BD3MG_EVAL_DOUBLES 7
+
+const char* bd3mg_last_error(void);
+const char* bd3mg_version(void);
+
+/* ---- drop-in native core: replaces bd3mg._core (src/_core.pyx:17-96) ---- */
+/* H rows: out[i] = sum_{a,b,c} K[zo,a,b,c] frag[zo+a-rz-frag_z0, y+b-ry, x+c-rx],
+ * zo = out_lo + i, zero outside the fragment.  Replaces
+ * _core.depthvar_correlate (src/_core.pyx:17-53).  out: (out_hi-out_lo+1, ny, nx). */
+int bd3mg_depthvar_correlate_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                 const double* kernels, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                                 int64_t frag_z0, int64_t out_lo, int64_t out_hi, double* out, void* stream);
+/* H^T rows.  Replaces _core.depthvar_correlate_adjoint (src/_core.pyx:56-96). */
+int bd3mg_depthvar_correlate_adjoint_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                         const double* kernels, int64_t nzk, int64_t kz, int64_t ky,
+                                         int64_t kx, int64_t frag_z0, int64_t out_lo, int64_t out_hi,
+                                         double* out, void* stream);
+int bd3mg_depthvar_correlate_f32(const float* frag, int64_t nzf, int64_t ny, int64_t nx, const float* kernels,
+                                 int64_t nzk, int64_t kz, int64_t ky, int64_t kx, int64_t frag_z0,
+                                 int64_t out_lo, int64_t out_hi, float* out, void* stream);
+int bd3mg_depthvar_correlate_adjoint_f32(const float* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                         const float* kernels, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                                         int64_t frag_z0, int64_t out_lo, int64_t out_hi, float* out,
+                                         void* stream);
+/* Host-buffer twins with the exact contract of the Cython functions: the
+ * callee computes into `out` (caller-allocated, zero-initialised semantics
+ * not required).  Synchronous. */
+int bd3mg_depthvar_correlate_host_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                      const double* kernels, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                                      int64_t frag_z0, int64_t out_lo, int64_t out_hi, double* out);
+int bd3mg_depthvar_correlate_adjoint_host_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                              const double* kernels, int64_t nzk, int64_t kz, int64_t ky,
+                                              int64_t kx, int64_t frag_z0, int64_t out_lo, int64_t out_hi,
+                                              double* out);
+
+/* ---- fused objective operators (device pointers, async) ---------------- */
+/* Gradient rows [lo, hi] from a fragment: reference objective.py:159-187
+ * (_grad_rows).  frag must cover [lo-1, hi+1] (clamped); rows of H are
+ * read with zero padding outside it.  Also writes the half-quadratic
+ * weights omega of rows [lo, hi] (objective.py:130-132). */
+size_t bd3mg_grad_rows_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi);
+int bd3mg_grad_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                    const void* frag, int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, void* g_out,
+                    void* omega_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Full objective value and stop-rule norms: objective.py:140-156 (eval_f),
+ * scheduler.py:218-219.  snap may be NULL.  terms_out: device, 7 doubles. */
+size_t bd3mg_eval_f_ws_bytes(const bd3mg_geom_t* g);
+int bd3mg_eval_f(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                 const void* x, const void* snap, double* terms_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Half-quadratic weights 1/sqrt(dx^2+dy^2+delta^2) of rows [lo, hi] of a
+ * fragment: objective.py:130-132 (_omega), as cached by MajorantOperator
+ * (objective.py:233-235).  omega_out: (hi-lo+1, ny, nx). */
+int bd3mg_omega_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* frag, int64_t frag_z0, int64_t nzf,
+                     int64_t lo, int64_t hi, void* omega_out, void* stream);
+
+/* A_S(x~) v for block [lo, hi]: objective.py:245-275 (MajorantOperator.apply),
+ * omega = block rows of the anchor's weights. */
+size_t bd3mg_majorant_apply_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi);
+int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* omega,
+                         const void* v, int64_t lo, int64_t hi, void* out, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* Batched memory-gradient block steps (mg_direction + receive_update) with
+ * the forward-only Gram.  Tasks sharing one anchor fragment compute the
+ * residual H x - y once over the union of their rows (block-Jacobi cycle of
+ * run_bp3mg_barrier, runtime.py:244-292).  info_out: device, ntasks*16. */
+size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks);
+int bd3mg_mg_steps(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                   const bd3mg_task_t* tasks, int ntasks, double* info_out, void* ws, size_t ws_bytes,
+                   void* stream);
+
+/* receive_update's block write (scheduler.py:151-153): x_rows += inc and,
+ * when dmem_rows is not NULL, dmem_rows = inc; n elements of `dtype`. */
+int bd3mg_apply_increment(int32_t dtype, void* x_rows, void* dmem_rows, const void* inc, int64_t n, void* stream);
+
+/* ---- host-buffer problem handle (worker-task boundary of the reference:
+ * TaskMessage -> UpdateMessage, scheduler.py:36-57, runtime.py:92-105) ---- */
+typedef struct bd3mg_problem bd3mg_problem;
+/* kernels/y are host float64 arrays; dtype selects the device arithmetic. */
+int bd3mg_problem_create(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const double* kernels_host,
+                         const double* y_host, int device, bd3mg_problem** out);
+int bd3mg_problem_destroy(bd3mg_problem* p);
+/* mg_direction(obj, x_slab, slab_z0, block, d_mem) with host float64 buffers:
+ * x_slab (nzs, ny, nx), d_mem block rows or NULL, inc_out block rows,
+ * info_out 16 doubles (may be NULL).  Returns BD3MG_ENONFINITE on a
+ * non-finite gradient. */
+int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int64_t slab_z0, int64_t nzs,
+                                    int64_t z_lo, int64_t z_hi, const double* d_mem, double* inc_out,
+                                    double* info_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BD3MG_B200_H */

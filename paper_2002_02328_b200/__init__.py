@@ -1,0 +1,8 @@
+"""B200-native BD3MG hot path (arXiv 2002.02328): depth-variant blur H/H^T,
+fused gradient, forward-only 2x2 memory-gradient Gram, device subspace solve
+and block update as sm_100a CUDA kernels behind a C ABI
+(include/bd3mg_b200.h), with the reference package's operator and solver
+entry points kept as a drop-in (blur, objective, directions, scheduler,
+runtime)."""
+
+__version__ = "0.1.0"

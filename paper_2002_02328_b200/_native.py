@@ -1,0 +1,113 @@
+"""ctypes binding of the C ABI in ``include/bd3mg_b200.h``.
+
+The library is the only compute backend: if it is missing this module raises
+at import time (there is no CPU fallback on the product path).  Build it with
+``python -m paper_2002_02328_b200.build`` or ``__graft_entry__.build()``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbd3mg_b200.so"
+
+BD3MG_OK, BD3MG_EINVAL, BD3MG_ECUDA, BD3MG_EWORKSPACE, BD3MG_ENONFINITE = range(5)
+BD3MG_F64, BD3MG_F32 = 0, 1
+INFO_DOUBLES = 16
+EVAL_DOUBLES = 7
+
+# every symbol the header declares (checked by tests/test_capi_symbols.py)
+EXPORTS = (
+    "bd3mg_last_error", "bd3mg_version",
+    "bd3mg_depthvar_correlate_f64", "bd3mg_depthvar_correlate_adjoint_f64",
+    "bd3mg_depthvar_correlate_f32", "bd3mg_depthvar_correlate_adjoint_f32",
+    "bd3mg_depthvar_correlate_host_f64", "bd3mg_depthvar_correlate_adjoint_host_f64",
+    "bd3mg_grad_rows_ws_bytes", "bd3mg_grad_rows",
+    "bd3mg_eval_f_ws_bytes", "bd3mg_eval_f",
+    "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
+    "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
+    "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
+)
+
+
+class Geom(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+                ("kx", C.c_int32), ("ky", C.c_int32), ("kz", C.c_int32), ("dtype", C.c_int32)]
+
+
+class Reg(C.Structure):
+    _fields_ = [("lam", C.c_double), ("eta", C.c_double), ("kappa", C.c_double),
+                ("delta", C.c_double), ("x_min", C.c_double), ("x_max", C.c_double)]
+
+
+class Task(C.Structure):
+    _fields_ = [("frag", C.c_void_p), ("frag_z0", C.c_int64), ("nzf", C.c_int64),
+                ("z_lo", C.c_int64), ("z_hi", C.c_int64), ("d_mem", C.c_void_p),
+                ("inc_out", C.c_void_p), ("x_rows", C.c_void_p), ("dmem_rows", C.c_void_p)]
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[bd3mg_b200 status {code}] {msg}")
+        self.code = code
+
+
+_i64, _vp, _dp, _sz = C.c_int64, C.c_void_p, C.POINTER(C.c_double), C.c_size_t
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"CUDA library {LIB_PATH} is not built; run `python -m paper_2002_02328_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
+    corr = [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp]
+    for name in ("bd3mg_depthvar_correlate_f64", "bd3mg_depthvar_correlate_adjoint_f64",
+                 "bd3mg_depthvar_correlate_f32", "bd3mg_depthvar_correlate_adjoint_f32"):
+        getattr(lib, name).argtypes = corr + [_vp]
+    for name in ("bd3mg_depthvar_correlate_host_f64", "bd3mg_depthvar_correlate_adjoint_host_f64"):
+        getattr(lib, name).argtypes = corr
+    G, R, T = C.POINTER(Geom), C.POINTER(Reg), C.POINTER(Task)
+    lib.bd3mg_last_error.restype = C.c_char_p
+    lib.bd3mg_version.restype = C.c_char_p
+    lib.bd3mg_grad_rows_ws_bytes.argtypes = [G, _i64, _i64]
+    lib.bd3mg_grad_rows_ws_bytes.restype = _sz
+    lib.bd3mg_grad_rows.argtypes = [G, R, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]
+    lib.bd3mg_eval_f_ws_bytes.argtypes = [G]
+    lib.bd3mg_eval_f_ws_bytes.restype = _sz
+    lib.bd3mg_eval_f.argtypes = [G, R, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.bd3mg_omega_rows.argtypes = [G, R, _vp, _i64, _i64, _i64, _i64, _vp, _vp]
+    lib.bd3mg_majorant_apply_ws_bytes.argtypes = [G, _i64, _i64]
+    lib.bd3mg_majorant_apply_ws_bytes.restype = _sz
+    lib.bd3mg_majorant_apply.argtypes = [G, R, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp]
+    lib.bd3mg_mg_steps_ws_bytes.argtypes = [G, T, C.c_int]
+    lib.bd3mg_mg_steps_ws_bytes.restype = _sz
+    lib.bd3mg_mg_steps.argtypes = [G, R, _vp, _vp, T, C.c_int, _vp, _vp, _sz, _vp]
+    lib.bd3mg_apply_increment.argtypes = [C.c_int32, _vp, _vp, _vp, _i64, _vp]
+    lib.bd3mg_problem_create.argtypes = [G, R, _vp, _vp, C.c_int, C.POINTER(C.c_void_p)]
+    lib.bd3mg_problem_destroy.argtypes = [_vp]
+    lib.bd3mg_problem_mg_direction_host.argtypes = [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    """Map a status to the reference's exception types."""
+    if rc == BD3MG_OK:
+        return
+    msg = (lib.bd3mg_last_error() or b"").decode()
+    if rc == BD3MG_EINVAL:
+        raise ValueError(msg)
+    if rc == BD3MG_ENONFINITE:
+        raise ValueError("non-finite gradient")
+    raise NativeError(rc, msg)
+
+
+def ws_bytes(n: int) -> int:
+    if n == C.c_size_t(-1).value:
+        check(BD3MG_EINVAL)
+    return n

@@ -1,0 +1,795 @@
+// C ABI of the B200-native BD3MG hot path (declarations: include/bd3mg_b200.h).
+//
+// Orchestrates the kernels of depthvar.cuh / solver.cuh into the reference
+// operators: H/H^T rows (_core.pyx), _grad_rows / eval_f /
+// MajorantOperator.apply (objective.py), mg_direction (directions.py) and the
+// block update of receive_update (scheduler.py).
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bd3mg_b200.h"
+#include "conv_dispatch.cuh"
+#include "solver.cuh"
+
+using namespace bd3mg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e__ = (expr);                                                                 \
+    if (e__ != cudaSuccess) return fail(BD3MG_ECUDA, "%s: %s", #expr, cudaGetErrorString(e__)); \
+  } while (0)
+
+constexpr double kPruneTol = 1e-14;  // directions.py:19
+constexpr double kPinvTol = 1e-12;   // directions.py:22
+
+// Bump allocator over a caller workspace; measure mode sizes it.
+struct Ws {
+  char* base = nullptr;
+  size_t cap = 0, off = 0;
+  bool measure = true;
+  template <typename U>
+  U* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    U* p = measure ? nullptr : reinterpret_cast<U*>(base + off);
+    off += n * sizeof(U);
+    return p;
+  }
+  bool ok() const { return measure || off <= cap; }
+};
+
+bool odd_pos(int64_t k) { return k >= 1 && (k % 2) == 1; }
+
+int check_geom(const bd3mg_geom_t* g) {
+  if (!g) return fail(BD3MG_EINVAL, "null geometry");
+  if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(BD3MG_EINVAL, "dimensions must be >= 1");
+  if (!odd_pos(g->kx) || !odd_pos(g->ky) || !odd_pos(g->kz)) return fail(BD3MG_EINVAL, "kernel dims must be odd and >= 1");
+  if (g->dtype != BD3MG_F64 && g->dtype != BD3MG_F32) return fail(BD3MG_EINVAL, "unknown dtype %d", g->dtype);
+  if (g->nx * g->ny > (int64_t)1 << 31) return fail(BD3MG_EINVAL, "plane too large");
+  return BD3MG_OK;
+}
+
+template <typename T>
+ConvArgs<T> base_args(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K) {
+  ConvArgs<T> a;
+  memset(&a, 0, sizeof(a));
+  a.K = K;
+  a.nzk = (int)g->nz;
+  a.kz = g->kz; a.ky = g->ky; a.kx = g->kx;
+  a.ny = (int)g->ny; a.nx = (int)g->nx;
+  a.plane = g->ny * g->nx;
+  a.nz_global = (int)g->nz;
+  if (r) {
+    a.two_eta = 2.0 * r->eta;
+    a.lam = r->lam;
+    a.two_kappa = 2.0 * r->kappa;
+    a.delta2 = r->delta * r->delta;
+    a.x_min = r->x_min;
+    a.x_max = r->x_max;
+  }
+  return a;
+}
+
+template <typename T>
+long long conv_rows(const bd3mg_geom_t* g, int mode, long long work) {
+  const ConvGrid cg = conv_grid<T>(g->ky, g->kx, mode, (int)g->ny, (int)g->nx);
+  return work * cg.tiles_x * cg.tiles_y;
+}
+
+cudaError_t reduce(const double* rows, int nv, const std::vector<std::pair<long long, long long>>& ranges,
+                   double* out, int out_stride, cudaStream_t s) {
+  for (size_t b0 = 0; b0 < ranges.size(); b0 += kMaxJobs) {
+    RowRanges rr;
+    memset(&rr, 0, sizeof(rr));
+    rr.njobs = (int)std::min<size_t>(kMaxJobs, ranges.size() - b0);
+    for (int j = 0; j < rr.njobs; ++j) {
+      rr.begin[j] = ranges[b0 + j].first;
+      rr.end[j] = ranges[b0 + j].second;
+    }
+    reduce_rows_kernel<<<rr.njobs, kEwNT, 0, s>>>(rows, nv, rr, out + b0 * out_stride, out_stride);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+int correlate_rows(const T* frag, int64_t nzf, int64_t ny, int64_t nx, const T* K, int64_t nzk, int64_t kz,
+                   int64_t ky, int64_t kx, int64_t frag_z0, int64_t out_lo, int64_t out_hi, T* out, bool adj,
+                   cudaStream_t s) {
+  if (!odd_pos(kz) || !odd_pos(ky) || !odd_pos(kx)) return fail(BD3MG_EINVAL, "kernel dims must be odd and >= 1");
+  if (ny < 1 || nx < 1 || nzf < 1 || nzk < 1) return fail(BD3MG_EINVAL, "empty fragment or kernel stack");
+  const int64_t nout = out_hi - out_lo + 1;
+  if (nout < 0) return fail(BD3MG_EINVAL, "out_hi < out_lo - 1");
+  if (nout == 0) return BD3MG_OK;
+  if (out_lo < 0) return fail(BD3MG_EINVAL, "out_lo < 0");
+  if (!adj && out_hi >= nzk) return fail(BD3MG_EINVAL, "output row %lld outside the kernel stack (nz=%lld)",
+                                         (long long)out_hi, (long long)nzk);
+  bd3mg_geom_t g{nx, ny, nzk, (int32_t)kx, (int32_t)ky, (int32_t)kz, 0};
+  ConvArgs<T> a = base_args<T>(&g, nullptr, K);
+  a.njobs = 1;
+  ConvJob<T>& j = a.jobs[0];
+  j.src0 = frag; j.src_z0 = frag_z0; j.src_nz = (int)nzf;
+  j.dst0 = out; j.out_lo = (int)out_lo; j.nout = (int)nout; j.work_begin = 0;
+  CU(conv_launch<T>(M_STORE, adj, a, (int)nout, s));
+  return BD3MG_OK;
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const T* frag,
+                   int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, T* g_out, T* omega_out, Ws& ws,
+                   cudaStream_t s) {
+  const int64_t nz = g->nz, plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
+  if (lo < 0 || hi < lo || hi >= nz) return fail(BD3MG_EINVAL, "invalid rows [%lld, %lld]", (long long)lo, (long long)hi);
+  const int64_t need_lo = std::max<int64_t>(0, lo - 1), need_hi = std::min<int64_t>(nz - 1, hi + 1);
+  if (frag_z0 > need_lo || frag_z0 + nzf - 1 < need_hi)
+    return fail(BD3MG_EINVAL, "fragment [%lld, %lld] does not cover the stencil rows [%lld, %lld]",
+                (long long)frag_z0, (long long)(frag_z0 + nzf - 1), (long long)need_lo, (long long)need_hi);
+  const int64_t o_lo = std::max<int64_t>(0, lo - rz), o_hi = std::min<int64_t>(nz - 1, hi + rz);
+  const int64_t nr = o_hi - o_lo + 1, h = hi - lo + 1;
+  T* rbuf = ws.take<T>(nr * plane);
+  double* parts = ws.take<double>(conv_rows<T>(g, M_RESID, nr));
+  if (ws.measure) return BD3MG_OK;
+  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  ConvArgs<T> a = base_args<T>(g, r, K);
+  a.njobs = 1;
+  a.partials = parts;
+  a.jobs[0].src0 = frag; a.jobs[0].src_z0 = frag_z0; a.jobs[0].src_nz = (int)nzf;
+  a.jobs[0].dst0 = rbuf; a.jobs[0].sub = y + o_lo * plane;
+  a.jobs[0].out_lo = (int)o_lo; a.jobs[0].nout = (int)nr;
+  CU(conv_launch<T>(M_RESID, false, a, (int)nr, s));
+  ConvArgs<T> b = base_args<T>(g, r, K);
+  b.njobs = 1;
+  ConvJob<T>& j = b.jobs[0];
+  j.src0 = rbuf; j.src_z0 = o_lo; j.src_nz = (int)nr;
+  j.dst0 = g_out; j.omega = omega_out;
+  j.xg = frag; j.xg_z0 = frag_z0; j.xg_nz = (int)nzf;
+  j.out_lo = (int)lo; j.nout = (int)h;
+  CU(conv_launch<T>(M_GRAD, true, b, (int)h, s));
+  return BD3MG_OK;
+}
+
+template <typename T>
+int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const T* x, const T* snap,
+                double* terms, Ws& ws, cudaStream_t s) {
+  const int64_t nz = g->nz, plane = g->ny * g->nx, n = nz * plane;
+  const long long crow = conv_rows<T>(g, M_RESID, nz);
+  double* parts = ws.take<double>(crow);
+  const int ctas = (int)std::min<int64_t>((n + kEwNT - 1) / kEwNT, 4 * 148);
+  double* eparts = ws.take<double>((size_t)ctas * kEvalNV);
+  double* sums = ws.take<double>(8);
+  if (ws.measure) return BD3MG_OK;
+  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  ConvArgs<T> a = base_args<T>(g, r, K);
+  a.njobs = 1;
+  a.partials = parts;
+  a.jobs[0].src0 = x; a.jobs[0].src_z0 = 0; a.jobs[0].src_nz = (int)nz;
+  a.jobs[0].dst0 = nullptr; a.jobs[0].sub = y;
+  a.jobs[0].out_lo = 0; a.jobs[0].nout = (int)nz;
+  CU(conv_launch<T>(M_RESID, false, a, (int)nz, s));
+  CU(reduce(parts, 1, {{0, crow}}, sums, 1, s));
+  EvalArgs<T> e;
+  e.x = x; e.snap = snap; e.nz = (int)nz; e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane; e.n = n;
+  e.delta2 = r->delta * r->delta; e.x_min = r->x_min; e.x_max = r->x_max; e.ctas = ctas;
+  eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts);
+  CU(cudaGetLastError());
+  CU(reduce(eparts, kEvalNV, {{0, ctas}}, sums + 1, kEvalNV, s));
+  eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms);
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+template <typename T>
+int majorant_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* omega, const T* v, int64_t lo,
+                  int64_t hi, T* out, Ws& ws, cudaStream_t s) {
+  const int64_t nz = g->nz, plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
+  if (lo < 0 || hi < lo || hi >= nz) return fail(BD3MG_EINVAL, "invalid block [%lld, %lld]", (long long)lo, (long long)hi);
+  const int64_t o_lo = std::max<int64_t>(0, lo - rz), o_hi = std::min<int64_t>(nz - 1, hi + rz);
+  const int64_t nr = o_hi - o_lo + 1, h = hi - lo + 1;
+  T* hv = ws.take<T>(nr * plane);
+  if (ws.measure) return BD3MG_OK;
+  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  ConvArgs<T> a = base_args<T>(g, r, K);
+  a.njobs = 1;
+  a.jobs[0].src0 = v; a.jobs[0].src_z0 = lo; a.jobs[0].src_nz = (int)h;
+  a.jobs[0].dst0 = hv; a.jobs[0].out_lo = (int)o_lo; a.jobs[0].nout = (int)nr;
+  CU(conv_launch<T>(M_STORE, false, a, (int)nr, s));
+  ConvArgs<T> b = base_args<T>(g, r, K);
+  b.njobs = 1;
+  b.jobs[0].src0 = hv; b.jobs[0].src_z0 = o_lo; b.jobs[0].src_nz = (int)nr;
+  b.jobs[0].dst0 = out; b.jobs[0].out_lo = (int)lo; b.jobs[0].nout = (int)h;
+  CU(conv_launch<T>(M_STORE, true, b, (int)h, s));
+  MajArgs<T> m;
+  m.v = v; m.omega = omega; m.out = out; m.lo = (int)lo; m.hi = (int)hi; m.nz = (int)nz;
+  m.ny = (int)g->ny; m.nx = (int)g->nx; m.plane = plane; m.n = h * plane;
+  m.two_eta = 2.0 * r->eta; m.lam = r->lam; m.two_kappa = 2.0 * r->kappa;
+  majorant_reg_kernel<T><<<(unsigned)((m.n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(m);
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+template <typename T>
+int omega_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* frag, int64_t frag_z0, int64_t nzf, int64_t lo,
+               int64_t hi, T* out, cudaStream_t s) {
+  if (lo < 0 || hi < lo || hi >= g->nz) return fail(BD3MG_EINVAL, "invalid rows [%lld, %lld]", (long long)lo, (long long)hi);
+  if (frag_z0 > lo || frag_z0 + nzf - 1 < hi) return fail(BD3MG_EINVAL, "fragment does not cover the rows");
+  const int64_t plane = g->ny * g->nx, n = (hi - lo + 1) * plane;
+  XView<T> xv{frag, frag_z0, (int)nzf, (int)g->ny, (int)g->nx, plane};
+  omega_kernel<T><<<(unsigned)((n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(xv, (int)lo, n, (T)(r->delta * r->delta), out);
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Batched mg_direction (+ optional in-place receive_update).
+template <typename T>
+int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
+                   int nt, double* info_out, Ws& ws, cudaStream_t s) {
+  const int64_t nz = g->nz, plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
+  std::vector<int64_t> olo(nt), ohi(nt), h(nt);
+  bool shared = true, any_d = false;
+  for (int t = 0; t < nt; ++t) {
+    const bd3mg_task_t& k = tasks[t];
+    if (k.z_lo < 0 || k.z_hi < k.z_lo || k.z_hi >= nz)
+      return fail(BD3MG_EINVAL, "invalid block [%lld, %lld]", (long long)k.z_lo, (long long)k.z_hi);
+    const int64_t s_lo = std::max<int64_t>(0, k.z_lo - g->kz), s_hi = std::min<int64_t>(nz - 1, k.z_hi + g->kz);
+    if (k.frag_z0 > s_lo || k.frag_z0 + k.nzf - 1 < s_hi)
+      return fail(BD3MG_EINVAL, "slab [%lld, %lld] does not cover the required support [%lld, %lld] of block [%lld, %lld]",
+                  (long long)k.frag_z0, (long long)(k.frag_z0 + k.nzf - 1), (long long)s_lo, (long long)s_hi,
+                  (long long)k.z_lo, (long long)k.z_hi);
+    olo[t] = std::max<int64_t>(0, k.z_lo - rz);
+    ohi[t] = std::min<int64_t>(nz - 1, k.z_hi + rz);
+    h[t] = k.z_hi - k.z_lo + 1;
+    if (k.frag != tasks[0].frag || k.frag_z0 != tasks[0].frag_z0 || k.nzf != tasks[0].nzf) shared = false;
+    if (k.d_mem) any_d = true;
+  }
+  // residual rows: union (shared anchor) or per task
+  std::vector<T*> rb(nt);
+  std::vector<int64_t> r_z0(nt), r_n(nt);
+  long long resid_work = 0;
+  int64_t u_lo = 0, u_hi = -1;
+  if (shared) {
+    u_lo = *std::min_element(olo.begin(), olo.end());
+    u_hi = *std::max_element(ohi.begin(), ohi.end());
+    T* ru = ws.take<T>((u_hi - u_lo + 1) * plane);
+    for (int t = 0; t < nt; ++t) { rb[t] = ru; r_z0[t] = u_lo; r_n[t] = u_hi - u_lo + 1; }
+    resid_work = u_hi - u_lo + 1;
+  } else {
+    for (int t = 0; t < nt; ++t) {
+      rb[t] = ws.take<T>((ohi[t] - olo[t] + 1) * plane);
+      r_z0[t] = olo[t]; r_n[t] = ohi[t] - olo[t] + 1;
+      resid_work += r_n[t];
+    }
+  }
+  std::vector<T*> gb(nt), wb(nt);
+  for (int t = 0; t < nt; ++t) { gb[t] = ws.take<T>(h[t] * plane); wb[t] = ws.take<T>(h[t] * plane); }
+  long long gram_work = 0;
+  for (int t = 0; t < nt; ++t) gram_work += ohi[t] - olo[t] + 1;
+  const int gmode = any_d ? M_GRAM2 : M_GRAM1;
+  const long long conv_part_rows = std::max(conv_rows<T>(g, M_RESID, resid_work), conv_rows<T>(g, gmode, gram_work));
+  double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
+  // reg partials: ctas per task proportional to block size, capped
+  std::vector<int> rctas(nt);
+  long long reg_rows = 0;
+  int max_ctas = 1;
+  for (int t = 0; t < nt; ++t) {
+    rctas[t] = (int)std::max<int64_t>(1, std::min<int64_t>((h[t] * plane + 4 * kEwNT - 1) / (4 * kEwNT), 256));
+    reg_rows += rctas[t];
+    max_ctas = std::max(max_ctas, rctas[t]);
+  }
+  double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
+  double* data3 = ws.take<double>((size_t)nt * 3);
+  double* reg12 = ws.take<double>((size_t)nt * kRegNV);
+  if (ws.measure) return BD3MG_OK;
+  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+
+  // (1) r = H x - y
+  {
+    ConvArgs<T> a = base_args<T>(g, r, K);
+    a.partials = cparts;
+    if (shared) {
+      a.njobs = 1;
+      ConvJob<T>& j = a.jobs[0];
+      j.src0 = (const T*)tasks[0].frag; j.src_z0 = tasks[0].frag_z0; j.src_nz = (int)tasks[0].nzf;
+      j.dst0 = rb[0]; j.sub = y + u_lo * plane; j.out_lo = (int)u_lo; j.nout = (int)(u_hi - u_lo + 1);
+    } else {
+      a.njobs = nt;
+      int wbeg = 0;
+      for (int t = 0; t < nt; ++t) {
+        ConvJob<T>& j = a.jobs[t];
+        j.src0 = (const T*)tasks[t].frag; j.src_z0 = tasks[t].frag_z0; j.src_nz = (int)tasks[t].nzf;
+        j.dst0 = rb[t]; j.sub = y + olo[t] * plane; j.out_lo = (int)olo[t]; j.nout = (int)r_n[t];
+        j.work_begin = wbeg;
+        wbeg += (int)r_n[t];
+      }
+    }
+    CU(conv_launch<T>(M_RESID, false, a, (int)resid_work, s));
+  }
+  // (2) g = H^T r + regulariser gradient; omega
+  {
+    ConvArgs<T> a = base_args<T>(g, r, K);
+    a.njobs = nt;
+    int wbeg = 0;
+    for (int t = 0; t < nt; ++t) {
+      ConvJob<T>& j = a.jobs[t];
+      j.src0 = rb[t]; j.src_z0 = r_z0[t]; j.src_nz = (int)r_n[t];
+      j.dst0 = gb[t]; j.omega = wb[t];
+      j.xg = (const T*)tasks[t].frag; j.xg_z0 = tasks[t].frag_z0; j.xg_nz = (int)tasks[t].nzf;
+      j.out_lo = (int)tasks[t].z_lo; j.nout = (int)h[t]; j.work_begin = wbeg;
+      wbeg += (int)h[t];
+    }
+    long long work = 0;
+    for (int t = 0; t < nt; ++t) work += h[t];
+    CU(conv_launch<T>(M_GRAD, true, a, (int)work, s));
+  }
+  // (3) regulariser Gram terms + rhs + flags
+  {
+    RegArgs<T> ra;
+    memset(&ra, 0, sizeof(ra));
+    ra.ny = (int)g->ny; ra.nx = (int)g->nx; ra.nz = (int)nz; ra.plane = plane; ra.nblocks = nt;
+    long long rb0 = 0;
+    for (int t = 0; t < nt; ++t) {
+      RegBlock<T>& B = ra.blk[t];
+      B.g = gb[t]; B.d = (const T*)tasks[t].d_mem; B.omega = wb[t];
+      B.lo = (int)tasks[t].z_lo; B.hi = (int)tasks[t].z_hi; B.ctas = rctas[t]; B.row_begin = rb0;
+      rb0 += rctas[t];
+    }
+    reg_gram_kernel<T><<<dim3(max_ctas, nt), kEwNT, 0, s>>>(ra, rparts);
+    CU(cudaGetLastError());
+  }
+  // (4) data Gram <H b_i, H b_j> (forward only, both columns share the taps)
+  std::vector<std::pair<long long, long long>> granges(nt);
+  {
+    ConvArgs<T> a = base_args<T>(g, r, K);
+    a.njobs = nt;
+    a.partials = cparts;
+    int wbeg = 0;
+    const long long tiles = conv_rows<T>(g, gmode, 1);
+    for (int t = 0; t < nt; ++t) {
+      ConvJob<T>& j = a.jobs[t];
+      j.src0 = gb[t];
+      j.src1 = tasks[t].d_mem ? (const T*)tasks[t].d_mem : gb[t];
+      j.src_z0 = tasks[t].z_lo; j.src_nz = (int)h[t];
+      j.out_lo = (int)olo[t]; j.nout = (int)(ohi[t] - olo[t] + 1); j.work_begin = wbeg;
+      granges[t] = {(long long)wbeg * tiles, (long long)(wbeg + j.nout) * tiles};
+      wbeg += j.nout;
+    }
+    CU(conv_launch<T>(gmode, false, a, (int)gram_work, s));
+  }
+  // (5) reductions
+  CU(reduce(cparts, any_d ? 3 : 1, granges, data3, 3, s));
+  {
+    std::vector<std::pair<long long, long long>> rr(nt);
+    long long b0 = 0;
+    for (int t = 0; t < nt; ++t) { rr[t] = {b0, b0 + rctas[t]}; b0 += rctas[t]; }
+    CU(reduce(rparts, kRegNV, rr, reg12, kRegNV, s));
+  }
+  // (6) 2x2 solves
+  {
+    SolveArgs sa;
+    memset(&sa, 0, sizeof(sa));
+    sa.nblocks = nt;
+    sa.two_eta = 2.0 * r->eta; sa.lam = r->lam; sa.two_kappa = 2.0 * r->kappa;
+    sa.prune_tol = kPruneTol; sa.pinv_tol = kPinvTol;
+    for (int t = 0; t < nt; ++t) sa.has_d[t] = tasks[t].d_mem != nullptr;
+    solve2x2_kernel<<<1, 32, 0, s>>>(sa, data3, reg12, info_out);
+    CU(cudaGetLastError());
+  }
+  // (7) increments / in-place update
+  {
+    UpdArgs<T> ua;
+    memset(&ua, 0, sizeof(ua));
+    ua.nblocks = nt;
+    int mc = 1;
+    for (int t = 0; t < nt; ++t) {
+      UpdBlock<T>& B = ua.blk[t];
+      B.g = gb[t]; B.d = (const T*)tasks[t].d_mem; B.inc_out = (T*)tasks[t].inc_out;
+      B.x = (T*)tasks[t].x_rows; B.dmem = (T*)tasks[t].dmem_rows;
+      B.n = h[t] * plane;
+      B.ctas = (int)std::max<int64_t>(1, std::min<int64_t>((B.n + 4 * kEwNT - 1) / (4 * kEwNT), 1024));
+      mc = std::max(mc, B.ctas);
+    }
+    update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, info_out);
+    CU(cudaGetLastError());
+  }
+  return BD3MG_OK;
+}
+
+template <typename T>
+int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
+                  int ntasks, double* info_out, Ws& ws, cudaStream_t s) {
+  if (ntasks < 0) return fail(BD3MG_EINVAL, "negative task count");
+  size_t peak = 0;
+  for (int t0 = 0; t0 < ntasks; t0 += kMaxJobs) {
+    const int nt = std::min(kMaxJobs, ntasks - t0);
+    Ws sub = ws;
+    sub.off = 0;
+    if (!ws.measure) { sub.base = ws.base; sub.cap = ws.cap; }
+    int rc = mg_steps_chunk<T>(g, r, K, y, tasks + t0, nt, info_out ? info_out + (size_t)t0 * kInfoNV : nullptr,
+                               sub, s);
+    if (rc != BD3MG_OK) return rc;
+    peak = std::max(peak, sub.off);
+  }
+  ws.off = std::max(ws.off, peak);
+  return BD3MG_OK;
+}
+
+template <typename F>
+size_t measure(F&& f) {
+  Ws ws;
+  ws.measure = true;
+  if (f(ws) != BD3MG_OK) return (size_t)-1;
+  return ws.off + 256;
+}
+
+Ws make_ws(void* p, size_t n) {
+  Ws ws;
+  ws.base = (char*)p;
+  ws.cap = n;
+  ws.measure = false;
+  return ws;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* bd3mg_last_error(void) { return g_err.c_str(); }
+const char* bd3mg_version(void) { return "bd3mg_b200 0.1 sm_100a"; }
+
+int bd3mg_depthvar_correlate_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx, const double* kernels,
+                                 int64_t nzk, int64_t kz, int64_t ky, int64_t kx, int64_t frag_z0, int64_t out_lo,
+                                 int64_t out_hi, double* out, void* stream) {
+  return correlate_rows<double>(frag, nzf, ny, nx, kernels, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, out, false,
+                                (cudaStream_t)stream);
+}
+int bd3mg_depthvar_correlate_adjoint_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                         const double* kernels, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                                         int64_t frag_z0, int64_t out_lo, int64_t out_hi, double* out,
+                                         void* stream) {
+  return correlate_rows<double>(frag, nzf, ny, nx, kernels, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, out, true,
+                                (cudaStream_t)stream);
+}
+int bd3mg_depthvar_correlate_f32(const float* frag, int64_t nzf, int64_t ny, int64_t nx, const float* kernels,
+                                 int64_t nzk, int64_t kz, int64_t ky, int64_t kx, int64_t frag_z0, int64_t out_lo,
+                                 int64_t out_hi, float* out, void* stream) {
+  return correlate_rows<float>(frag, nzf, ny, nx, kernels, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, out, false,
+                               (cudaStream_t)stream);
+}
+int bd3mg_depthvar_correlate_adjoint_f32(const float* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                         const float* kernels, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                                         int64_t frag_z0, int64_t out_lo, int64_t out_hi, float* out,
+                                         void* stream) {
+  return correlate_rows<float>(frag, nzf, ny, nx, kernels, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, out, true,
+                               (cudaStream_t)stream);
+}
+
+static int correlate_host(const double* frag, int64_t nzf, int64_t ny, int64_t nx, const double* kernels,
+                          int64_t nzk, int64_t kz, int64_t ky, int64_t kx, int64_t frag_z0, int64_t out_lo,
+                          int64_t out_hi, double* out, bool adj) {
+  const int64_t nout = out_hi - out_lo + 1;
+  if (nout <= 0 || nzf < 1 || ny < 1 || nx < 1 || nzk < 1) {
+    return correlate_rows<double>(nullptr, nzf, ny, nx, nullptr, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, nullptr,
+                                  adj, 0);
+  }
+  const size_t nf = (size_t)nzf * ny * nx, nk = (size_t)nzk * kz * ky * kx, no = (size_t)nout * ny * nx;
+  double *df = nullptr, *dk = nullptr, *dout = nullptr;
+  cudaStream_t s;
+  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int rc = BD3MG_OK;
+  do {
+    if (cudaMallocAsync(&df, nf * 8, s) != cudaSuccess || cudaMallocAsync(&dk, nk * 8, s) != cudaSuccess ||
+        cudaMallocAsync(&dout, no * 8, s) != cudaSuccess) {
+      rc = fail(BD3MG_ECUDA, "device allocation failed");
+      break;
+    }
+    if (cudaMemcpyAsync(df, frag, nf * 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(dk, kernels, nk * 8, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      rc = fail(BD3MG_ECUDA, "host-to-device copy failed");
+      break;
+    }
+    rc = correlate_rows<double>(df, nzf, ny, nx, dk, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, dout, adj, s);
+    if (rc != BD3MG_OK) break;
+    if (cudaMemcpyAsync(out, dout, no * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+      rc = fail(BD3MG_ECUDA, "device-to-host copy failed");
+      break;
+    }
+  } while (0);
+  if (df) cudaFreeAsync(df, s);
+  if (dk) cudaFreeAsync(dk, s);
+  if (dout) cudaFreeAsync(dout, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (rc == BD3MG_OK && e != cudaSuccess) rc = fail(BD3MG_ECUDA, "%s", cudaGetErrorString(e));
+  return rc;
+}
+
+int bd3mg_depthvar_correlate_host_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                      const double* kernels, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                                      int64_t frag_z0, int64_t out_lo, int64_t out_hi, double* out) {
+  return correlate_host(frag, nzf, ny, nx, kernels, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, out, false);
+}
+int bd3mg_depthvar_correlate_adjoint_host_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx,
+                                              const double* kernels, int64_t nzk, int64_t kz, int64_t ky,
+                                              int64_t kx, int64_t frag_z0, int64_t out_lo, int64_t out_hi,
+                                              double* out) {
+  return correlate_host(frag, nzf, ny, nx, kernels, nzk, kz, ky, kx, frag_z0, out_lo, out_hi, out, true);
+}
+
+// ---- fused operators ------------------------------------------------------
+#define DISPATCH_T(g, CALL_F64, CALL_F32) ((g)->dtype == BD3MG_F64 ? (CALL_F64) : (CALL_F32))
+
+size_t bd3mg_grad_rows_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g,
+                      grad_rows_impl<double>(g, nullptr, nullptr, nullptr, nullptr, 0, g->nz, lo, hi, nullptr,
+                                             nullptr, ws, 0),
+                      grad_rows_impl<float>(g, nullptr, nullptr, nullptr, nullptr, 0, g->nz, lo, hi, nullptr,
+                                            nullptr, ws, 0));
+  });
+}
+
+int bd3mg_grad_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                    const void* frag, int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, void* g_out,
+                    void* omega_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    grad_rows_impl<double>(g, r, (const double*)kernels, (const double*)y, (const double*)frag,
+                                           frag_z0, nzf, lo, hi, (double*)g_out, (double*)omega_out, ws,
+                                           (cudaStream_t)stream),
+                    grad_rows_impl<float>(g, r, (const float*)kernels, (const float*)y, (const float*)frag, frag_z0,
+                                          nzf, lo, hi, (float*)g_out, (float*)omega_out, ws,
+                                          (cudaStream_t)stream));
+}
+
+size_t bd3mg_eval_f_ws_bytes(const bd3mg_geom_t* g) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, eval_f_impl<double>(g, &r, nullptr, nullptr, nullptr, nullptr, nullptr, ws, 0),
+                      eval_f_impl<float>(g, &r, nullptr, nullptr, nullptr, nullptr, nullptr, ws, 0));
+  });
+}
+
+int bd3mg_eval_f(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y, const void* x,
+                 const void* snap, double* terms_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    eval_f_impl<double>(g, r, (const double*)kernels, (const double*)y, (const double*)x,
+                                        (const double*)snap, terms_out, ws, (cudaStream_t)stream),
+                    eval_f_impl<float>(g, r, (const float*)kernels, (const float*)y, (const float*)x,
+                                       (const float*)snap, terms_out, ws, (cudaStream_t)stream));
+}
+
+int bd3mg_omega_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* frag, int64_t frag_z0, int64_t nzf,
+                     int64_t lo, int64_t hi, void* omega_out, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  return DISPATCH_T(g,
+                    omega_impl<double>(g, r, (const double*)frag, frag_z0, nzf, lo, hi, (double*)omega_out,
+                                       (cudaStream_t)stream),
+                    omega_impl<float>(g, r, (const float*)frag, frag_z0, nzf, lo, hi, (float*)omega_out,
+                                      (cudaStream_t)stream));
+}
+
+int bd3mg_apply_increment(int32_t dtype, void* x_rows, void* dmem_rows, const void* inc, int64_t n, void* stream) {
+  if (n < 0 || !x_rows || !inc) return fail(BD3MG_EINVAL, "invalid increment arguments");
+  if (n == 0) return BD3MG_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + kEwNT - 1) / kEwNT, 4 * 148);
+  if (dtype == BD3MG_F64)
+    apply_increment_kernel<double><<<grid, kEwNT, 0, (cudaStream_t)stream>>>((double*)x_rows, (double*)dmem_rows,
+                                                                            (const double*)inc, n);
+  else if (dtype == BD3MG_F32)
+    apply_increment_kernel<float><<<grid, kEwNT, 0, (cudaStream_t)stream>>>((float*)x_rows, (float*)dmem_rows,
+                                                                           (const float*)inc, n);
+  else
+    return fail(BD3MG_EINVAL, "unknown dtype %d", dtype);
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+size_t bd3mg_majorant_apply_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, majorant_impl<double>(g, &r, nullptr, nullptr, nullptr, lo, hi, nullptr, ws, 0),
+                      majorant_impl<float>(g, &r, nullptr, nullptr, nullptr, lo, hi, nullptr, ws, 0));
+  });
+}
+
+int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* omega,
+                         const void* v, int64_t lo, int64_t hi, void* out, void* wsp, size_t ws_bytes,
+                         void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    majorant_impl<double>(g, r, (const double*)kernels, (const double*)omega, (const double*)v, lo,
+                                          hi, (double*)out, ws, (cudaStream_t)stream),
+                    majorant_impl<float>(g, r, (const float*)kernels, (const float*)omega, (const float*)v, lo, hi,
+                                         (float*)out, ws, (cudaStream_t)stream));
+}
+
+size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, mg_steps_impl<double>(g, &r, nullptr, nullptr, tasks, ntasks, nullptr, ws, 0),
+                      mg_steps_impl<float>(g, &r, nullptr, nullptr, tasks, ntasks, nullptr, ws, 0));
+  });
+}
+
+int bd3mg_mg_steps(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                   const bd3mg_task_t* tasks, int ntasks, double* info_out, void* wsp, size_t ws_bytes,
+                   void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  if (!info_out) return fail(BD3MG_EINVAL, "info_out is required");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    mg_steps_impl<double>(g, r, (const double*)kernels, (const double*)y, tasks, ntasks, info_out,
+                                          ws, (cudaStream_t)stream),
+                    mg_steps_impl<float>(g, r, (const float*)kernels, (const float*)y, tasks, ntasks, info_out, ws,
+                                         (cudaStream_t)stream));
+}
+
+}  // extern "C"
+
+// ---- host-buffer problem handle --------------------------------------------
+namespace {
+__global__ void cvt_kernel_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+__global__ void cvt_kernel_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = (double)a[i];
+}
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t reserve(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  ~DevBuf() { if (p) cudaFree(p); }
+};
+}  // namespace
+
+struct bd3mg_problem {
+  bd3mg_geom_t g;
+  bd3mg_reg_t r;
+  int device;
+  cudaStream_t s;
+  DevBuf K, y, stage, slab, dmem, inc, info, ws;
+};
+
+static int upload_f64(bd3mg_problem* p, const double* host, size_t n, DevBuf& dst) {
+  const size_t esz = p->g.dtype == BD3MG_F64 ? 8 : 4;
+  CU(dst.reserve(n * esz));
+  if (p->g.dtype == BD3MG_F64) {
+    CU(cudaMemcpyAsync(dst.p, host, n * 8, cudaMemcpyHostToDevice, p->s));
+  } else {
+    CU(p->stage.reserve(n * 8));
+    CU(cudaMemcpyAsync(p->stage.p, host, n * 8, cudaMemcpyHostToDevice, p->s));
+    cvt_kernel_f64_to_f32<<<592, 256, 0, p->s>>>((const double*)p->stage.p, (float*)dst.p, (long long)n);
+    CU(cudaGetLastError());
+  }
+  return BD3MG_OK;
+}
+
+extern "C" {
+
+int bd3mg_problem_create(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const double* kernels_host,
+                         const double* y_host, int device, bd3mg_problem** out) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !kernels_host || !y_host || !out) return fail(BD3MG_EINVAL, "null argument");
+  CU(cudaSetDevice(device));
+  bd3mg_problem* p = new bd3mg_problem();
+  p->g = *g;
+  p->r = *r;
+  p->device = device;
+  if (cudaStreamCreateWithFlags(&p->s, cudaStreamNonBlocking) != cudaSuccess) {
+    delete p;
+    return fail(BD3MG_ECUDA, "stream creation failed");
+  }
+  const size_t nk = (size_t)g->nz * g->kz * g->ky * g->kx, nv = (size_t)g->nz * g->ny * g->nx;
+  rc = upload_f64(p, kernels_host, nk, p->K);
+  if (!rc) rc = upload_f64(p, y_host, nv, p->y);
+  if (!rc && cudaStreamSynchronize(p->s) != cudaSuccess) rc = fail(BD3MG_ECUDA, "upload failed");
+  if (rc) {
+    bd3mg_problem_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return BD3MG_OK;
+}
+
+int bd3mg_problem_destroy(bd3mg_problem* p) {
+  if (!p) return BD3MG_OK;
+  cudaSetDevice(p->device);
+  cudaStreamSynchronize(p->s);
+  cudaStreamDestroy(p->s);
+  delete p;
+  return BD3MG_OK;
+}
+
+int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int64_t slab_z0, int64_t nzs,
+                                    int64_t z_lo, int64_t z_hi, const double* d_mem, double* inc_out,
+                                    double* info_out) {
+  if (!p || !x_slab || !inc_out) return fail(BD3MG_EINVAL, "null argument");
+  CU(cudaSetDevice(p->device));
+  const bd3mg_geom_t* g = &p->g;
+  const int64_t plane = g->ny * g->nx, h = z_hi - z_lo + 1;
+  if (h < 1) return fail(BD3MG_EINVAL, "empty block");
+  const size_t esz = g->dtype == BD3MG_F64 ? 8 : 4;
+  int rc = upload_f64(p, x_slab, (size_t)nzs * plane, p->slab);
+  if (rc) return rc;
+  if (d_mem) {
+    rc = upload_f64(p, d_mem, (size_t)h * plane, p->dmem);
+    if (rc) return rc;
+  }
+  CU(p->inc.reserve((size_t)h * plane * esz));
+  CU(p->info.reserve(BD3MG_INFO_DOUBLES * sizeof(double)));
+  bd3mg_task_t t;
+  memset(&t, 0, sizeof(t));
+  t.frag = p->slab.p; t.frag_z0 = slab_z0; t.nzf = nzs; t.z_lo = z_lo; t.z_hi = z_hi;
+  t.d_mem = d_mem ? p->dmem.p : nullptr;
+  t.inc_out = p->inc.p;
+  const size_t wsb = bd3mg_mg_steps_ws_bytes(g, &t, 1);
+  if (wsb == (size_t)-1) return BD3MG_EINVAL;
+  CU(p->ws.reserve(wsb));
+  rc = bd3mg_mg_steps(g, &p->r, p->K.p, p->y.p, &t, 1, (double*)p->info.p, p->ws.p, wsb, p->s);
+  if (rc) return rc;
+  double info[BD3MG_INFO_DOUBLES];
+  if (g->dtype == BD3MG_F64) {
+    CU(cudaMemcpyAsync(inc_out, p->inc.p, (size_t)h * plane * 8, cudaMemcpyDeviceToHost, p->s));
+  } else {
+    CU(p->stage.reserve((size_t)h * plane * 8));
+    cvt_kernel_f32_to_f64<<<592, 256, 0, p->s>>>((const float*)p->inc.p, (double*)p->stage.p, (long long)h * plane);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(inc_out, p->stage.p, (size_t)h * plane * 8, cudaMemcpyDeviceToHost, p->s));
+  }
+  CU(cudaMemcpyAsync(info, p->info.p, sizeof(info), cudaMemcpyDeviceToHost, p->s));
+  CU(cudaStreamSynchronize(p->s));
+  if (info_out) memcpy(info_out, info, sizeof(info));
+  if (info[8] != 0.0) return fail(BD3MG_ENONFINITE, "non-finite gradient");
+  return BD3MG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// Host-side dispatch of the depth-variant correlation kernels: picks the
+// register-tiled instantiation for square ky = kx in {3,5,7,9}, else the
+// generic one-voxel-per-thread kernel.
+#pragma once
+
+#include "depthvar.cuh"
+
+namespace bd3mg {
+
+struct ConvGrid {
+  int tiles_x, tiles_y;
+};
+
+inline bool conv_tiled_shape(int ky, int kx) {
+  return ky == kx && (ky == 3 || ky == 5 || ky == 7 || ky == 9);
+}
+
+template <typename T>
+ConvGrid conv_grid(int ky, int kx, int mode, int ny, int nx) {
+  if (!conv_tiled_shape(ky, kx))
+    return {(nx + kGenericTX - 1) / kGenericTX, (ny + kGenericTY - 1) / kGenericTY};
+  // all tiled configurations share TX; TY depends on dual vs single input
+  constexpr int TX = ConvCfg<T, 3, 3, M_STORE>::TX;
+  const int TY = (mode == M_GRAM2) ? ConvCfg<T, 3, 3, M_GRAM2>::TY : ConvCfg<T, 3, 3, M_STORE>::TY;
+  return {(nx + TX - 1) / TX, (ny + TY - 1) / TY};
+}
+
+// per-device "max dynamic smem" attribute, set once per kernel instantiation
+template <typename Kern>
+inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <typename T, int K, int MODE, bool ADJ>
+cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
+  using Cfg = ConvCfg<T, K, K, MODE>;
+  const size_t sm = Cfg::smem_bytes(p.kz);
+  auto kern = conv_tiled_kernel<T, K, K, MODE, ADJ>;
+  cudaError_t e = ensure_smem_attr(kern, sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.tiles_x, p.tiles_y, total_work);
+  kern<<<grid, Cfg::NT, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int MODE, bool ADJ>
+cudaError_t launch_generic(ConvArgs<T>& p, int total_work, cudaStream_t s) {
+  size_t coef = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
+  const size_t sm = coef + 8 * (kGenericNT / 32) * sizeof(double);
+  auto kern = conv_generic_kernel<T, MODE, ADJ>;
+  cudaError_t e = ensure_smem_attr(kern, sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.tiles_x, p.tiles_y, total_work);
+  kern<<<grid, kGenericNT, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int MODE, bool ADJ>
+cudaError_t launch_mode(ConvArgs<T>& p, int total_work, cudaStream_t s) {
+  if (p.ky == p.kx) {
+    switch (p.ky) {
+      case 3: return launch_tiled<T, 3, MODE, ADJ>(p, total_work, s);
+      case 5: return launch_tiled<T, 5, MODE, ADJ>(p, total_work, s);
+      case 7: return launch_tiled<T, 7, MODE, ADJ>(p, total_work, s);
+      case 9: return launch_tiled<T, 9, MODE, ADJ>(p, total_work, s);
+      default: break;
+    }
+  }
+  return launch_generic<T, MODE, ADJ>(p, total_work, s);
+}
+
+// Fill tiles_{x,y} and launch `mode` over `total_work` output planes.
+template <typename T>
+cudaError_t conv_launch(int mode, bool adj, ConvArgs<T>& p, int total_work, cudaStream_t s);
+
+}  // namespace bd3mg

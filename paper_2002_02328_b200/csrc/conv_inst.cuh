@@ -1,0 +1,31 @@
+// Explicit instantiation body of conv_launch<T>; included once per dtype TU
+// so the large unrolled kernels compile in parallel.
+#pragma once
+
+#include "conv_dispatch.cuh"
+
+namespace bd3mg {
+
+template <typename T>
+cudaError_t conv_launch(int mode, bool adj, ConvArgs<T>& p, int total_work, cudaStream_t s) {
+  if (total_work <= 0) return cudaSuccess;
+  const ConvGrid g = conv_grid<T>(p.ky, p.kx, mode, p.ny, p.nx);
+  p.tiles_x = g.tiles_x;
+  p.tiles_y = g.tiles_y;
+  if (!adj) {
+    switch (mode) {
+      case M_STORE: return launch_mode<T, M_STORE, false>(p, total_work, s);
+      case M_RESID: return launch_mode<T, M_RESID, false>(p, total_work, s);
+      case M_GRAM1: return launch_mode<T, M_GRAM1, false>(p, total_work, s);
+      case M_GRAM2: return launch_mode<T, M_GRAM2, false>(p, total_work, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (mode) {
+    case M_STORE: return launch_mode<T, M_STORE, true>(p, total_work, s);
+    case M_GRAD: return launch_mode<T, M_GRAD, true>(p, total_work, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace bd3mg

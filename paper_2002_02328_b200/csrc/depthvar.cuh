@@ -1,0 +1,422 @@
+// Depth-variant 3-D correlation H and its adjoint H^T for sm_100a, with the
+// fused epilogues of the BD3MG block step.
+//
+// Operator (reference pkg/src/bd3mg/_core.pyx:17-53):
+//   out[zo,y,x] = sum_{a,b,c} K[zo,a,b,c] * frag[zo+a-rz, y+b-ry, x+c-rx]
+// zero outside the fragment / plane.  The adjoint (_core.pyx:56-96) is the
+// same correlation with the per-output coefficient set
+//   Kt[zi,a',b',c'] = K[zi+a'-rz, kz-1-a', ky-1-b', kx-1-c']   (0 if the
+//   source depth zi+a'-rz is outside [0,nzk))
+// which is gathered once per CTA into shared memory, so H and H^T share one
+// FMA loop.
+//
+// Work decomposition: one CTA computes a TY x TX output tile of one output
+// plane.  It walks the kz input planes of that plane; each plane's halo tile
+// (TY+ky-1) x (TX+kx-1) is staged by cp.async (zero-filled outside the
+// fragment/plane, so the FMA loop has no branches) into a double-buffered
+// shared-memory ring.  Each thread owns an RY x RX register tile of
+// accumulators; it streams the RY+ky-1 input rows of its window through
+// registers (RX+kx-1 values per row) and applies every coefficient row that
+// touches them.  Accumulation order per output is a -> b -> c, the reference
+// order, for every fragment offset (so slab and full-volume results are
+// bitwise identical, reference tests/test_blur.py:139-147).
+//
+// Shared-memory row layout is de-interleaved by x mod RX: element e of a row
+// lives at (e % RX) * Q + e / RX.  Thread tx reads element tx*RX + j, i.e.
+// phase j % RX, slot tx + j / RX: consecutive lanes read consecutive words,
+// so every LDS is conflict-free.
+#pragma once
+
+#include "common.cuh"
+
+namespace bd3mg {
+
+enum ConvMode : int {
+  M_STORE = 0,  // dst0 = acc
+  M_RESID = 1,  // dst0 = acc - sub; partial: sum dst0^2
+  M_GRAD = 2,   // (adjoint) dst0 = acc + 2eta*box + lam*tv + 2kappa*axial; omega out
+  M_GRAM1 = 3,  // partial: sum acc0^2               (+ optional store dst0 = acc0)
+  M_GRAM2 = 4,  // partial: acc0^2, acc0*acc1, acc1^2 (dual input, shared taps)
+};
+
+constexpr int kMaxJobs = 32;
+
+template <typename T>
+struct ConvJob {
+  const T* src0;        // fragment base; plane 0 is global depth src_z0
+  const T* src1;        // second fragment (M_GRAM2), same geometry
+  T* dst0;              // output rows; row 0 is global depth out_lo
+  const T* sub;         // M_RESID: rows aligned with dst0
+  const T* xg;          // M_GRAD: iterate fragment (plane 0 = depth xg_z0)
+  T* omega;             // M_GRAD: rows aligned with dst0
+  long long src_z0;
+  long long xg_z0;
+  int src_nz, xg_nz;
+  int out_lo, nout;     // global output rows [out_lo, out_lo+nout)
+  int work_begin;       // prefix of nout over jobs (grid.z index of first plane)
+  int pad_;
+};
+
+template <typename T>
+struct ConvArgs {
+  const T* K;           // (nzk, kz, ky, kx) coefficient stack
+  int nzk, kz, ky, kx;  // runtime kz; ky/kx also template params on fast path
+  int ny, nx;
+  long long plane;      // ny*nx
+  int nz_global;        // global depth (axial far-face rule)
+  int njobs;
+  int tiles_x, tiles_y;
+  double* partials;     // [gridDim.z * tiles_y * tiles_x][NV]
+  double two_eta, lam, two_kappa, delta2, x_min, x_max;
+  ConvJob<T> jobs[kMaxJobs];
+};
+
+template <int MODE>
+struct ModeNV {
+  static constexpr int value = (MODE == M_RESID || MODE == M_GRAM1) ? 1 : (MODE == M_GRAM2 ? 3 : 0);
+};
+
+// ---------------------------------------------------------------------------
+// Regulariser pieces shared by the gradient epilogue and the oracle-mirroring
+// elementwise kernels.  Each mirrors numpy's separate roundings
+// (reference objective.py:87-137).
+template <typename T>
+struct XView {
+  const T* p;          // plane 0 is global depth z0
+  long long z0;
+  int nzv, ny, nx;
+  long long plane;
+  BD3MG_D T at(int z, int y, int x) const { return p[(long long)(z - z0) * plane + (long long)y * nx + x]; }
+};
+
+// forward differences with a zero row at the far face (objective.py:87-98)
+template <typename T>
+BD3MG_D T fdx(const XView<T>& v, int z, int y, int x) {
+  return (x < v.nx - 1) ? sub_rn(v.at(z, y, x + 1), v.at(z, y, x)) : T(0);
+}
+template <typename T>
+BD3MG_D T fdy(const XView<T>& v, int z, int y, int x) {
+  return (y < v.ny - 1) ? sub_rn(v.at(z, y + 1, x), v.at(z, y, x)) : T(0);
+}
+// half-quadratic weight 1/sqrt(dx^2+dy^2+delta^2) (objective.py:130-132)
+template <typename T>
+BD3MG_D T omega_of(T dx, T dy, T delta2) {
+  const T s = add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), delta2);
+  return T(1) / sqrt(s);
+}
+
+// gradient epilogue at one voxel: objective.py:172-186
+template <typename T>
+BD3MG_D T grad_voxel(T hta, const XView<T>& xv, int z, int y, int x, int nz_global, T two_eta, T lam,
+                     T two_kappa, T delta2, T x_min, T x_max, T* omega_out) {
+  const T xc = xv.at(z, y, x);
+  // 2*eta*(x - clip(x))
+  const T clipped = xc < x_min ? x_min : (xc > x_max ? x_max : xc);
+  T g = add_rn(hta, mul_rn(two_eta, sub_rn(xc, clipped)));
+  // lam * (Dx^T(w Dx x) + Dy^T(w Dy x))
+  const T dx0 = fdx(xv, z, y, x), dy0 = fdy(xv, z, y, x);
+  const T w0 = omega_of(dx0, dy0, delta2);
+  *omega_out = w0;
+  const T px0 = mul_rn(w0, dx0), py0 = mul_rn(w0, dy0);
+  T tvx, tvy;
+  if (xv.nx == 1) {
+    tvx = T(0);
+  } else if (x == 0) {
+    tvx = -px0;
+  } else {
+    const T dxm = fdx(xv, z, y, x - 1), dym = fdy(xv, z, y, x - 1);
+    const T pxm = mul_rn(omega_of(dxm, dym, delta2), dxm);
+    tvx = (x == xv.nx - 1) ? pxm : sub_rn(pxm, px0);
+  }
+  if (xv.ny == 1) {
+    tvy = T(0);
+  } else if (y == 0) {
+    tvy = -py0;
+  } else {
+    const T dxm = fdx(xv, z, y - 1, x), dym = fdy(xv, z, y - 1, x);
+    const T pym = mul_rn(omega_of(dxm, dym, delta2), dym);
+    tvy = (y == xv.ny - 1) ? pym : sub_rn(pym, py0);
+  }
+  g = add_rn(g, mul_rn(lam, add_rn(tvx, tvy)));
+  // 2*kappa*(dz[z-1] - dz[z]), dz[t] = x[t+1]-x[t] for 0 <= t < nz-1
+  const T dzm = (z - 1 >= 0 && z - 1 < nz_global - 1) ? sub_rn(xc, xv.at(z - 1, y, x)) : T(0);
+  const T dzp = (z < nz_global - 1) ? sub_rn(xv.at(z + 1, y, x), xc) : T(0);
+  g = add_rn(g, mul_rn(two_kappa, sub_rn(dzm, dzp)));
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int KY_, int KX_, int MODE>
+struct ConvCfg {
+  static constexpr bool DUAL = (MODE == M_GRAM2);
+  static constexpr int KY = KY_, KX = KX_;
+  static constexpr int RX = 4;
+  static constexpr int RY = DUAL ? 4 : 8;
+  static constexpr int WX = 16, WY = 8;
+  static constexpr int NT = WX * WY;
+  static constexpr int TX = WX * RX, TY = WY * RY;
+  static constexpr int TXH = TX + KX - 1, TYH = TY + KY - 1;
+  static constexpr int Q = (TXH + RX - 1) / RX;
+  static constexpr int PITCH = RX * Q;
+  static constexpr int NIN = DUAL ? 2 : 1;
+  static constexpr int TILE = TYH * PITCH;  // elements per input per buffer
+  static constexpr int NV = ModeNV<MODE>::value;
+  static size_t smem_bytes(int kz) {
+    size_t coef = (size_t)kz * KY * KX * sizeof(T);
+    coef = (coef + 15) & ~size_t(15);
+    return coef + 2 * NIN * (size_t)TILE * sizeof(T) + 8 * (NT / 32) * sizeof(double);
+  }
+};
+
+template <typename T>
+BD3MG_D int find_job(const ConvArgs<T>& p, int zidx) {
+  int j = 0;
+  while (j + 1 < p.njobs && p.jobs[j + 1].work_begin <= zidx) ++j;
+  return j;
+}
+
+// Stage the coefficient set of output plane `zo` (adjoint: gathered) into smem.
+template <typename T, bool ADJ>
+BD3MG_D void stage_coefs(const ConvArgs<T>& p, int zo, T* cs, int nt) {
+  const int KYX = p.ky * p.kx, n = p.kz * KYX;
+  const int rz = (p.kz - 1) / 2;
+  for (int i = threadIdx.x; i < n; i += nt) {
+    if (!ADJ) {
+      cs[i] = p.K[(long long)zo * n + i];
+    } else {
+      const int a = i / KYX, rem = i - a * KYX;
+      const int b = rem / p.kx, c = rem - b * p.kx;
+      const int zsrc = zo + a - rz;
+      T v = T(0);
+      if (zsrc >= 0 && zsrc < p.nzk)
+        v = p.K[(long long)zsrc * n + (long long)(p.kz - 1 - a) * KYX + (p.ky - 1 - b) * p.kx + (p.kx - 1 - c)];
+      cs[i] = v;
+    }
+  }
+}
+
+// Load one (TYH x TXH) halo tile of input plane `zi` into de-interleaved smem.
+template <typename Cfg, typename T>
+BD3MG_D void stage_tile(T* dst, const T* src, long long src_z0, int zi, int y0, int x0, int ny, int nx,
+                        long long plane) {
+  constexpr int RYH = (Cfg::KY - 1) / 2, RXH = (Cfg::KX - 1) / 2;
+  const T* base = src + (long long)(zi - src_z0) * plane;
+  for (int idx = threadIdx.x; idx < Cfg::TYH * Cfg::TXH; idx += Cfg::NT) {
+    const int row = idx / Cfg::TXH, e = idx - row * Cfg::TXH;
+    const int gy = y0 - RYH + row, gx = x0 - RXH + e;
+    const bool ok = (gy >= 0) && (gy < ny) && (gx >= 0) && (gx < nx);
+    const T* g = ok ? base + (long long)gy * nx + gx : src;
+    cp_async<sizeof(T)>(dst + row * Cfg::PITCH + (e % Cfg::RX) * Cfg::Q + e / Cfg::RX, g, ok);
+  }
+}
+
+template <typename T, int KY, int KX, int MODE, bool ADJ>
+__global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
+    conv_tiled_kernel(const __grid_constant__ ConvArgs<T> p) {
+  using Cfg = ConvCfg<T, KY, KX, MODE>;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, NIN = Cfg::NIN;
+  constexpr int WIN = RX + KX - 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* coef_s = reinterpret_cast<T*>(smem_raw);
+  size_t coef_bytes = ((size_t)p.kz * KY * KX * sizeof(T) + 15) & ~size_t(15);
+  T* tiles = reinterpret_cast<T*>(smem_raw + coef_bytes);
+  double* red_s = reinterpret_cast<double*>(tiles + 2 * NIN * Cfg::TILE);
+
+  const int zidx = blockIdx.z;
+  const int jid = find_job(p, zidx);
+  const ConvJob<T>& job = p.jobs[jid];
+  const int zo = job.out_lo + (zidx - job.work_begin);
+  const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
+  const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
+  const int rz = (p.kz - 1) / 2;
+
+  // taps a whose input plane zo+a-rz lies inside the fragment
+  const long long zlo_in = job.src_z0, zhi_in = job.src_z0 + job.src_nz - 1;
+  const int a_lo = (int)max(0LL, zlo_in - zo + rz);
+  const int a_hi = (int)min((long long)p.kz - 1, zhi_in - zo + rz);
+
+  stage_coefs<T, ADJ>(p, zo, coef_s, Cfg::NT);
+
+  T acc[NIN][RY][RX];
+#pragma unroll
+  for (int s = 0; s < NIN; ++s)
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int i = 0; i < RX; ++i) acc[s][r][i] = T(0);
+
+  if (a_lo <= a_hi) {
+    stage_tile<Cfg>(tiles, job.src0, job.src_z0, zo + a_lo - rz, y0, x0, p.ny, p.nx, p.plane);
+    if constexpr (NIN == 2)
+      stage_tile<Cfg>(tiles + Cfg::TILE, job.src1, job.src_z0, zo + a_lo - rz, y0, x0, p.ny, p.nx, p.plane);
+    cp_async_commit();
+  }
+  int buf = 0;
+  for (int a = a_lo; a <= a_hi; ++a) {
+    if (a < a_hi) {
+      T* nb = tiles + (buf ^ 1) * NIN * Cfg::TILE;
+      stage_tile<Cfg>(nb, job.src0, job.src_z0, zo + a + 1 - rz, y0, x0, p.ny, p.nx, p.plane);
+      if constexpr (NIN == 2)
+        stage_tile<Cfg>(nb + Cfg::TILE, job.src1, job.src_z0, zo + a + 1 - rz, y0, x0, p.ny, p.nx, p.plane);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const T* cs = coef_s + a * (KY * KX);
+    const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx;
+#pragma unroll
+    for (int yi = 0; yi < RY + KY - 1; ++yi) {
+      T v[NIN][WIN];
+#pragma unroll
+      for (int s = 0; s < NIN; ++s)
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) v[s][j] = tb[s * Cfg::TILE + yi * Cfg::PITCH + (j % RX) * Cfg::Q + j / RX];
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const int b = yi - r;
+        if (b < 0 || b >= KY) continue;
+#pragma unroll
+        for (int c = 0; c < KX; ++c) {
+          const T k = cs[b * KX + c];
+#pragma unroll
+          for (int s = 0; s < NIN; ++s)
+#pragma unroll
+            for (int i = 0; i < RX; ++i) acc[s][r][i] = fma_rn(k, v[s][i + c], acc[s][r][i]);
+        }
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+
+  // ---- epilogue -----------------------------------------------------------
+  constexpr int NV = Cfg::NV;
+  double part[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
+  const long long orow = (long long)(zo - job.out_lo) * p.plane;
+  XView<T> xv;
+  if constexpr (MODE == M_GRAD) {
+    xv.p = job.xg; xv.z0 = job.xg_z0; xv.nzv = job.xg_nz; xv.ny = p.ny; xv.nx = p.nx; xv.plane = p.plane;
+  }
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int y = y0 + ty * RY + r;
+    if (y >= p.ny) continue;
+#pragma unroll
+    for (int i = 0; i < RX; ++i) {
+      const int x = x0 + tx * RX + i;
+      if (x >= p.nx) continue;
+      const long long o = orow + (long long)y * p.nx + x;
+      const T a0 = acc[0][r][i];
+      if constexpr (MODE == M_STORE) {
+        job.dst0[o] = a0;
+      } else if constexpr (MODE == M_RESID) {
+        const T res = sub_rn(a0, job.sub[o]);
+        if (job.dst0) job.dst0[o] = res;
+        part[0] += (double)res * (double)res;
+      } else if constexpr (MODE == M_GRAD) {
+        T w;
+        const T g = grad_voxel<T>(a0, xv, zo, y, x, p.nz_global, (T)p.two_eta, (T)p.lam, (T)p.two_kappa,
+                                  (T)p.delta2, (T)p.x_min, (T)p.x_max, &w);
+        job.dst0[o] = g;
+        job.omega[o] = w;
+      } else if constexpr (MODE == M_GRAM1) {
+        if (job.dst0) job.dst0[o] = a0;
+        part[0] += (double)a0 * (double)a0;
+      } else if constexpr (MODE == M_GRAM2) {
+        const T a1 = acc[NIN - 1][r][i];
+        part[0] += (double)a0 * (double)a0;
+        part[1] += (double)a0 * (double)a1;
+        part[2] += (double)a1 * (double)a1;
+      }
+    }
+  }
+  if constexpr (NV > 0) {
+    cta_reduce<NV, Cfg::NT>(part, red_s);
+    if (threadIdx.x == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic path for kernel widths without a tuned instantiation: one output
+// voxel per thread, runtime ky/kx, same a->b->c order and same epilogues.
+constexpr int kGenericNT = 128;
+constexpr int kGenericTX = 32, kGenericTY = 4;
+
+template <typename T, int MODE, bool ADJ>
+__global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_constant__ ConvArgs<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* coef_s = reinterpret_cast<T*>(smem_raw);
+  size_t coef_bytes = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
+  double* red_s = reinterpret_cast<double*>(smem_raw + coef_bytes);
+  const int zidx = blockIdx.z;
+  const int jid = find_job(p, zidx);
+  const ConvJob<T>& job = p.jobs[jid];
+  const int zo = job.out_lo + (zidx - job.work_begin);
+  stage_coefs<T, ADJ>(p, zo, coef_s, kGenericNT);
+  __syncthreads();
+  const int x = blockIdx.x * kGenericTX + (threadIdx.x % kGenericTX);
+  const int y = blockIdx.y * kGenericTY + (threadIdx.x / kGenericTX);
+  const int rz = (p.kz - 1) / 2, ry = (p.ky - 1) / 2, rx = (p.kx - 1) / 2;
+  constexpr int NV = ModeNV<MODE>::value;
+  double part[NV > 0 ? NV : 1];
+  for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
+  if (y < p.ny && x < p.nx) {
+    T acc0 = T(0), acc1 = T(0);
+    for (int a = 0; a < p.kz; ++a) {
+      const long long zi = (long long)zo + a - rz;
+      if (zi < job.src_z0 || zi >= job.src_z0 + job.src_nz) continue;
+      const long long pbase = (zi - job.src_z0) * p.plane;
+      for (int b = 0; b < p.ky; ++b) {
+        const int yy = y + b - ry;
+        if (yy < 0 || yy >= p.ny) continue;
+        for (int c = 0; c < p.kx; ++c) {
+          const int xx = x + c - rx;
+          if (xx < 0 || xx >= p.nx) continue;
+          const T k = coef_s[(a * p.ky + b) * p.kx + c];
+          const long long off = pbase + (long long)yy * p.nx + xx;
+          acc0 = fma_rn(k, job.src0[off], acc0);
+          if constexpr (MODE == M_GRAM2) acc1 = fma_rn(k, job.src1[off], acc1);
+        }
+      }
+    }
+    const long long o = (long long)(zo - job.out_lo) * p.plane + (long long)y * p.nx + x;
+    if constexpr (MODE == M_STORE) {
+      job.dst0[o] = acc0;
+    } else if constexpr (MODE == M_RESID) {
+      const T res = sub_rn(acc0, job.sub[o]);
+      if (job.dst0) job.dst0[o] = res;
+      part[0] = (double)res * (double)res;
+    } else if constexpr (MODE == M_GRAD) {
+      XView<T> xv{job.xg, job.xg_z0, job.xg_nz, p.ny, p.nx, p.plane};
+      T w;
+      const T g = grad_voxel<T>(acc0, xv, zo, y, x, p.nz_global, (T)p.two_eta, (T)p.lam, (T)p.two_kappa,
+                                (T)p.delta2, (T)p.x_min, (T)p.x_max, &w);
+      job.dst0[o] = g;
+      job.omega[o] = w;
+    } else if constexpr (MODE == M_GRAM1) {
+      if (job.dst0) job.dst0[o] = acc0;
+      part[0] = (double)acc0 * (double)acc0;
+    } else if constexpr (MODE == M_GRAM2) {
+      part[0] = (double)acc0 * (double)acc0;
+      part[1] = (double)acc0 * (double)acc1;
+      part[2] = (double)acc1 * (double)acc1;
+    }
+  }
+  if constexpr (NV > 0) {
+    cta_reduce<NV, kGenericNT>(part, red_s);
+    if (threadIdx.x == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
+    }
+  }
+}
+
+}  // namespace bd3mg

@@ -1,0 +1,383 @@
+// HBM-bound kernels of the BD3MG block step: regulariser Gram terms, the
+// per-block 2x2 memory-gradient solve, the in-place block update, the
+// elementwise objective terms, the majorant regulariser epilogue, and the
+// deterministic two-level reductions that feed them.
+#pragma once
+
+#include "depthvar.cuh"
+
+namespace bd3mg {
+
+constexpr int kEwNT = 256;           // threads per CTA, elementwise kernels
+constexpr int kRegNV = 12;           // sums produced per block by reg_gram
+constexpr int kInfoNV = 16;          // doubles of StepInfo per block
+constexpr int kEvalNV = 5;           // box, tv, axial, |x-snap|^2, |snap|^2
+
+// ---------------------------------------------------------------------------
+// Deterministic final reduction: out[j*nv + k] = sum_{r in [begin_j, end_j)}
+// rows[r*nv + k], each thread summing a fixed stride class in order, then a
+// fixed tree.  One CTA per job.
+struct RowRanges {
+  int njobs;
+  long long begin[kMaxJobs];
+  long long end[kMaxJobs];
+};
+
+__global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
+                                                            const __grid_constant__ RowRanges rr,
+                                                            double* __restrict__ out, int out_stride) {
+  __shared__ double s[kEwNT];
+  const int j = blockIdx.x;
+  for (int k = 0; k < nv; ++k) {
+    double acc = 0.0;
+    for (long long r = rr.begin[j] + threadIdx.x; r < rr.end[j]; r += kEwNT) acc += rows[r * nv + k];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = kEwNT / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j * out_stride + k] = s[0];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Regulariser part of the forward-only Gram D^T A_S D for D = [-g, d]
+// (reference directions.py:80-85 with A from objective.py:262-274):
+//   e_ij = <b_i,b_j>, t_ij = sum w (Dx b_i Dx b_j + Dy b_i Dy b_j),
+//   a_ij = <Dz E b_i, Dz E b_j> (block-embedded axial differences)
+// plus rhs pieces <g,d>, and the nonzero / non-finite counts of g.
+template <typename T>
+struct RegBlock {
+  const T* g;      // block rows
+  const T* d;      // block rows or null (zero memory direction)
+  const T* omega;  // block rows
+  int lo, hi;
+  int ctas;        // CTAs assigned to this block
+  long long row_begin;  // first partial row of this block
+};
+template <typename T>
+struct RegArgs {
+  int ny, nx, nz;
+  long long plane;
+  int nblocks;
+  RegBlock<T> blk[kMaxJobs];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) reg_gram_kernel(const __grid_constant__ RegArgs<T> p,
+                                                          double* __restrict__ partials) {
+  __shared__ double red[(kEwNT / 32) * kRegNV];
+  const RegBlock<T>& B = p.blk[blockIdx.y];
+  if ((int)blockIdx.x >= B.ctas) return;  // uniform per CTA
+  const int h = B.hi - B.lo + 1;
+  const long long n = (long long)h * p.plane;
+  double v[kRegNV];
+#pragma unroll
+  for (int k = 0; k < kRegNV; ++k) v[k] = 0.0;
+  const XView<T> gv{B.g, B.lo, h, p.ny, p.nx, p.plane};
+  const XView<T> dv{B.d, B.lo, h, p.ny, p.nx, p.plane};
+  const bool has_d = B.d != nullptr;
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < n; i += (long long)B.ctas * kEwNT) {
+    const int z = B.lo + (int)(i / p.plane);
+    const long long rem = i % p.plane;
+    const int y = (int)(rem / p.nx), x = (int)(rem % p.nx);
+    const T g = gv.at(z, y, x);
+    const T d = has_d ? dv.at(z, y, x) : T(0);
+    const double b0 = -(double)g, b1 = (double)d;
+    v[0] += b0 * b0;
+    v[1] += b0 * b1;
+    v[2] += b1 * b1;
+    const double w = (double)B.omega[i];
+    const double dx0 = -(double)fdx(gv, z, y, x), dy0 = -(double)fdy(gv, z, y, x);
+    const double dx1 = has_d ? (double)fdx(dv, z, y, x) : 0.0, dy1 = has_d ? (double)fdy(dv, z, y, x) : 0.0;
+    v[3] += w * (dx0 * dx0 + dy0 * dy0);
+    v[4] += w * (dx0 * dx1 + dy0 * dy1);
+    v[5] += w * (dx1 * dx1 + dy1 * dy1);
+    // axial row z (between z and z+1) of the block-embedded vector
+    double z0v, z1v;
+    if (z < B.hi) {
+      z0v = -((double)gv.at(z + 1, y, x) - (double)g);
+      z1v = has_d ? (double)dv.at(z + 1, y, x) - (double)d : 0.0;
+    } else if (B.hi < p.nz - 1) {
+      z0v = -b0;  // row hi sees E b[hi+1] = 0
+      z1v = -b1;
+    } else {
+      z0v = 0.0;
+      z1v = 0.0;
+    }
+    v[6] += z0v * z0v;
+    v[7] += z0v * z1v;
+    v[8] += z1v * z1v;
+    if (z == B.lo && B.lo >= 1) {  // row lo-1: E b[lo] - 0
+      v[6] += b0 * b0;
+      v[7] += b0 * b1;
+      v[8] += b1 * b1;
+    }
+    v[9] += (double)g * (double)d;
+    v[10] += (g != T(0)) ? 1.0 : 0.0;
+    v[11] += isfinite((double)g) ? 0.0 : 1.0;
+  }
+  cta_reduce<kRegNV, kEwNT>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = partials + (B.row_begin + blockIdx.x) * kRegNV;
+#pragma unroll
+    for (int k = 0; k < kRegNV; ++k) o[k] = v[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2x2 symmetric pseudo-inverse (reference directions.py:43-54): eigenvalues
+// with |lambda| <= 1e-12 * max|lambda| are dropped.  Stable Jacobi rotation.
+BD3MG_D void pinv_sym2(double a, double b, double c, double tol_rel, double& pa, double& pb, double& pc) {
+  double l1, l2, cs, sn;
+  if (b == 0.0) {
+    l1 = a; l2 = c; cs = 1.0; sn = 0.0;
+  } else {
+    const double th = (c - a) / (2.0 * b);
+    double t;
+    if (fabs(th) > 1e150) t = 0.5 / th;
+    else t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
+    cs = 1.0 / sqrt(1.0 + t * t);
+    sn = t * cs;
+    l1 = a - t * b;
+    l2 = c + t * b;
+  }
+  // eigenvectors v1 = (cs, -sn), v2 = (sn, cs)
+  const double amax = fmax(fabs(l1), fabs(l2));
+  if (amax == 0.0) { pa = pb = pc = 0.0; return; }
+  const double i1 = fabs(l1) > tol_rel * amax ? 1.0 / l1 : 0.0;
+  const double i2 = fabs(l2) > tol_rel * amax ? 1.0 / l2 : 0.0;
+  pa = cs * cs * i1 + sn * sn * i2;
+  pb = -cs * sn * i1 + sn * cs * i2;
+  pc = sn * sn * i1 + cs * cs * i2;
+}
+
+struct SolveArgs {
+  int nblocks;
+  double two_eta, lam, two_kappa;
+  double prune_tol, pinv_tol;
+  int has_d[kMaxJobs];
+};
+
+// info layout per block (kInfoNV doubles):
+// 0-2 gram (00,01,11 of the kept columns; 1 column -> [0]), 3-4 rhs,
+// 5-6 coeffs, 7 ncols, 8 status (0 ok, 1 non-finite g), 9 |g|, 10 c_g
+// (coefficient of -g), 11 c_d (coefficient of d), 12 column mask (1:-g, 2:d)
+__global__ void solve2x2_kernel(const __grid_constant__ SolveArgs p, const double* __restrict__ data3,
+                                const double* __restrict__ reg12, double* __restrict__ info) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p.nblocks) return;
+  const double* D = data3 + j * 3;
+  const double* R = reg12 + j * kRegNV;
+  double* o = info + j * kInfoNV;
+  for (int k = 0; k < kInfoNV; ++k) o[k] = 0.0;
+  const double gg = R[0], dd = R[2], gd = R[9];
+  const double gn = sqrt(gg);
+  o[9] = gn;
+  if (R[11] > 0.0) { o[8] = 1.0; return; }      // non-finite gradient
+  if (R[10] == 0.0) return;                      // g == 0: zero step
+  const double tol = p.prune_tol * (1.0 + gn);
+  const bool k0 = gn > tol;
+  const bool k1 = p.has_d[j] && sqrt(dd) > tol;
+  const int ncols = (int)k0 + (int)k1;
+  o[7] = ncols;
+  o[12] = (k0 ? 1 : 0) + (k1 ? 2 : 0);
+  if (ncols == 0) return;
+  // full 2x2 for columns [-g, d]; data part <H b_i, H b_j> (H(-g) = -Hg)
+  const double G00 = D[0] + p.two_eta * R[0] + p.lam * R[3] + p.two_kappa * R[6];
+  const double G01 = -D[1] + p.two_eta * R[1] + p.lam * R[4] + p.two_kappa * R[7];
+  const double G11 = D[2] + p.two_eta * R[2] + p.lam * R[5] + p.two_kappa * R[8];
+  const double r0 = -gg, r1 = gd;
+  double cg = 0.0, cd = 0.0;
+  if (ncols == 2) {
+    double pa, pb, pc;
+    pinv_sym2(G00, G01, G11, p.pinv_tol, pa, pb, pc);
+    cg = -(pa * r0 + pb * r1);
+    cd = -(pb * r0 + pc * r1);
+    o[0] = G00; o[1] = G01; o[2] = G11; o[3] = r0; o[4] = r1; o[5] = cg; o[6] = cd;
+  } else {
+    const double G = k0 ? G00 : G11, r = k0 ? r0 : r1;
+    const double pinv = (G != 0.0 && fabs(G) > p.pinv_tol * fabs(G)) ? 1.0 / G : 0.0;
+    const double cf = -(pinv * r);
+    if (k0) cg = cf; else cd = cf;
+    o[0] = G; o[3] = r; o[5] = cf;
+  }
+  o[10] = cg;
+  o[11] = cd;
+}
+
+// ---------------------------------------------------------------------------
+// increment = c_g * (-g) + c_d * d  (reference directions.py:86), optionally
+// applied in place: x_S += inc; d_mem_S = inc (scheduler.py:151-153).
+template <typename T>
+struct UpdBlock {
+  const T* g;
+  const T* d;      // may be null
+  T* inc_out;      // may be null
+  T* x;            // block rows of the iterate, may be null
+  T* dmem;         // block rows of the memory store, may be null
+  long long n;
+  int ctas;
+};
+template <typename T>
+struct UpdArgs {
+  int nblocks;
+  UpdBlock<T> blk[kMaxJobs];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) update_kernel(const __grid_constant__ UpdArgs<T> p,
+                                                        const double* __restrict__ info) {
+  const UpdBlock<T>& B = p.blk[blockIdx.y];
+  if ((int)blockIdx.x >= B.ctas) return;
+  const double* o = info + blockIdx.y * kInfoNV;
+  if (o[8] != 0.0) return;  // non-finite gradient: host raises, nothing applied
+  const T cg = (T)o[10], cd = (T)o[11];
+  const bool has_d = B.d != nullptr;
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < B.n; i += (long long)B.ctas * kEwNT) {
+    T inc = mul_rn(-B.g[i], cg);
+    if (has_d) inc = add_rn(inc, mul_rn(B.d[i], cd));
+    if (B.inc_out) B.inc_out[i] = inc;
+    if (B.x) B.x[i] = add_rn(B.x[i], inc);
+    if (B.dmem) B.dmem[i] = inc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise objective terms over a whole volume (objective.py:148-152) and
+// the stop-rule norms (scheduler.py:218-219).
+template <typename T>
+struct EvalArgs {
+  const T* x;
+  const T* snap;  // may be null
+  int nz, ny, nx;
+  long long plane, n;
+  double delta2, x_min, x_max;
+  int ctas;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) eval_terms_kernel(const __grid_constant__ EvalArgs<T> p,
+                                                            double* __restrict__ partials) {
+  __shared__ double red[(kEwNT / 32) * kEvalNV];
+  double v[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const XView<T> xv{p.x, 0, p.nz, p.ny, p.nx, p.plane};
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < p.n; i += (long long)p.ctas * kEwNT) {
+    const int z = (int)(i / p.plane);
+    const long long rem = i % p.plane;
+    const int y = (int)(rem / p.nx), x = (int)(rem % p.nx);
+    const double xc = (double)p.x[i];
+    const double cl = xc < p.x_min ? p.x_min : (xc > p.x_max ? p.x_max : xc);
+    const double e = xc - cl;
+    v[0] += e * e;
+    const double dx = (double)fdx(xv, z, y, x), dy = (double)fdy(xv, z, y, x);
+    v[1] += sqrt(dx * dx + dy * dy + p.delta2);
+    if (z < p.nz - 1) {
+      const double dz = (double)p.x[i + p.plane] - xc;
+      v[2] += dz * dz;
+    }
+    if (p.snap) {
+      const double s = (double)p.snap[i];
+      v[3] += (xc - s) * (xc - s);
+      v[4] += s * s;
+    }
+  }
+  cta_reduce<kEvalNV, kEwNT>(v, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kEvalNV; ++k) partials[(long long)blockIdx.x * kEvalNV + k] = v[k];
+  }
+}
+
+// terms: [data, box, tv, axial, f, |x-snap|^2, |snap|^2]
+__global__ void eval_finalize_kernel(const double* __restrict__ data1, const double* __restrict__ ew5,
+                                     double eta, double lam, double kappa, double* __restrict__ terms) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double data = 0.5 * data1[0];
+  const double box = eta * ew5[0];
+  const double tv = lam * ew5[1];
+  const double ax = kappa * ew5[2];
+  terms[0] = data; terms[1] = box; terms[2] = tv; terms[3] = ax;
+  terms[4] = data + box + tv + ax;
+  terms[5] = ew5[3]; terms[6] = ew5[4];
+}
+
+// ---------------------------------------------------------------------------
+// MajorantOperator.apply regulariser epilogue (objective.py:262-274), in place
+// on out = (H^T H)_SS v:  out += 2eta v; out += lam(DxT(w Dx v)+DyT(w Dy v));
+// out += 2kappa (dz[:-1]-dz[1:]) of the block-embedded v.
+template <typename T>
+struct MajArgs {
+  const T* v;
+  const T* omega;
+  T* out;
+  int lo, hi, nz, ny, nx;
+  long long plane, n;
+  double two_eta, lam, two_kappa;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) majorant_reg_kernel(const __grid_constant__ MajArgs<T> p) {
+  const long long i = (long long)blockIdx.x * kEwNT + threadIdx.x;
+  if (i >= p.n) return;
+  const int h = p.hi - p.lo + 1;
+  const int t = (int)(i / p.plane);  // local plane
+  const long long rem = i % p.plane;
+  const int y = (int)(rem / p.nx), x = (int)(rem % p.nx);
+  const XView<T> vv{p.v, 0, h, p.ny, p.nx, p.plane};
+  const XView<T> wv{p.omega, 0, h, p.ny, p.nx, p.plane};
+  const T vc = vv.at(t, y, x);
+  T o = add_rn(p.out[i], mul_rn((T)p.two_eta, vc));
+  const T px0 = mul_rn(wv.at(t, y, x), fdx(vv, t, y, x));
+  const T py0 = mul_rn(wv.at(t, y, x), fdy(vv, t, y, x));
+  T tvx, tvy;
+  if (p.nx == 1) tvx = T(0);
+  else if (x == 0) tvx = -px0;
+  else {
+    const T pxm = mul_rn(wv.at(t, y, x - 1), fdx(vv, t, y, x - 1));
+    tvx = (x == p.nx - 1) ? pxm : sub_rn(pxm, px0);
+  }
+  if (p.ny == 1) tvy = T(0);
+  else if (y == 0) tvy = -py0;
+  else {
+    const T pym = mul_rn(wv.at(t, y - 1, x), fdy(vv, t, y - 1, x));
+    tvy = (y == p.ny - 1) ? pym : sub_rn(pym, py0);
+  }
+  o = add_rn(o, mul_rn((T)p.lam, add_rn(tvx, tvy)));
+  // dz over global rows [lo-1, hi] of the embedded vector (objective.py:267-273)
+  T dzm, dzp;
+  if (t == 0) dzm = (p.lo - 1 >= 0) ? vc : T(0);
+  else dzm = sub_rn(vc, vv.at(t - 1, y, x));
+  if (t == h - 1) dzp = (p.hi < p.nz - 1) ? -vc : T(0);
+  else dzp = sub_rn(vv.at(t + 1, y, x), vc);
+  o = add_rn(o, mul_rn((T)p.two_kappa, sub_rn(dzm, dzp)));
+  p.out[i] = o;
+}
+
+// receive_update's block write (scheduler.py:151-153): x += inc; d_mem = inc.
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) apply_increment_kernel(T* __restrict__ x, T* __restrict__ dmem,
+                                                                 const T* __restrict__ inc, long long n) {
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < n; i += (long long)gridDim.x * kEwNT) {
+    const T v = inc[i];
+    x[i] = add_rn(x[i], v);
+    if (dmem) dmem[i] = v;
+  }
+}
+
+// Half-quadratic weights of rows [lo, lo+n/plane) of a fragment
+// (objective.py:130-132, cached by MajorantOperator.__init__ :233-235).
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) omega_kernel(const __grid_constant__ XView<T> xv, int lo, long long n,
+                                                       T delta2, T* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * kEwNT + threadIdx.x;
+  if (i >= n) return;
+  const int z = lo + (int)(i / xv.plane);
+  const long long rem = i % xv.plane;
+  const int y = (int)(rem / xv.nx), x = (int)(rem % xv.nx);
+  out[i] = omega_of(fdx(xv, z, y, x), fdy(xv, z, y, x), delta2);
+}
+
+}  // namespace bd3mg

@@ -1,0 +1,164 @@
+"""Volume and block types plus the seeded input generators.
+
+Mirrors the type layer of the reference (`pkg/src/bd3mg/volume.py:35-94`):
+a volume is a C-contiguous array of shape ``(nz, ny, nx)`` with x fastest,
+blocks are inclusive z-slice ranges.  The stochastic helpers draw from numpy's
+Philox counter-based generator so the oracle and the CUDA path consume
+bitwise-identical arrays (`volume.py:176-178`, `:222-239`).
+
+The ellipsoid phantom is not in the reference (its phantom is
+blobs/spheres/boxes); it is the BASELINE.json generator for configs C1-C5.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import NamedTuple
+
+import numpy as np
+
+
+class Dims3(NamedTuple):
+    """Voxel counts per axis (reference `volume.py:35-54`)."""
+
+    nx: int
+    ny: int
+    nz: int
+
+    @property
+    def shape(self) -> tuple[int, int, int]:
+        return (self.nz, self.ny, self.nx)
+
+    @property
+    def count(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def validate(self) -> "Dims3":
+        if min(self) < 1:
+            raise ValueError(f"dimensions must be >= 1, got {self}")
+        return self
+
+
+@dataclass(frozen=True)
+class SliceBlock:
+    """Inclusive depth range [z_lo, z_hi] (reference `volume.py:57-79`)."""
+
+    z_lo: int
+    z_hi: int
+
+    def __post_init__(self):
+        if not (0 <= self.z_lo <= self.z_hi):
+            raise ValueError(f"invalid slice range [{self.z_lo}, {self.z_hi}]")
+
+    @property
+    def height(self) -> int:
+        return self.z_hi - self.z_lo + 1
+
+    def count(self, dims: Dims3) -> int:
+        return dims.nx * dims.ny * self.height
+
+    def check_within(self, dims: Dims3) -> "SliceBlock":
+        if self.z_hi >= dims.nz:
+            raise ValueError(f"block {self} exceeds nz={dims.nz}")
+        return self
+
+
+def dims_of(vol) -> Dims3:
+    nz, ny, nx = tuple(vol.shape)
+    return Dims3(int(nx), int(ny), int(nz))
+
+
+def check_volume(vol) -> np.ndarray:
+    """float64, C-order, 3-D, finite (reference `volume.py:87-94`)."""
+    arr = np.ascontiguousarray(vol, dtype=np.float64)
+    if arr.ndim != 3:
+        raise ValueError(f"volume must be 3-dimensional, got shape {arr.shape}")
+    if not np.isfinite(arr).all():
+        raise ValueError("volume contains non-finite entries")
+    return arr
+
+
+def philox(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(seed))
+
+
+def add_gaussian_noise(vol, sigma: float, seed: int) -> np.ndarray:
+    """vol + sigma * N(0,1) i.i.d. (reference `volume.py:222-229`)."""
+    base = np.asarray(vol, dtype=np.float64)
+    if sigma < 0:
+        raise ValueError("sigma must be nonnegative")
+    if sigma == 0:
+        return base.copy()
+    return base + sigma * philox(seed).standard_normal(base.shape)
+
+
+def init_uniform(dims: Dims3, upper: float, seed: int) -> np.ndarray:
+    """U[0, upper] i.i.d. (reference `volume.py:232-239`)."""
+    dims = Dims3(*dims).validate()
+    if upper < 0:
+        raise ValueError("upper must be nonnegative")
+    if upper == 0:
+        return np.zeros(dims.shape)
+    return philox(seed).uniform(0.0, upper, dims.shape)
+
+
+def snr_db(reference, estimate) -> float:
+    """20 log10(||ref|| / ||est - ref||) (reference `volume.py:148-161`)."""
+    ref = np.asarray(reference, dtype=np.float64)
+    est = np.asarray(estimate, dtype=np.float64)
+    if ref.shape != est.shape:
+        raise ValueError(f"shape mismatch {ref.shape} vs {est.shape}")
+    rn = float(np.linalg.norm(ref))
+    if rn == 0.0:
+        raise ValueError("reference volume has zero norm")
+    en = float(np.linalg.norm(est - ref))
+    return math.inf if en == 0.0 else 20.0 * math.log10(rn / en)
+
+
+def rel_dist(x, x_star) -> float:
+    """||x - x*|| / ||x*|| (reference `volume.py:164-173`)."""
+    a = np.asarray(x, dtype=np.float64)
+    b = np.asarray(x_star, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch {a.shape} vs {b.shape}")
+    bn = float(np.linalg.norm(b))
+    if bn == 0.0:
+        raise ValueError("x_star has zero norm")
+    return float(np.linalg.norm(a - b)) / bn
+
+
+def ellipsoid_phantom(dims: Dims3, n: int, seed: int, amplitude: str = "uniform",
+                      axis_frac=(0.05, 0.2)) -> np.ndarray:
+    """Sum of ``n`` axis-aligned solid ellipsoids (BASELINE configs C1-C5).
+
+    Centres ~ U over the volume, semi-axes ~ U[axis_frac]*extent + 1 voxel,
+    amplitudes ~ U[0,1] (``amplitude="uniform"``) or Gamma(2, 0.25)
+    (``"gamma"``, the Poisson-like spread of C3/C4).  Built plane by plane so
+    the 1024x1024x512 config does not need a full-volume meshgrid.
+    """
+    dims = Dims3(*dims).validate()
+    rng = philox(seed)
+    nz, ny, nx = dims.shape
+    extent = np.array([nz, ny, nx], dtype=np.float64)
+    centres = rng.uniform(0.0, 1.0, (n, 3)) * (extent - 1)
+    axes = rng.uniform(axis_frac[0], axis_frac[1], (n, 3)) * extent + 1.0
+    if amplitude == "uniform":
+        amps = rng.uniform(0.0, 1.0, n)
+    elif amplitude == "gamma":
+        amps = rng.gamma(2.0, 0.25, n)
+    else:
+        raise ValueError(f"unknown amplitude law {amplitude!r}")
+    vol = np.zeros(dims.shape)
+    yy = np.arange(ny, dtype=np.float64)[:, None]
+    xx = np.arange(nx, dtype=np.float64)[None, :]
+    for (cz, cy, cx), (az, ay, ax), amp in zip(centres, axes, amps):
+        z0 = max(0, int(math.floor(cz - az)))
+        z1 = min(nz - 1, int(math.ceil(cz + az)))
+        for z in range(z0, z1 + 1):
+            tz = ((z - cz) / az) ** 2
+            if tz > 1.0:
+                continue
+            mask = ((yy - cy) / ay) ** 2 + ((xx - cx) / ax) ** 2 <= 1.0 - tz
+            vol[z][mask] += amp
+    return vol
