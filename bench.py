@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""BD3MG block-iterations/s on BASELINE config C2 (256x256x64 fp64, PSF
+5x5x11, 8 blocks of 8 planes), plus H/H^T Gvoxel/s against the measured
+FP64 FMA-pipe roofline.
+
+One step = one block-Jacobi sweep (reference run_bp3mg_barrier with
+workers = #blocks, runtime.py:244-292): 8 block-iterations (mg_direction +
+receive_update each) and the per-sweep recorder pass (f(x) + stop norms).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 is launched by torchrun (one rank per GPU): the z-slabs of the volume are
+split into contiguous block ranges per rank with kz-plane halos exchanged
+over NCCL each sweep (paper_2002_02328_b200/distributed.py).  Rank 0 prints
+ONE JSON line.  ``--impl reference`` times the reference's CPU
+implementation of the same sweep on the host cores (oracle port driving the
+reference's own compiled _core, oracle/_ref), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BD3MG block-iterations/sec (C2 256x256x64 fp64, PSF 5x5x11, 8 blocks x 8 planes, block-Jacobi sweeps)"
+UNIT = "block-it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e / cpu baseline / roofline (profiling runs)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def reference_arm(args, cfg_name):
+    """The reference CPU implementation on the host cores: oracle port of
+    objective/directions/runtime driving the reference's compiled core
+    (oracle/_ref) -- or the bitwise-identical C restatement when absent --
+    with the reference's multi-core mode (bp3mg barrier, ThreadPool of
+    min(cores, B) workers, GIL released in the core)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    from paper_2002_02328_b200 import configs
+
+    kind = "reference" if O.ref_core_available() else "port"
+    O.core("ref" if kind == "reference" else "c", threads=1)
+    cfg = configs.CONFIGS[cfg_name]
+    psf_k, y, x0 = _host_problem(cfg, O)
+    crit = O.Criterion(psf_k, y, cfg.lam, cfg.eta, cfg.kappa, cfg.delta)
+    nz = cfg.dims.nz
+    blocks = O.blocks_of(nz, cfg.block_height)
+    B = len(blocks)
+    cores = os.cpu_count() or 1
+    threads = max(1, min(cores, B))
+    pool = ThreadPoolExecutor(max_workers=threads)
+    x = x0.copy()
+    prev = np.zeros_like(x)
+    snap = x.copy()
+
+    def sweep():
+        nonlocal x, snap
+
+        def one(b):
+            lo, hi = b
+            s_lo, s_hi = O.support(nz, crit.kz, lo, hi)
+            return O.mg_direction(crit, x[s_lo:s_hi + 1].copy(), s_lo, lo, hi, prev[lo:hi + 1].ravel().copy())
+
+        incs = list(pool.map(one, blocks))
+        for (lo, hi), inc in zip(blocks, incs):
+            inc = inc.reshape((hi - lo + 1,) + x.shape[1:])
+            x[lo:hi + 1] += inc
+            prev[lo:hi + 1] = inc
+        crit.value(x)
+        np.linalg.norm(x - snap), np.linalg.norm(snap)
+        snap = x.copy()
+
+    for _ in range(args.warmup):
+        sweep()
+    t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        sweep()
+        t.append(time.perf_counter() - t0)
+    total = sum(t)
+    value = args.steps * B / total
+    sample = (f"{args.steps} timed sweeps x {B} blocks of config {cfg_name} after {args.warmup} warm-up; "
+              f"bp3mg barrier, {threads} worker threads; core: "
+              + ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if kind == "reference"
+                 else "oracle/bd3mg_oracle.c (bitwise the reference core)"))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_dict(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _host_problem(cfg, O):
+    """Seeded inputs on the host: kernels, y (through the oracle H, bitwise
+    the reference's), x0."""
+    from paper_2002_02328_b200 import blur, configs
+    from paper_2002_02328_b200.volume import add_gaussian_noise, init_uniform
+    psf = blur.depth_variant_stack(cfg.dims, cfg.kdims, cfg.sigma_xy, cfg.sigma_z)
+    truth = configs.truth_of(cfg)
+    y = add_gaussian_noise(O.H(psf.kernels, truth), cfg.noise, cfg.seed + 2)
+    x0 = init_uniform(cfg.dims, float(np.max(y)), cfg.seed + 3)
+    return psf.kernels, y, x0
+
+
+def _config_dict(cfg, world):
+    B = -(-cfg.dims.nz // cfg.block_height)
+    return {"workload": f"{cfg.name}: {cfg.dims.nx}x{cfg.dims.ny}x{cfg.dims.nz} {cfg.dtype}, PSF "
+                        f"{cfg.kdims[0]}x{cfg.kdims[1]}x{cfg.kdims[2]} depth-variant Gaussian, {B} blocks x "
+                        f"{cfg.block_height} planes, block-Jacobi sweep (bp3mg workers=B) + per-sweep f",
+            "global_batch": B, "blocks_per_step": B, "ranks": world,
+            "l2": "flushed between timed steps (256 MB write, untimed)",
+            "regulariser": {"lam": cfg.lam, "eta": cfg.eta, "kappa": cfg.kappa, "delta": cfg.delta}}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args, args.config)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_02328_b200 import _native as N
+    from paper_2002_02328_b200 import blur, configs, device as D, objective, runtime
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.CONFIGS[args.config]
+    dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    obj = objective.Objective(psf, y, params)
+    B = -(-cfg.dims.nz // cfg.block_height)
+
+    if world > 1:
+        from paper_2002_02328_b200 import distributed
+        eng = distributed.ShardedJacobi(obj, x0, cfg.block_height, dtype)
+    else:
+        eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, dtype)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    # warm-up: eager sweep (counts launches), then capture the sweep graph
+    n0 = N.lib.bd3mg_launch_count()
+    eng.sweep()
+    launches_per_step = N.lib.bd3mg_launch_count() - n0
+    if not args.no_graph:
+        eng.capture()
+    for _ in range(max(args.warmup - 1, 0)):
+        eng.sweep()
+    torch.cuda.synchronize()
+    eng.check()
+
+    clocks = Clocks(local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record()
+        eng.sweep()
+        ends[i].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    eng.check()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t_max = ms
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    value = args.steps * B / (t_max / 1e3)
+    f_last = eng.f()
+
+    extra = {}
+    if not args.quick and rank == 0:
+        extra["roofline"], extra["operators"] = roofline(obj, cfg, dtype, torch, N, D, blur)
+    if not args.quick:
+        extra["e2e"] = e2e(obj, cfg, x0, args, world, rank, torch, N, D)
+    if not args.quick and rank == 0 and world == 1:
+        extra["cpu_baseline"] = cpu_baseline(cfg)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+                "dtype": cfg.dtype, "data": "synthetic (seeded ellipsoid phantom, BASELINE PSF family)",
+                "config": _config_dict(cfg, world), "clocks": clk,
+                "gpu_launches": int(launches_per_step * args.steps),
+                "f_after": f_last}
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def roofline(obj, cfg, dtype, torch, N, D, blur):
+    """Dominant kernel family: the dense depth-variant correlation.  Time
+    full-volume H and H^T launches with CUDA events on the launching stream;
+    achieved = algorithmic 2*nnz(H) flops / launch time; peak = measured
+    FMA-pipe probe (fp64 or fp32) on this GPU."""
+    x = torch.rand(obj.dims.shape, dtype=dtype, device="cuda")
+    out = torch.empty_like(x)
+    psf = obj.psf
+    nz = obj.dims.nz
+    flops = blur.flops_H(obj.dims, psf.kdims)
+    res = {}
+    for adj in (False, True):
+        for _ in range(3):
+            blur.correlate_rows(psf, x, 0, 0, nz - 1, adj, out=out)
+        reps = 20
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(reps):
+            blur.correlate_rows(psf, x, 0, 0, nz - 1, adj, out=out)
+        e.record()
+        torch.cuda.synchronize()
+        t = s.elapsed_time(e) / reps / 1e3
+        res["Ht" if adj else "H"] = {"ms": t * 1e3, "gvox_s": obj.dims.count / t / 1e9, "tflops": flops / t / 1e12}
+    # FMA pipe probe
+    probe = torch.empty(148 * 8 * 256, dtype=dtype, device="cuda")
+    import ctypes
+    fl = ctypes.c_double()
+    dcode = D.DTYPES[dtype]
+    iters = 2000 if dtype == torch.float64 else 4000
+    for _ in range(2):
+        N.check(N.lib.bd3mg_fma_probe(dcode, 148 * 8, iters, probe.data_ptr(), ctypes.byref(fl), D.stream_handle()))
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(5):
+        N.check(N.lib.bd3mg_fma_probe(dcode, 148 * 8, iters, probe.data_ptr(), ctypes.byref(fl), D.stream_handle()))
+    e.record()
+    torch.cuda.synchronize()
+    peak = fl.value * 5 / (s.elapsed_time(e) / 1e3) / 1e12
+    achieved = res["H"]["tflops"]
+    roof = {"bound": "fp64_fma" if dtype == torch.float64 else "fp32_fma", "kernel": "conv_tiled_kernel (H, full volume)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_source": "measured: bd3mg_fma_probe (dense FMA chains) on this GPU, this run "
+                           "(MEASURED_PEAKS.json has no FP64/FP32 entry)",
+            "algorithmic_flops_per_launch": flops, "traffic": None}
+    return roof, res
+
+
+def e2e(obj, cfg, x0, args, world, rank, torch, N, D):
+    """The same sweep through the reference-facing host-buffer C ABI
+    (bd3mg_problem_mg_direction_host: TaskMessage in, increment out -- the
+    worker boundary of the reference, runtime.py:92-105) with the master on
+    the host like the reference's, plus the per-sweep eval_f through the
+    public API.  Host<->device copies are inside the timed region."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2002_02328_b200 import objective
+
+    nz, ny, nx = obj.dims.shape
+    plane = ny * nx
+    kz = obj.psf.kdims.kz
+    B = -(-nz // cfg.block_height)
+    blocks = [(lo, min(lo + cfg.block_height - 1, nz - 1)) for lo in range(0, nz, cfg.block_height)]
+    if world > 1:
+        per = -(-B // world)
+        blocks = blocks[rank * per:(rank + 1) * per]
+    dcode = N.BD3MG_F64 if cfg.dtype == "f64" else N.BD3MG_F32
+    g = N.Geom(nx, ny, nz, *obj.psf.kdims, dcode)
+    r = D.reg(obj.params)
+    nthreads = 4
+    handles = []
+    for _ in range(nthreads):
+        h = ctypes.c_void_p()
+        N.check(N.lib.bd3mg_problem_create(ctypes.byref(g), ctypes.byref(r), obj.psf.kernels.ctypes.data,
+                                           obj.y.ctypes.data, torch.cuda.current_device(), ctypes.byref(h)))
+        handles.append(h)
+    pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    x = pin(x0.shape)
+    x[...] = x0
+    prev = pin(x0.shape)
+    prev[...] = 0.0
+    incs = [pin(((hi - lo + 1) * plane,)) for lo, hi in blocks]
+    infos = [np.zeros(N.INFO_DOUBLES) for _ in blocks]
+    pool = ThreadPoolExecutor(max_workers=nthreads)
+    h2d = d2h = 0
+
+    def one(i):
+        lo, hi = blocks[i]
+        s_lo, s_hi = max(0, lo - kz), min(nz - 1, hi + kz)
+        N.check(N.lib.bd3mg_problem_mg_direction_host(
+            handles[i % nthreads], x[s_lo:].ctypes.data, s_lo, s_hi - s_lo + 1, lo, hi,
+            prev[lo:].ctypes.data, incs[i].ctypes.data, infos[i].ctypes.data))
+        return (s_hi - s_lo + 1 + hi - lo + 1) * plane * 8, (hi - lo + 1) * plane * 8
+
+    def sweep():
+        nonlocal h2d, d2h
+        res = list(pool.map(one, range(len(blocks))))
+        for (lo, hi), inc in zip(blocks, incs):
+            inc3 = inc.reshape(hi - lo + 1, ny, nx)
+            x[lo:hi + 1] += inc3
+            prev[lo:hi + 1] = inc3
+        f = objective.eval_f(obj, x) if world == 1 else 0.0
+        h2d = sum(a for a, _ in res) + (x.nbytes if world == 1 else 0)
+        d2h = sum(b for _, b in res) + (8 * N.EVAL_DOUBLES if world == 1 else 0)
+        return f
+
+    for _ in range(2):
+        sweep()
+    steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sweep()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    for h in handles:
+        N.lib.bd3mg_problem_destroy(h)
+    return {"value": steps * B / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": steps, "path": "host buffers -> bd3mg_problem_mg_direction_host (4 host threads, one "
+                                    "stream each) + host master update + eval_f(numpy x)"}
+
+
+def cpu_baseline(cfg):
+    """Reference CPU path on this host, bounded sample: one block-Jacobi
+    sweep (B block-iterations) with the reference's compiled core."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "0",
+           "--config", cfg.name]
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+        return line["cpu_baseline"]
+    except Exception as exc:  # reported, never fatal
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+
+if __name__ == "__main__":
+    main()

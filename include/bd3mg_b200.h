@@ -77,6 +77,9 @@ typedef struct {
 
 const char* bd3mg_last_error(void);
 const char* bd3mg_version(void);
+/* Number of kernels this library has launched in the process (eager calls;
+ * a captured CUDA graph's replays are not counted). */
+long long bd3mg_launch_count(void);
 
 /* ---- drop-in native core: replaces bd3mg._core (src/_core.pyx:17-96) ---- */
 /* H rows: out[i] = sum_{a,b,c} K[zo,a,b,c] frag[zo+a-rz-frag_z0, y+b-ry, x+c-rx],
@@ -164,6 +167,13 @@ int bd3mg_problem_destroy(bd3mg_problem* p);
 int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int64_t slab_z0, int64_t nzs,
                                     int64_t z_lo, int64_t z_hi, const double* d_mem, double* inc_out,
                                     double* info_out);
+
+/* ---- measurement probe ------------------------------------------------- */
+/* Dense FMA throughput probe (fp64 or fp32): `blocks` x 256 threads, 8
+ * independent chains each, 128*iters FMAs per thread; *flops_out receives
+ * the flop count of the launch.  out: blocks*256 elements of dtype.  Used by
+ * bench.py to measure the FMA-pipe peak of the roofline. */
+int bd3mg_fma_probe(int32_t dtype, int32_t blocks, int32_t iters, void* out, double* flops_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ EVAL_DOUBLES = 7
 
 # every symbol the header declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
-    "bd3mg_last_error", "bd3mg_version",
+    "bd3mg_last_error", "bd3mg_version", "bd3mg_launch_count",
     "bd3mg_depthvar_correlate_f64", "bd3mg_depthvar_correlate_adjoint_f64",
     "bd3mg_depthvar_correlate_f32", "bd3mg_depthvar_correlate_adjoint_f32",
     "bd3mg_depthvar_correlate_host_f64", "bd3mg_depthvar_correlate_adjoint_host_f64",
@@ -29,6 +29,7 @@ EXPORTS = (
     "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
+    "bd3mg_fma_probe",
 )
 
 
@@ -72,6 +73,7 @@ def _load() -> C.CDLL:
     G, R, T = C.POINTER(Geom), C.POINTER(Reg), C.POINTER(Task)
     lib.bd3mg_last_error.restype = C.c_char_p
     lib.bd3mg_version.restype = C.c_char_p
+    lib.bd3mg_launch_count.restype = C.c_longlong
     lib.bd3mg_grad_rows_ws_bytes.argtypes = [G, _i64, _i64]
     lib.bd3mg_grad_rows_ws_bytes.restype = _sz
     lib.bd3mg_grad_rows.argtypes = [G, R, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]
@@ -89,6 +91,7 @@ def _load() -> C.CDLL:
     lib.bd3mg_problem_create.argtypes = [G, R, _vp, _vp, C.c_int, C.POINTER(C.c_void_p)]
     lib.bd3mg_problem_destroy.argtypes = [_vp]
     lib.bd3mg_problem_mg_direction_host.argtypes = [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]
+    lib.bd3mg_fma_probe.argtypes = [C.c_int32, C.c_int32, C.c_int32, _vp, _dp, _vp]
     return lib
 
 

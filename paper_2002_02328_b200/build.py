@@ -24,7 +24,7 @@ INCLUDE = PKG.parent / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
-UNITS = ["capi.cu", "conv_f64.cu", "conv_f32.cu"]
+UNITS = ["capi.cu", "conv_f64.cu", "conv_f32.cu", "microbench.cu"]
 
 
 def _deps() -> list[Path]:

@@ -5,6 +5,7 @@
 // MajorantOperator.apply (objective.py), mg_direction (directions.py) and the
 // block update of receive_update (scheduler.py).
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +21,8 @@ using namespace bd3mg;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<long long> g_launches{0};  // kernels launched by this library
+inline void launched(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
@@ -105,6 +108,7 @@ cudaError_t reduce(const double* rows, int nv, const std::vector<std::pair<long 
       rr.end[j] = ranges[b0 + j].second;
     }
     reduce_rows_kernel<<<rr.njobs, kEwNT, 0, s>>>(rows, nv, rr, out + b0 * out_stride, out_stride);
+    launched();
   }
   return cudaGetLastError();
 }
@@ -129,6 +133,7 @@ int correlate_rows(const T* frag, int64_t nzf, int64_t ny, int64_t nx, const T* 
   j.src0 = frag; j.src_z0 = frag_z0; j.src_nz = (int)nzf;
   j.dst0 = out; j.out_lo = (int)out_lo; j.nout = (int)nout; j.work_begin = 0;
   CU(conv_launch<T>(M_STORE, adj, a, (int)nout, s));
+  launched();
   return BD3MG_OK;
 }
 
@@ -156,6 +161,7 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   a.jobs[0].dst0 = rbuf; a.jobs[0].sub = y + o_lo * plane;
   a.jobs[0].out_lo = (int)o_lo; a.jobs[0].nout = (int)nr;
   CU(conv_launch<T>(M_RESID, false, a, (int)nr, s));
+  launched();
   ConvArgs<T> b = base_args<T>(g, r, K);
   b.njobs = 1;
   ConvJob<T>& j = b.jobs[0];
@@ -164,6 +170,7 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   j.xg = frag; j.xg_z0 = frag_z0; j.xg_nz = (int)nzf;
   j.out_lo = (int)lo; j.nout = (int)h;
   CU(conv_launch<T>(M_GRAD, true, b, (int)h, s));
+  launched();
   return BD3MG_OK;
 }
 
@@ -185,14 +192,15 @@ int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T
   a.jobs[0].dst0 = nullptr; a.jobs[0].sub = y;
   a.jobs[0].out_lo = 0; a.jobs[0].nout = (int)nz;
   CU(conv_launch<T>(M_RESID, false, a, (int)nz, s));
+  launched();
   CU(reduce(parts, 1, {{0, crow}}, sums, 1, s));
   EvalArgs<T> e;
   e.x = x; e.snap = snap; e.nz = (int)nz; e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane; e.n = n;
   e.delta2 = r->delta * r->delta; e.x_min = r->x_min; e.x_max = r->x_max; e.ctas = ctas;
-  eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts);
+  eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts); launched();
   CU(cudaGetLastError());
   CU(reduce(eparts, kEvalNV, {{0, ctas}}, sums + 1, kEvalNV, s));
-  eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms);
+  eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
 }
@@ -212,16 +220,18 @@ int majorant_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   a.jobs[0].src0 = v; a.jobs[0].src_z0 = lo; a.jobs[0].src_nz = (int)h;
   a.jobs[0].dst0 = hv; a.jobs[0].out_lo = (int)o_lo; a.jobs[0].nout = (int)nr;
   CU(conv_launch<T>(M_STORE, false, a, (int)nr, s));
+  launched();
   ConvArgs<T> b = base_args<T>(g, r, K);
   b.njobs = 1;
   b.jobs[0].src0 = hv; b.jobs[0].src_z0 = o_lo; b.jobs[0].src_nz = (int)nr;
   b.jobs[0].dst0 = out; b.jobs[0].out_lo = (int)lo; b.jobs[0].nout = (int)h;
   CU(conv_launch<T>(M_STORE, true, b, (int)h, s));
+  launched();
   MajArgs<T> m;
   m.v = v; m.omega = omega; m.out = out; m.lo = (int)lo; m.hi = (int)hi; m.nz = (int)nz;
   m.ny = (int)g->ny; m.nx = (int)g->nx; m.plane = plane; m.n = h * plane;
   m.two_eta = 2.0 * r->eta; m.lam = r->lam; m.two_kappa = 2.0 * r->kappa;
-  majorant_reg_kernel<T><<<(unsigned)((m.n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(m);
+  majorant_reg_kernel<T><<<(unsigned)((m.n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(m); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
 }
@@ -233,7 +243,7 @@ int omega_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* frag, int64
   if (frag_z0 > lo || frag_z0 + nzf - 1 < hi) return fail(BD3MG_EINVAL, "fragment does not cover the rows");
   const int64_t plane = g->ny * g->nx, n = (hi - lo + 1) * plane;
   XView<T> xv{frag, frag_z0, (int)nzf, (int)g->ny, (int)g->nx, plane};
-  omega_kernel<T><<<(unsigned)((n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(xv, (int)lo, n, (T)(r->delta * r->delta), out);
+  omega_kernel<T><<<(unsigned)((n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(xv, (int)lo, n, (T)(r->delta * r->delta), out); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
 }
@@ -322,6 +332,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       }
     }
     CU(conv_launch<T>(M_RESID, false, a, (int)resid_work, s));
+  launched();
   }
   // (2) g = H^T r + regulariser gradient; omega
   {
@@ -339,6 +350,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     long long work = 0;
     for (int t = 0; t < nt; ++t) work += h[t];
     CU(conv_launch<T>(M_GRAD, true, a, (int)work, s));
+  launched();
   }
   // (3) regulariser Gram terms + rhs + flags
   {
@@ -352,7 +364,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       B.lo = (int)tasks[t].z_lo; B.hi = (int)tasks[t].z_hi; B.ctas = rctas[t]; B.row_begin = rb0;
       rb0 += rctas[t];
     }
-    reg_gram_kernel<T><<<dim3(max_ctas, nt), kEwNT, 0, s>>>(ra, rparts);
+    reg_gram_kernel<T><<<dim3(max_ctas, nt), kEwNT, 0, s>>>(ra, rparts); launched();
     CU(cudaGetLastError());
   }
   // (4) data Gram <H b_i, H b_j> (forward only, both columns share the taps)
@@ -373,6 +385,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       wbeg += j.nout;
     }
     CU(conv_launch<T>(gmode, false, a, (int)gram_work, s));
+  launched();
   }
   // (5) reductions
   CU(reduce(cparts, any_d ? 3 : 1, granges, data3, 3, s));
@@ -390,7 +403,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     sa.two_eta = 2.0 * r->eta; sa.lam = r->lam; sa.two_kappa = 2.0 * r->kappa;
     sa.prune_tol = kPruneTol; sa.pinv_tol = kPinvTol;
     for (int t = 0; t < nt; ++t) sa.has_d[t] = tasks[t].d_mem != nullptr;
-    solve2x2_kernel<<<1, 32, 0, s>>>(sa, data3, reg12, info_out);
+    solve2x2_kernel<<<1, 32, 0, s>>>(sa, data3, reg12, info_out); launched();
     CU(cudaGetLastError());
   }
   // (7) increments / in-place update
@@ -407,7 +420,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       B.ctas = (int)std::max<int64_t>(1, std::min<int64_t>((B.n + 4 * kEwNT - 1) / (4 * kEwNT), 1024));
       mc = std::max(mc, B.ctas);
     }
-    update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, info_out);
+    update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, info_out); launched();
     CU(cudaGetLastError());
   }
   return BD3MG_OK;
@@ -455,6 +468,7 @@ extern "C" {
 
 const char* bd3mg_last_error(void) { return g_err.c_str(); }
 const char* bd3mg_version(void) { return "bd3mg_b200 0.1 sm_100a"; }
+long long bd3mg_launch_count(void) { return g_launches.load(); }
 
 int bd3mg_depthvar_correlate_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx, const double* kernels,
                                  int64_t nzk, int64_t kz, int64_t ky, int64_t kx, int64_t frag_z0, int64_t out_lo,
@@ -611,6 +625,7 @@ int bd3mg_apply_increment(int32_t dtype, void* x_rows, void* dmem_rows, const vo
                                                                            (const float*)inc, n);
   else
     return fail(BD3MG_EINVAL, "unknown dtype %d", dtype);
+  launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
 }

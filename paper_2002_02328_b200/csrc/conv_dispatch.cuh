@@ -25,11 +25,18 @@ ConvGrid conv_grid(int ky, int kx, int mode, int ny, int nx) {
   return {(nx + TX - 1) / TX, (ny + TY - 1) / TY};
 }
 
-// per-device "max dynamic smem" attribute, set once per kernel instantiation
+// per-device "max dynamic smem" attribute, raised at most once per kernel
+// instantiation and device (never inside a stream capture after warm-up)
 template <typename Kern>
-inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes) {
+inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes, size_t* granted) {
   if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && granted[dev] >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess && dev < 64) granted[dev] = 227 * 1024;
+  return e;
 }
 
 template <typename T, int K, int MODE, bool ADJ>
@@ -37,7 +44,8 @@ cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   using Cfg = ConvCfg<T, K, K, MODE>;
   const size_t sm = Cfg::smem_bytes(p.kz);
   auto kern = conv_tiled_kernel<T, K, K, MODE, ADJ>;
-  cudaError_t e = ensure_smem_attr(kern, sm);
+  static size_t granted[64] = {0};  // one table per instantiation
+  cudaError_t e = ensure_smem_attr(kern, sm, granted);
   if (e != cudaSuccess) return e;
   dim3 grid(p.tiles_x, p.tiles_y, total_work);
   kern<<<grid, Cfg::NT, sm, s>>>(p);
@@ -49,7 +57,8 @@ cudaError_t launch_generic(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   size_t coef = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
   const size_t sm = coef + 8 * (kGenericNT / 32) * sizeof(double);
   auto kern = conv_generic_kernel<T, MODE, ADJ>;
-  cudaError_t e = ensure_smem_attr(kern, sm);
+  static size_t granted[64] = {0};  // one table per instantiation
+  cudaError_t e = ensure_smem_attr(kern, sm, granted);
   if (e != cudaSuccess) return e;
   dim3 grid(p.tiles_x, p.tiles_y, total_work);
   kern<<<grid, kGenericNT, sm, s>>>(p);

@@ -442,3 +442,79 @@ def write_log_csv(log: list[IterationLogEntry], sink) -> None:
     finally:
         if close:
             sink.close()
+
+
+# ---------------------------------------------------------------------------
+class JacobiSweeper:
+    """Device-resident block-Jacobi driver: ``run_bp3mg_barrier`` with
+    workers = #blocks, where every cycle is one sweep (runtime.py:244-292).
+
+    One sweep = one batched ``bd3mg_mg_steps`` launch set (all blocks at the
+    common anchor, in-place update of x and the memory store) followed by the
+    per-sweep recorder pass (f(x) and the stop-rule norms against the
+    previous sweep's snapshot, runtime.py:120 / scheduler.py:208-219) and the
+    snapshot roll.  All buffers are preallocated and every launch goes to
+    the current stream, so a sweep can be captured as a CUDA graph.
+    """
+
+    def __init__(self, obj: Objective, x0, block_height: int, dtype: torch.dtype = torch.float64,
+                 blocks: list | None = None):
+        self.obj = obj
+        self.dtype = dtype
+        self.x = D.to_device(x0, dtype).clone()
+        self.prev = torch.zeros_like(self.x)
+        self.snap = self.x.clone()
+        dims = obj.dims
+        self.blocks = blocks or scheduler.partition_blocks(dims.nz, block_height)
+        self.tasks = (N.Task * len(self.blocks))(*[
+            N.Task(self.x.data_ptr(), 0, dims.nz, b.z_lo, b.z_hi, _rows(self.prev, b.z_lo, b.z_hi).data_ptr(),
+                   None, _rows(self.x, b.z_lo, b.z_hi).data_ptr(), _rows(self.prev, b.z_lo, b.z_hi).data_ptr())
+            for b in self.blocks])
+        self.geom = obj.geom(dtype)
+        self.reg = D.reg(obj.params)
+        self.ws_bytes = N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(self.geom), self.tasks, len(self.blocks)))
+        self.eval_bytes = N.ws_bytes(N.lib.bd3mg_eval_f_ws_bytes(D.byref(self.geom)))
+        dev = self.x.device
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.ews = torch.empty(self.eval_bytes, dtype=torch.uint8, device=dev)
+        self.info = torch.empty((len(self.blocks), N.INFO_DOUBLES), dtype=torch.float64, device=dev)
+        self.terms = torch.empty(N.EVAL_DOUBLES, dtype=torch.float64, device=dev)
+        self.K = obj.psf.device_kernels(dtype, dev)
+        self.Y = obj.device_y(dtype, dev)
+        self.k = 0
+        self.graph = None
+
+    @property
+    def nblocks(self) -> int:
+        return len(self.blocks)
+
+    def _launch(self) -> None:
+        s = D.stream_handle()
+        N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
+                                     self.tasks, len(self.blocks), self.info.data_ptr(), self.ws.data_ptr(),
+                                     self.ws_bytes, s))
+        N.check(N.lib.bd3mg_eval_f(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
+                                   self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
+                                   self.ews.data_ptr(), self.eval_bytes, s))
+        self.snap.copy_(self.x)
+
+    def capture(self) -> None:
+        """Record one sweep as a CUDA graph (after one eager warm-up sweep)."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch()
+        self.graph = g
+
+    def sweep(self) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch()
+        self.k += len(self.blocks)
+
+    def check(self) -> None:
+        if bool((self.info[:, 8] != 0).any().item()):
+            raise ValueError("non-finite gradient")
+
+    def f(self) -> float:
+        return float(self.terms[4].item())
