@@ -366,15 +366,23 @@ def e2e(obj, cfg, x0, args, world, rank, torch, N, D):
     prev[...] = 0.0
     incs = [pin(((hi - lo + 1) * plane,)) for lo, hi in blocks]
     infos = [np.zeros(N.INFO_DOUBLES) for _ in blocks]
+    import queue
     pool = ThreadPoolExecutor(max_workers=nthreads)
+    free = queue.Queue()  # a handle (stream + buffers) is used by one thread at a time
+    for h in handles:
+        free.put(h)
     h2d = d2h = 0
 
     def one(i):
         lo, hi = blocks[i]
         s_lo, s_hi = max(0, lo - kz), min(nz - 1, hi + kz)
-        N.check(N.lib.bd3mg_problem_mg_direction_host(
-            handles[i % nthreads], x[s_lo:].ctypes.data, s_lo, s_hi - s_lo + 1, lo, hi,
-            prev[lo:].ctypes.data, incs[i].ctypes.data, infos[i].ctypes.data))
+        h = free.get()
+        try:
+            N.check(N.lib.bd3mg_problem_mg_direction_host(
+                h, x[s_lo:].ctypes.data, s_lo, s_hi - s_lo + 1, lo, hi,
+                prev[lo:].ctypes.data, incs[i].ctypes.data, infos[i].ctypes.data))
+        finally:
+            free.put(h)
         return (s_hi - s_lo + 1 + hi - lo + 1) * plane * 8, (hi - lo + 1) * plane * 8
 
     def sweep():

@@ -3,6 +3,9 @@
 // generic one-voxel-per-thread kernel.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "depthvar.cuh"
 
 namespace bd3mg {
@@ -39,9 +42,24 @@ inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes, size_t* granted) {
   return e;
 }
 
+// TMA descriptor of a fragment (nx, ny, nz) with a (boxw, boxh, 1) box;
+// out-of-bounds elements are zero-filled by the copy engine.  Returns false
+// when the layout is not TMA-legal (row pitch / base not 16-byte aligned).
+bool encode_tmap(CUtensorMap* map, const void* base, bool f64, long long nx, long long ny, long long nz, int boxw,
+                 int boxh);
+
 template <typename T, int K, int MODE, bool ADJ>
 cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   using Cfg = ConvCfg<T, K, K, MODE>;
+  static const bool no_tma = getenv("BD3MG_NO_TMA") != nullptr;  // diagnostics: force cp.async staging
+  for (int j = 0; j < p.njobs; ++j) {
+    ConvJob<T>& jb = p.jobs[j];
+    const bool f64 = sizeof(T) == 8;
+    bool ok = encode_tmap(&jb.tmap0, jb.src0, f64, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH);
+    if (ok && Cfg::NIN == 2) ok = encode_tmap(&jb.tmap1, jb.src1, f64, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH);
+    jb.use_tma = (ok && !no_tma) ? 1 : 0;
+    if (getenv("BD3MG_DEBUG_TMA")) fprintf(stderr, "conv K=%d mode=%d job=%d tma=%d box=%dx%d\n", K, MODE, j, (int)jb.use_tma, Cfg::PITCH, Cfg::BOXH);
+  }
   const size_t sm = Cfg::smem_bytes(p.kz);
   auto kern = conv_tiled_kernel<T, K, K, MODE, ADJ>;
   static size_t granted[64] = {0};  // one table per instantiation

@@ -27,6 +27,8 @@
 // so every LDS is conflict-free.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace bd3mg {
@@ -42,7 +44,9 @@ enum ConvMode : int {
 constexpr int kMaxJobs = 32;
 
 template <typename T>
-struct ConvJob {
+struct alignas(64) ConvJob {
+  CUtensorMap tmap0;    // TMA descriptors of src0/src1 (filled by conv_launch)
+  CUtensorMap tmap1;
   const T* src0;        // fragment base; plane 0 is global depth src_z0
   const T* src1;        // second fragment (M_GRAM2), same geometry
   T* dst0;              // output rows; row 0 is global depth out_lo
@@ -54,7 +58,7 @@ struct ConvJob {
   int src_nz, xg_nz;
   int out_lo, nout;     // global output rows [out_lo, out_lo+nout)
   int work_begin;       // prefix of nout over jobs (grid.z index of first plane)
-  int pad_;
+  int use_tma;          // 1: stage tiles with TMA; 0: cp.async fallback
 };
 
 template <typename T>
@@ -146,25 +150,44 @@ BD3MG_D T grad_voxel(T hta, const XView<T>& xv, int z, int y, int x, int nz_glob
 }
 
 // ---------------------------------------------------------------------------
+// Tile configuration.  fp64: RX=2 (one 16-byte LDS per 2 window values);
+// fp32: RX=4.  Consecutive lanes of a quarter-warp read consecutive 16-byte
+// chunks of one dense smem row, so every window load is conflict-free.
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
 template <typename T, int KY_, int KX_, int MODE>
 struct ConvCfg {
   static constexpr bool DUAL = (MODE == M_GRAM2);
   static constexpr int KY = KY_, KX = KX_;
-  static constexpr int RX = 4;
-  static constexpr int RY = DUAL ? 4 : 8;
+  static constexpr int VEC = 16 / sizeof(T);        // elements per 16-byte load
+  static constexpr int RX = VEC;                    // outputs per thread in x
+  static constexpr int RY = DUAL ? 8 : 16;          // outputs per thread in y
   static constexpr int WX = 16, WY = 8;
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
-  static constexpr int TXH = TX + KX - 1, TYH = TY + KY - 1;
-  static constexpr int Q = (TXH + RX - 1) / RX;
-  static constexpr int PITCH = RX * Q;
+  // TMA boxes must start on a 16-byte boundary in x (measured: odd-element
+  // starts fault), so the box origin is x0 - RXA with RXA = RXH rounded up to
+  // VEC; OFF = RXA - RXH extra leading columns are read and skipped.
+  static constexpr int RXH = (KX - 1) / 2, RYH = (KY - 1) / 2;
+  static constexpr int RXA = (RXH + VEC - 1) / VEC * VEC, OFF = RXA - RXH;
+  static constexpr int TXH = TX + KX - 1 + OFF, TYH = TY + KY - 1;
+  // smem row = TMA box width, padded to 32 bytes; box height padded so the
+  // box is a whole number of 128-byte lines (boxes with an odd number of
+  // 16-byte chunks per row fault on sm_100a -- measured, scripts/tma_probe.py)
+  static constexpr int PITCH = (TXH + 2 * VEC - 1) / (2 * VEC) * (2 * VEC);
+  static constexpr int ROWQ = 128 / cgcd(PITCH * (int)sizeof(T), 128);
+  static constexpr int BOXH = (TYH + ROWQ - 1) / ROWQ * ROWQ;
+  static constexpr int WIN = RX + KX - 1;
+  static constexpr int WINP = (OFF + WIN + VEC - 1) / VEC * VEC;  // aligned window incl. OFF lead
   static constexpr int NIN = DUAL ? 2 : 1;
-  static constexpr int TILE = TYH * PITCH;  // elements per input per buffer
+  static constexpr int BOX = BOXH * PITCH;          // elements one TMA box delivers
+  static constexpr int TILE = (BOX + 128 / (int)sizeof(T) - 1) / (128 / (int)sizeof(T)) * (128 / (int)sizeof(T));
   static constexpr int NV = ModeNV<MODE>::value;
+  static constexpr size_t TILE_BYTES = (size_t)TILE * sizeof(T);  // 128-byte aligned buffer stride
+  static constexpr size_t BOX_BYTES = (size_t)BOX * sizeof(T);
+  BD3MG_HD static size_t coef_bytes(int kz) { return ((size_t)kz * KY * KX * sizeof(T) + 127) & ~size_t(127); }
   static size_t smem_bytes(int kz) {
-    size_t coef = (size_t)kz * KY * KX * sizeof(T);
-    coef = (coef + 15) & ~size_t(15);
-    return coef + 2 * NIN * (size_t)TILE * sizeof(T) + 8 * (NT / 32) * sizeof(double);
+    return coef_bytes(kz) + 2 * NIN * TILE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
   }
 };
 
@@ -195,32 +218,47 @@ BD3MG_D void stage_coefs(const ConvArgs<T>& p, int zo, T* cs, int nt) {
   }
 }
 
-// Load one (TYH x TXH) halo tile of input plane `zi` into de-interleaved smem.
+// Fallback staging when TMA is not usable (row pitch not a multiple of 16
+// bytes): element-wise cp.async with zero fill into the same dense layout.
 template <typename Cfg, typename T>
-BD3MG_D void stage_tile(T* dst, const T* src, long long src_z0, int zi, int y0, int x0, int ny, int nx,
-                        long long plane) {
-  constexpr int RYH = (Cfg::KY - 1) / 2, RXH = (Cfg::KX - 1) / 2;
+BD3MG_D void stage_tile_fallback(T* dst, const T* src, long long src_z0, int zi, int y0, int x0, int ny, int nx,
+                                 long long plane) {
   const T* base = src + (long long)(zi - src_z0) * plane;
-  for (int idx = threadIdx.x; idx < Cfg::TYH * Cfg::TXH; idx += Cfg::NT) {
-    const int row = idx / Cfg::TXH, e = idx - row * Cfg::TXH;
-    const int gy = y0 - RYH + row, gx = x0 - RXH + e;
+  for (int idx = threadIdx.x; idx < Cfg::BOX; idx += Cfg::NT) {
+    const int row = idx / Cfg::PITCH, e = idx - row * Cfg::PITCH;
+    const int gy = y0 - Cfg::RYH + row, gx = x0 - Cfg::RXA + e;
     const bool ok = (gy >= 0) && (gy < ny) && (gx >= 0) && (gx < nx);
     const T* g = ok ? base + (long long)gy * nx + gx : src;
-    cp_async<sizeof(T)>(dst + row * Cfg::PITCH + (e % Cfg::RX) * Cfg::Q + e / Cfg::RX, g, ok);
+    cp_async<sizeof(T)>(dst + idx, g, ok);
   }
 }
+
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<double> {
+  using type = double2;
+};
+template <>
+struct Vec16<float> {
+  using type = float4;
+};
 
 template <typename T, int KY, int KX, int MODE, bool ADJ>
 __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
     conv_tiled_kernel(const __grid_constant__ ConvArgs<T> p) {
   using Cfg = ConvCfg<T, KY, KX, MODE>;
-  constexpr int RX = Cfg::RX, RY = Cfg::RY, NIN = Cfg::NIN;
-  constexpr int WIN = RX + KX - 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* coef_s = reinterpret_cast<T*>(smem_raw);
-  size_t coef_bytes = ((size_t)p.kz * KY * KX * sizeof(T) + 15) & ~size_t(15);
-  T* tiles = reinterpret_cast<T*>(smem_raw + coef_bytes);
-  double* red_s = reinterpret_cast<double*>(tiles + 2 * NIN * Cfg::TILE);
+  using V = typename Vec16<T>::type;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, NIN = Cfg::NIN, VEC = Cfg::VEC;
+  constexpr int WINP = Cfg::WINP, OFF = Cfg::OFF;
+  constexpr int RYH = Cfg::RYH, RXA = Cfg::RXA;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // 128-byte aligned carve-out: [tiles][coefs][mbarriers][reduction scratch]
+  unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // stays in .shared
+  T* tiles = reinterpret_cast<T*>(sbase);
+  T* coef_s = reinterpret_cast<T*>(sbase + 2 * NIN * Cfg::TILE_BYTES);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::coef_bytes(p.kz));
+  double* red_s = reinterpret_cast<double*>(mbar + 2);
 
   const int zidx = blockIdx.z;
   const int jid = find_job(p, zidx);
@@ -229,13 +267,38 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
   const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
   const int rz = (p.kz - 1) / 2;
+  const bool tma = job.use_tma != 0;
 
   // taps a whose input plane zo+a-rz lies inside the fragment
   const long long zlo_in = job.src_z0, zhi_in = job.src_z0 + job.src_nz - 1;
   const int a_lo = (int)max(0LL, zlo_in - zo + rz);
   const int a_hi = (int)min((long long)p.kz - 1, zhi_in - zo + rz);
 
+  if (tma && threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
   stage_coefs<T, ADJ>(p, zo, coef_s, Cfg::NT);
+  __syncthreads();
+
+  auto issue = [&](int a, int b) {
+    T* dst = tiles + b * NIN * Cfg::TILE;
+    const int zi = zo + a - rz;
+    if (tma) {
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&mbar[b], (uint32_t)(NIN * Cfg::BOX_BYTES));
+        tma_load_3d(dst, &job.tmap0, x0 - RXA, y0 - RYH, (int)(zi - job.src_z0), &mbar[b]);
+        if constexpr (NIN == 2)
+          tma_load_3d(dst + Cfg::TILE, &job.tmap1, x0 - RXA, y0 - RYH, (int)(zi - job.src_z0), &mbar[b]);
+      }
+    } else {
+      stage_tile_fallback<Cfg>(dst, job.src0, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
+      if constexpr (NIN == 2)
+        stage_tile_fallback<Cfg>(dst + Cfg::TILE, job.src1, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
+      cp_async_commit();
+    }
+  };
 
   T acc[NIN][RY][RX];
 #pragma unroll
@@ -245,34 +308,35 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
 #pragma unroll
       for (int i = 0; i < RX; ++i) acc[s][r][i] = T(0);
 
-  if (a_lo <= a_hi) {
-    stage_tile<Cfg>(tiles, job.src0, job.src_z0, zo + a_lo - rz, y0, x0, p.ny, p.nx, p.plane);
-    if constexpr (NIN == 2)
-      stage_tile<Cfg>(tiles + Cfg::TILE, job.src1, job.src_z0, zo + a_lo - rz, y0, x0, p.ny, p.nx, p.plane);
-    cp_async_commit();
-  }
+  if (a_lo <= a_hi) issue(a_lo, 0);
+  uint32_t phase = 0;  // bit b = parity of buffer b
   int buf = 0;
   for (int a = a_lo; a <= a_hi; ++a) {
-    if (a < a_hi) {
-      T* nb = tiles + (buf ^ 1) * NIN * Cfg::TILE;
-      stage_tile<Cfg>(nb, job.src0, job.src_z0, zo + a + 1 - rz, y0, x0, p.ny, p.nx, p.plane);
-      if constexpr (NIN == 2)
-        stage_tile<Cfg>(nb + Cfg::TILE, job.src1, job.src_z0, zo + a + 1 - rz, y0, x0, p.ny, p.nx, p.plane);
-      cp_async_commit();
-      cp_async_wait<1>();
+    if (a < a_hi) issue(a + 1, buf ^ 1);
+    if (tma) {
+      mbar_wait(&mbar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
     } else {
-      cp_async_wait<0>();
+      if (a < a_hi) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncthreads();
     }
-    __syncthreads();
     const T* cs = coef_s + a * (KY * KX);
-    const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx;
+    const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
 #pragma unroll
     for (int yi = 0; yi < RY + KY - 1; ++yi) {
-      T v[NIN][WIN];
+      T v[NIN][WINP];
 #pragma unroll
       for (int s = 0; s < NIN; ++s)
 #pragma unroll
-        for (int j = 0; j < WIN; ++j) v[s][j] = tb[s * Cfg::TILE + yi * Cfg::PITCH + (j % RX) * Cfg::Q + j / RX];
+        for (int j = 0; j < WINP; j += VEC) {
+          const V q = *reinterpret_cast<const V*>(tb + s * Cfg::TILE + yi * Cfg::PITCH + j);
+          if constexpr (VEC == 2) {
+            v[s][j] = q.x; v[s][j + 1] = q.y;
+          } else {
+            v[s][j] = q.x; v[s][j + 1] = q.y; v[s][j + 2] = q.z; v[s][j + 3] = q.w;
+          }
+        }
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         const int b = yi - r;
@@ -283,7 +347,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
 #pragma unroll
           for (int s = 0; s < NIN; ++s)
 #pragma unroll
-            for (int i = 0; i < RX; ++i) acc[s][r][i] = fma_rn(k, v[s][i + c], acc[s][r][i]);
+            for (int i = 0; i < RX; ++i) acc[s][r][i] = fma_rn(k, v[s][OFF + i + c], acc[s][r][i]);
         }
       }
     }
