@@ -127,6 +127,17 @@ size_t bd3mg_eval_f_ws_bytes(const bd3mg_geom_t* g);
 int bd3mg_eval_f(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
                  const void* x, const void* snap, double* terms_out, void* ws, size_t ws_bytes, void* stream);
 
+/* Objective terms restricted to rows [lo, hi] (a rank's owned planes in the
+ * multi-GPU layout): data term over H rows [lo, hi] of `frag` minus y_rows
+ * (row lo of y), box / TV / axial terms of rows [lo, hi]; frag must cover
+ * [lo, hi+1] and, for exact data terms, [lo-2rz, hi+2rz].  snap_rows (row lo
+ * of the sweep snapshot) may be NULL.  Terms as bd3mg_eval_f (sums over the
+ * rows; add across ranks for the global value). */
+size_t bd3mg_eval_rows_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi);
+int bd3mg_eval_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y_rows,
+                    const void* frag, int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, const void* snap_rows,
+                    double* terms_out, void* ws, size_t ws_bytes, void* stream);
+
 /* Half-quadratic weights 1/sqrt(dx^2+dy^2+delta^2) of rows [lo, hi] of a
  * fragment: objective.py:130-132 (_omega), as cached by MajorantOperator
  * (objective.py:233-235).  omega_out: (hi-lo+1, ny, nx). */
@@ -141,7 +152,8 @@ int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void
                          void* stream);
 
 /* Batched memory-gradient block steps (mg_direction + receive_update) with
- * the forward-only Gram.  Tasks sharing one anchor fragment compute the
+ * the forward-only Gram.  `y` must satisfy: y + z*ny*nx is observation row z
+ * for every row the tasks touch (a shard may pass its local rows shifted).  Tasks sharing one anchor fragment compute the
  * residual H x - y once over the union of their rows (block-Jacobi cycle of
  * run_bp3mg_barrier, runtime.py:244-292).  info_out: device, ntasks*16. */
 size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks);

@@ -25,7 +25,7 @@ EXPORTS = (
     "bd3mg_depthvar_correlate_f32", "bd3mg_depthvar_correlate_adjoint_f32",
     "bd3mg_depthvar_correlate_host_f64", "bd3mg_depthvar_correlate_adjoint_host_f64",
     "bd3mg_grad_rows_ws_bytes", "bd3mg_grad_rows",
-    "bd3mg_eval_f_ws_bytes", "bd3mg_eval_f",
+    "bd3mg_eval_f_ws_bytes", "bd3mg_eval_f", "bd3mg_eval_rows_ws_bytes", "bd3mg_eval_rows",
     "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
@@ -80,6 +80,9 @@ def _load() -> C.CDLL:
     lib.bd3mg_eval_f_ws_bytes.argtypes = [G]
     lib.bd3mg_eval_f_ws_bytes.restype = _sz
     lib.bd3mg_eval_f.argtypes = [G, R, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.bd3mg_eval_rows_ws_bytes.argtypes = [G, _i64, _i64]
+    lib.bd3mg_eval_rows_ws_bytes.restype = _sz
+    lib.bd3mg_eval_rows.argtypes = [G, R, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]
     lib.bd3mg_omega_rows.argtypes = [G, R, _vp, _i64, _i64, _i64, _i64, _vp, _vp]
     lib.bd3mg_majorant_apply_ws_bytes.argtypes = [G, _i64, _i64]
     lib.bd3mg_majorant_apply_ws_bytes.restype = _sz

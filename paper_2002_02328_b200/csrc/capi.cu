@@ -176,11 +176,19 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   return BD3MG_OK;
 }
 
+// Objective terms over rows [lo, hi] from a fragment covering [lo-2rz, hi+2rz]
+// (clamped): data term of H rows minus y rows, box / TV / axial over the rows.
 template <typename T>
-int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const T* x, const T* snap,
-                double* terms, Ws& ws, cudaStream_t s) {
-  const int64_t nz = g->nz, plane = g->ny * g->nx, n = nz * plane;
-  const long long crow = conv_rows<T>(g, M_RESID, nz);
+int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y_rows, const T* frag,
+                   int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, const T* snap_rows, double* terms, Ws& ws,
+                   cudaStream_t s) {
+  const int64_t nz = g->nz, plane = g->ny * g->nx;
+  if (lo < 0 || hi < lo || hi >= nz) return fail(BD3MG_EINVAL, "invalid rows [%lld, %lld]", (long long)lo, (long long)hi);
+  const int64_t need_hi = std::min<int64_t>(nz - 1, hi + 1);
+  if (frag_z0 > lo || frag_z0 + nzf - 1 < need_hi)
+    return fail(BD3MG_EINVAL, "fragment does not cover rows [%lld, %lld]", (long long)lo, (long long)need_hi);
+  const int64_t nr = hi - lo + 1, n = nr * plane;
+  const long long crow = conv_rows<T>(g, M_RESID, nr);
   double* parts = ws.take<double>(crow);
   const int ctas = (int)std::min<int64_t>((n + kEwNT - 1) / kEwNT, 4 * 148);
   double* eparts = ws.take<double>((size_t)ctas * kEvalNV);
@@ -190,14 +198,15 @@ int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
   a.partials = parts;
-  a.jobs[0].src0 = x; a.jobs[0].src_z0 = 0; a.jobs[0].src_nz = (int)nz;
-  a.jobs[0].dst0 = nullptr; a.jobs[0].sub = y;
-  a.jobs[0].out_lo = 0; a.jobs[0].nout = (int)nz;
-  CU(conv_launch<T>(M_RESID, false, a, (int)nz, s));
+  a.jobs[0].src0 = frag; a.jobs[0].src_z0 = frag_z0; a.jobs[0].src_nz = (int)nzf;
+  a.jobs[0].dst0 = nullptr; a.jobs[0].sub = y_rows;
+  a.jobs[0].out_lo = (int)lo; a.jobs[0].nout = (int)nr;
+  CU(conv_launch<T>(M_RESID, false, a, (int)nr, s));
   launched();
   CU(reduce(parts, 1, {{0, crow}}, sums, 1, s));
   EvalArgs<T> e;
-  e.x = x; e.snap = snap; e.nz = (int)nz; e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane; e.n = n;
+  e.x = frag + (lo - frag_z0) * plane; e.snap = snap_rows; e.lo = (int)lo; e.nz = (int)nz;
+  e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane; e.n = n;
   e.delta2 = r->delta * r->delta; e.x_min = r->x_min; e.x_max = r->x_max; e.ctas = ctas;
   eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts); launched();
   CU(cudaGetLastError());
@@ -205,6 +214,12 @@ int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T
   eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
+}
+
+template <typename T>
+int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const T* x, const T* snap,
+                double* terms, Ws& ws, cudaStream_t s) {
+  return eval_rows_impl<T>(g, r, K, y, x, 0, g->nz, 0, g->nz - 1, snap, terms, ws, s);
 }
 
 template <typename T>
@@ -628,6 +643,33 @@ int bd3mg_eval_f(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernel
                                         (const double*)snap, terms_out, ws, (cudaStream_t)stream),
                     eval_f_impl<float>(g, r, (const float*)kernels, (const float*)y, (const float*)x,
                                        (const float*)snap, terms_out, ws, (cudaStream_t)stream));
+}
+
+size_t bd3mg_eval_rows_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, eval_rows_impl<double>(g, &r, nullptr, nullptr, nullptr, 0, g->nz, lo, hi, nullptr, nullptr,
+                                                ws, 0),
+                      eval_rows_impl<float>(g, &r, nullptr, nullptr, nullptr, 0, g->nz, lo, hi, nullptr, nullptr,
+                                            ws, 0));
+  });
+}
+
+int bd3mg_eval_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y_rows,
+                    const void* frag, int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, const void* snap_rows,
+                    double* terms_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    eval_rows_impl<double>(g, r, (const double*)kernels, (const double*)y_rows, (const double*)frag,
+                                           frag_z0, nzf, lo, hi, (const double*)snap_rows, terms_out, ws,
+                                           (cudaStream_t)stream),
+                    eval_rows_impl<float>(g, r, (const float*)kernels, (const float*)y_rows, (const float*)frag,
+                                          frag_z0, nzf, lo, hi, (const float*)snap_rows, terms_out, ws,
+                                          (cudaStream_t)stream));
 }
 
 int bd3mg_omega_rows(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* frag, int64_t frag_z0, int64_t nzf,

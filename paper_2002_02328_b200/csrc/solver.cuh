@@ -250,10 +250,10 @@ __global__ void __launch_bounds__(kEwNT) update_kernel(const __grid_constant__ U
 // the stop-rule norms (scheduler.py:218-219).
 template <typename T>
 struct EvalArgs {
-  const T* x;
-  const T* snap;  // may be null
-  int nz, ny, nx;
-  long long plane, n;
+  const T* x;     // row `lo` of the iterate; row lo+1.. follow (axial needs row hi+1)
+  const T* snap;  // row `lo` of the snapshot, may be null
+  int lo, nz, ny, nx;
+  long long plane, n;  // n = rows * plane
   double delta2, x_min, x_max;
   int ctas;
 };
@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(kEwNT) eval_terms_kernel(const __grid_constant
                                                             double* __restrict__ partials) {
   __shared__ double red[(kEwNT / 32) * kEvalNV];
   double v[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  const XView<T> xv{p.x, 0, p.nz, p.ny, p.nx, p.plane};
+  const XView<T> xv{p.x, p.lo, p.nz, p.ny, p.nx, p.plane};
   for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < p.n; i += (long long)p.ctas * kEwNT) {
-    const int z = (int)(i / p.plane);
+    const int z = p.lo + (int)(i / p.plane);
     const long long rem = i % p.plane;
     const int y = (int)(rem / p.nx), x = (int)(rem % p.nx);
     const double xc = (double)p.x[i];

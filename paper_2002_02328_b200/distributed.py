@@ -1,0 +1,266 @@
+"""Multi-GPU block-Jacobi over z-slabs (one process per GPU).
+
+Layout: the B blocks are split into P contiguous
+ranges, rank p owns the planes of its blocks.  Each rank keeps a local slab
+= its owned planes plus kz halo planes per side (the reference's
+slab_support reach, blur.py:190-198), clamped to the volume.  Blocks never
+span ranks, so a sweep is:
+
+  1. halo exchange -- every rank receives the halo planes it does not own
+     from their owners (torch.distributed P2P, NCCL over NVLink on GPUs,
+     grouped in one batch_isend_irecv); halos can span several ranks when a
+     rank owns fewer than kz planes;
+  2. the per-sweep recorder pass on owned rows (f terms + stop-rule norms),
+     then ONE all-reduce of the 7 terms;
+  3. the fused block steps of every owned block at the common anchor
+     (bd3mg_mg_steps, in place).
+
+Per-block arithmetic is identical to the single-GPU sweep (same rows, same
+fixed reduction trees), so the iterate is bitwise independent of P.  The
+recorder pass of sweep k runs at the start of sweep k+1 (after the halo
+exchange that makes x_k current on every rank); ``finish()`` evaluates the
+last one.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .volume import SliceBlock
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Block ownership and halo plan for `world` ranks."""
+
+    nz: int
+    kz: int
+    blocks: tuple
+    world: int
+
+    @staticmethod
+    def build(nz: int, kz: int, block_height: int, world: int) -> "SlabLayout":
+        blocks = tuple(SliceBlock(lo, min(lo + block_height - 1, nz - 1)) for lo in range(0, nz, block_height))
+        if world > len(blocks):
+            raise ValueError(f"{world} ranks for {len(blocks)} blocks: every rank needs a block")
+        return SlabLayout(nz, kz, blocks, world)
+
+    def owned_blocks(self, rank: int) -> list[SliceBlock]:
+        B, P = len(self.blocks), self.world
+        lo = (rank * B) // P
+        hi = ((rank + 1) * B) // P
+        return list(self.blocks[lo:hi])
+
+    def owned(self, rank: int) -> tuple[int, int]:
+        ob = self.owned_blocks(rank)
+        return ob[0].z_lo, ob[-1].z_hi
+
+    def local(self, rank: int) -> tuple[int, int]:
+        o_lo, o_hi = self.owned(rank)
+        return max(0, o_lo - self.kz), min(self.nz - 1, o_hi + self.kz)
+
+    def transfers(self, rank: int):
+        """(peer, lo, hi, 'recv'|'send') plane ranges for this rank."""
+        out = []
+        me_lo, me_hi = self.owned(rank)
+        l_lo, l_hi = self.local(rank)
+        for q in range(self.world):
+            if q == rank:
+                continue
+            q_lo, q_hi = self.owned(q)
+            ql_lo, ql_hi = self.local(q)
+            # what I need from q: my local range minus my owned range, within q's owned
+            for a, b in ((l_lo, me_lo - 1), (me_hi + 1, l_hi)):
+                lo, hi = max(a, q_lo), min(b, q_hi)
+                if lo <= hi:
+                    out.append((q, lo, hi, "recv"))
+            for a, b in ((ql_lo, q_lo - 1), (q_hi + 1, ql_hi)):
+                lo, hi = max(a, me_lo), min(b, me_hi)
+                if lo <= hi:
+                    out.append((q, lo, hi, "send"))
+        return out
+
+
+def exchange_halos(buf: torch.Tensor, z0: int, plan, group=None) -> None:
+    """Fill the halo planes of the local slab `buf` (plane 0 = depth z0)."""
+    ops = []
+    for peer, lo, hi, kind in plan:
+        view = buf[lo - z0:hi - z0 + 1]
+        if kind == "send":
+            ops.append(dist.P2POp(dist.isend, view, peer, group))
+        else:
+            ops.append(dist.P2POp(dist.irecv, view, peer, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class ShardedJacobi:
+    """GPU block-Jacobi shard of this rank (NCCL halos, fused CUDA steps)."""
+
+    def __init__(self, obj, x0, block_height: int, dtype: torch.dtype = torch.float64, group=None,
+                 rank: int | None = None, world: int | None = None):
+        from . import _native as N
+        from . import device as D
+
+        self.N, self.D = N, D
+        self.obj, self.dtype, self.group = obj, dtype, group
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        self.virtual = rank is not None  # single-process emulation: caller drives exchange/reduce
+        dims = obj.dims
+        self.layout = SlabLayout.build(dims.nz, obj.psf.kdims.kz, block_height, self.world)
+        self.blocks = self.layout.owned_blocks(self.rank)
+        self.o_lo, self.o_hi = self.layout.owned(self.rank)
+        self.l_lo, self.l_hi = self.layout.local(self.rank)
+        self.plan = self.layout.transfers(self.rank)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        self.x = torch.from_numpy(x0[self.l_lo:self.l_hi + 1]).to(dev).to(dtype).contiguous()
+        self.y = torch.from_numpy(obj.y[self.l_lo:self.l_hi + 1]).to(dev).to(dtype).contiguous()
+        self.prev = torch.zeros_like(self.x)
+        self.snap = self.x.clone()
+        self.plane = dims.ny * dims.nx
+        z0 = self.l_lo
+        esz = self.x.element_size()
+        y_shift = self.y.data_ptr() - z0 * self.plane * esz  # y + z*plane is row z (C ABI contract)
+        self.y_shift = y_shift
+
+        def rows(t, b):
+            return t[b.z_lo - z0:b.z_hi - z0 + 1]
+
+        self.tasks = (N.Task * len(self.blocks))(*[
+            N.Task(self.x.data_ptr(), z0, self.x.shape[0], b.z_lo, b.z_hi, rows(self.prev, b).data_ptr(), None,
+                   rows(self.x, b).data_ptr(), rows(self.prev, b).data_ptr()) for b in self.blocks])
+        self.geom = obj.geom(dtype)
+        self.reg = D.reg(obj.params)
+        self.ws_bytes = N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(self.geom), self.tasks, len(self.blocks)))
+        self.ev_bytes = N.ws_bytes(N.lib.bd3mg_eval_rows_ws_bytes(D.byref(self.geom), self.o_lo, self.o_hi))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.ews = torch.empty(self.ev_bytes, dtype=torch.uint8, device=dev)
+        self.info = torch.empty((len(self.blocks), N.INFO_DOUBLES), dtype=torch.float64, device=dev)
+        self.terms = torch.zeros(N.EVAL_DOUBLES, dtype=torch.float64, device=dev)
+        self.K = obj.psf.device_kernels(dtype, dev)
+        self.k = 0
+        self.sweeps = 0
+        self.log_terms: list[torch.Tensor] = []
+
+    @property
+    def nblocks(self) -> int:
+        return len(self.layout.blocks)
+
+    # -- phases of one sweep (sweep() runs them; a single-process emulation
+    #    of several ranks drives them itself) --------------------------------
+    def exchange(self) -> None:
+        exchange_halos(self.x, self.l_lo, self.plan, self.group)
+
+    def record_local(self) -> None:
+        """This rank's share of the recorder pass (owned rows)."""
+        N, D = self.N, self.D
+        esz = self.x.element_size()
+        off = (self.o_lo - self.l_lo) * self.plane * esz
+        N.check(N.lib.bd3mg_eval_rows(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(),
+                                      self.y.data_ptr() + off, self.x.data_ptr(), self.l_lo, self.x.shape[0],
+                                      self.o_lo, self.o_hi, self.snap.data_ptr() + off, self.terms.data_ptr(),
+                                      self.ews.data_ptr(), self.ev_bytes, D.stream_handle()))
+
+    def step(self) -> None:
+        N, D = self.N, self.D
+        N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.y_shift,
+                                     self.tasks, len(self.blocks), self.info.data_ptr(), self.ws.data_ptr(),
+                                     self.ws_bytes, D.stream_handle()))
+        self.sweeps += 1
+        self.k += self.nblocks
+
+    def sweep(self) -> None:
+        self.exchange()
+        if self.sweeps > 0:   # recorder pass of the previous sweep (x current everywhere)
+            self.record_local()
+            dist.all_reduce(self.terms, group=self.group)
+            self.snap.copy_(self.x)
+        self.step()
+
+    def finish(self) -> float:
+        """Recorder pass of the last sweep; returns f(x)."""
+        self.exchange()
+        self.record_local()
+        dist.all_reduce(self.terms, group=self.group)
+        return float(self.terms[4].item())
+
+    def capture(self) -> None:
+        """Sweeps with NCCL P2P stay eager (no graph capture)."""
+
+    def check(self) -> None:
+        if bool((self.info[:, 8] != 0).any().item()):
+            raise ValueError("non-finite gradient")
+
+    def f(self) -> float:
+        return float(self.terms[4].item())
+
+    def gather(self) -> np.ndarray | None:
+        """Full iterate on rank 0 (owned planes from every rank)."""
+        own = self.x[self.o_lo - self.l_lo:self.o_hi - self.l_lo + 1].contiguous()
+        sizes = [self.layout.owned(q) for q in range(self.world)]
+        if self.rank == 0:
+            parts = [own]
+            for q in range(1, self.world):
+                lo, hi = sizes[q]
+                t = torch.empty((hi - lo + 1,) + tuple(own.shape[1:]), dtype=own.dtype, device=own.device)
+                dist.recv(t, q, group=self.group)
+                parts.append(t)
+            return torch.cat(parts).double().cpu().numpy()
+        dist.send(own, 0, group=self.group)
+        return None
+
+
+class OracleShardedJacobi:
+    """Same layout, exchange and recorder schedule with the CPU oracle as the
+    per-block step -- the host-logic check of the sharded path (gloo tests).
+    Test infrastructure only: the oracle module is passed in by the caller."""
+
+    def __init__(self, oracle, crit, x0, block_height: int, group=None):
+        self.O, self.crit, self.group = oracle, crit, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        nz = x0.shape[0]
+        self.layout = SlabLayout.build(nz, crit.kz, block_height, self.world)
+        self.blocks = self.layout.owned_blocks(self.rank)
+        self.o_lo, self.o_hi = self.layout.owned(self.rank)
+        self.l_lo, self.l_hi = self.layout.local(self.rank)
+        self.plan = self.layout.transfers(self.rank)
+        self.x = torch.from_numpy(np.ascontiguousarray(x0[self.l_lo:self.l_hi + 1], dtype=np.float64)).clone()
+        self.prev = torch.zeros_like(self.x)
+        self.sweeps = 0
+
+    def sweep(self) -> None:
+        exchange_halos(self.x, self.l_lo, self.plan, self.group)
+        xl = self.x.numpy()
+        incs = []
+        for b in self.blocks:
+            s_lo, s_hi = self.O.support(self.layout.nz, self.crit.kz, b.z_lo, b.z_hi)
+            slab = xl[s_lo - self.l_lo:s_hi - self.l_lo + 1].copy()
+            d = self.prev.numpy()[b.z_lo - self.l_lo:b.z_hi - self.l_lo + 1].ravel().copy()
+            incs.append(self.O.mg_direction(self.crit, slab, s_lo, b.z_lo, b.z_hi, d))
+        for b, inc in zip(self.blocks, incs):
+            sl = slice(b.z_lo - self.l_lo, b.z_hi - self.l_lo + 1)
+            inc = torch.from_numpy(inc.reshape((b.height,) + tuple(self.x.shape[1:])))
+            self.x[sl] += inc
+            self.prev[sl] = inc
+        self.sweeps += 1
+
+    def gather(self) -> np.ndarray | None:
+        own = self.x[self.o_lo - self.l_lo:self.o_hi - self.l_lo + 1].contiguous()
+        if self.rank == 0:
+            parts = [own]
+            for q in range(1, self.world):
+                lo, hi = self.layout.owned(q)
+                t = torch.empty((hi - lo + 1,) + tuple(own.shape[1:]), dtype=own.dtype)
+                dist.recv(t, q, group=self.group)
+                parts.append(t)
+            return torch.cat(parts).numpy()
+        dist.send(own, 0, group=self.group)
+        return None

@@ -1,0 +1,85 @@
+"""Multi-rank path on CPU: the slab layout / halo plan, and a sharded
+block-Jacobi over `gloo` (world sizes 2 and 4, halos spanning several ranks)
+that must reproduce the single-process block-Jacobi bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2002_02328_b200.distributed import SlabLayout
+
+
+def test_layout_plan_is_consistent():
+    for nz, kz, h, world in [(64, 11, 8, 8), (64, 11, 8, 2), (24, 5, 2, 4), (30, 7, 4, 3), (16, 3, 16, 1)]:
+        lay = SlabLayout.build(nz, kz, h, world)
+        owned = [lay.owned(r) for r in range(world)]
+        assert owned[0][0] == 0 and owned[-1][1] == nz - 1
+        assert all(owned[r][1] + 1 == owned[r + 1][0] for r in range(world - 1))
+        sends = {(r, p, lo, hi) for r in range(world) for p, lo, hi, k in lay.transfers(r) if k == "send"}
+        recvs = {(p, r, lo, hi) for r in range(world) for p, lo, hi, k in lay.transfers(r) if k == "recv"}
+        assert sends == recvs  # every receive has its matching send
+        for r in range(world):  # halos exactly cover local minus owned
+            got = sorted(z for p, lo, hi, k in lay.transfers(r) if k == "recv" for z in range(lo, hi + 1))
+            l_lo, l_hi = lay.local(r)
+            want = [z for z in range(l_lo, l_hi + 1) if not owned[r][0] <= z <= owned[r][1]]
+            assert got == want
+    with pytest.raises(ValueError):
+        SlabLayout.build(16, 3, 8, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, sweeps, out_path):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2002_02328_b200.distributed import OracleShardedJacobi
+        O.core("c", threads=1)
+        crit, x0, h = _problem(O)
+        eng = OracleShardedJacobi(O, crit, x0, h)
+        for _ in range(sweeps):
+            eng.sweep()
+        full = eng.gather()
+        if rank == 0:
+            np.save(out_path, full)
+    finally:
+        dist.destroy_process_group()
+
+
+def _problem(O):
+    from paper_2002_02328_b200 import blur
+    from paper_2002_02328_b200.volume import Dims3
+    dims = Dims3(20, 18, 16)
+    psf = blur.depth_variant_stack(dims, (3, 3, 5), (0.8, 1.6), (1.0, 2.0))
+    rng = np.random.Generator(np.random.Philox(3))
+    y = rng.uniform(0, 1, dims.shape)
+    x0 = rng.uniform(0, 1, dims.shape)
+    crit = O.Criterion(psf.kernels, y, lam=1e-2, eta=1e-1, kappa=0.05, delta=1e-2)
+    return crit, x0, 2
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_jacobi_matches_single_process(world, tmp_path, oracle_mod):
+    sweeps = 3
+    out = tmp_path / "x.npy"
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, sweeps, str(out)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    crit, x0, h = _problem(oracle_mod)
+    B = -(-x0.shape[0] // h)
+    want, _, _ = oracle_mod.run_bp3mg(crit, x0, B, h, max_updates=sweeps * B)
+    assert np.array_equal(got, want)
