@@ -256,6 +256,9 @@ def main():
         t_max = float(t.item())
     value = args.steps * B / (t_max / 1e3)
     f_last = eng.f()
+    blocks_all = [runtime.scheduler.SliceBlock(lo, min(lo + cfg.block_height - 1, cfg.dims.nz - 1))
+                  for lo in range(0, cfg.dims.nz, cfg.block_height)]
+    sweep_flops = blur.flops_jacobi_sweep(cfg.dims, cfg.kdims, blocks_all)
 
     extra = {}
     if not args.quick and rank == 0:
@@ -263,6 +266,7 @@ def main():
     if not args.quick:
         extra["e2e"] = e2e(obj, cfg, x0, args, world, rank, torch, N, D)
     if not args.quick and rank == 0 and world == 1:
+        extra["variants"] = {"hd-cache": variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush)}
         extra["cpu_baseline"] = cpu_baseline(cfg)
 
     if rank == 0:
@@ -272,7 +276,10 @@ def main():
                 "dtype": cfg.dtype, "data": "synthetic (seeded ellipsoid phantom, BASELINE PSF family)",
                 "config": _config_dict(cfg, world), "clocks": clk,
                 "gpu_launches": int(launches_per_step * args.steps),
-                "f_after": f_last}
+                "sweep": {"variant": "exact (residual, gradient and both Gram columns recomputed every visit)",
+                          "correlation_flops_per_step": sweep_flops,
+                          "achieved_tflops": sweep_flops / (t_max / args.steps / 1e3) / 1e12},
+                "f_anchor_last_step": f_last}
         line.update(extra)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -281,6 +288,30 @@ def main():
 
 
 # ---------------------------------------------------------------------------
+def variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush):
+    """Secondary number: the "hd-cache" variant (H E_S d_mem kept from the
+    previous visit; one forward correlation per Gram instead of two)."""
+    eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, dtype, hd_cache=True)
+    eng.sweep()
+    eng.capture()
+    for _ in range(max(args.warmup - 1, 0)):
+        eng.sweep()
+    torch.cuda.synchronize()
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        st[i].record()
+        eng.sweep()
+        en[i].record()
+    torch.cuda.synchronize()
+    eng.check()
+    ms = sum(a.elapsed_time(b) for a, b in zip(st, en))
+    fl = blur.flops_jacobi_sweep(cfg.dims, cfg.kdims, eng.blocks, hd_cache=True)
+    return {"value": args.steps * eng.nblocks / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
+            "correlation_flops_per_step": fl, "achieved_tflops": fl / (ms / args.steps / 1e3) / 1e12}
+
+
 def roofline(obj, cfg, dtype, torch, N, D, blur):
     """Dominant kernel family: the dense depth-variant correlation.  Time
     full-volume H and H^T launches with CUDA events on the launching stream;

@@ -165,6 +165,32 @@ int bd3mg_mg_steps(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kern
  * when dmem_rows is not NULL, dmem_rows = inc; n elements of `dtype`. */
 int bd3mg_apply_increment(int32_t dtype, void* x_rows, void* dmem_rows, const void* inc, int64_t n, void* stream);
 
+/* One block-Jacobi sweep on a device-resident fragment (reference
+ * run_bp3mg_barrier with every block of the fragment as a worker,
+ * runtime.py:244-292, plus the per-sweep recorder of runtime.py:108-141).
+ * Order: (1) recorder terms of the ANCHOR x over rows [rec_lo, rec_hi]
+ * (data term taken from the step's own residual, box / TV / axial and the
+ * stop norms against `snap`), (2) snap <- anchor rows, (3) every block's
+ * fused step at the anchor, x and dmem updated in place.  With hd_cache
+ * (variant "hd-cache", bd3mg_jacobi_cache_elems elements, zero-initialised)
+ * the Gram reuses H E_S d_mem cached from the block's previous visit
+ * (linearity of H) instead of recomputing it. */
+typedef struct {
+  void* x;              /* iterate fragment, plane 0 = depth frag_z0 */
+  void* dmem;           /* memory-direction store, same layout as x */
+  int64_t frag_z0, nzf;
+  const int64_t* blocks; /* host: nblocks (z_lo, z_hi) pairs inside the fragment, <= 32 */
+  int nblocks;
+  int64_t rec_lo, rec_hi; /* recorder rows; rec_hi < rec_lo disables it */
+  void* snap;           /* rows rec_lo..rec_hi of the sweep snapshot, or NULL */
+  void* hd_cache;       /* NULL, or the hd-cache buffer */
+} bd3mg_sweep_t;
+size_t bd3mg_jacobi_sweep_ws_bytes(const bd3mg_geom_t* g, const bd3mg_sweep_t* sw);
+int64_t bd3mg_jacobi_cache_elems(const bd3mg_geom_t* g, const bd3mg_sweep_t* sw);
+int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                       const bd3mg_sweep_t* sw, double* terms_out, double* info_out, void* ws, size_t ws_bytes,
+                       void* stream);
+
 /* ---- host-buffer problem handle (worker-task boundary of the reference:
  * TaskMessage -> UpdateMessage, scheduler.py:36-57, runtime.py:92-105) ---- */
 typedef struct bd3mg_problem bd3mg_problem;

@@ -28,6 +28,7 @@ EXPORTS = (
     "bd3mg_eval_f_ws_bytes", "bd3mg_eval_f", "bd3mg_eval_rows_ws_bytes", "bd3mg_eval_rows",
     "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
+    "bd3mg_jacobi_sweep_ws_bytes", "bd3mg_jacobi_cache_elems", "bd3mg_jacobi_sweep",
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
     "bd3mg_fma_probe",
 )
@@ -47,6 +48,12 @@ class Task(C.Structure):
     _fields_ = [("frag", C.c_void_p), ("frag_z0", C.c_int64), ("nzf", C.c_int64),
                 ("z_lo", C.c_int64), ("z_hi", C.c_int64), ("d_mem", C.c_void_p),
                 ("inc_out", C.c_void_p), ("x_rows", C.c_void_p), ("dmem_rows", C.c_void_p)]
+
+
+class Sweep(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("dmem", C.c_void_p), ("frag_z0", C.c_int64), ("nzf", C.c_int64),
+                ("blocks", C.POINTER(C.c_int64)), ("nblocks", C.c_int), ("rec_lo", C.c_int64),
+                ("rec_hi", C.c_int64), ("snap", C.c_void_p), ("hd_cache", C.c_void_p)]
 
 
 class NativeError(RuntimeError):
@@ -90,6 +97,12 @@ def _load() -> C.CDLL:
     lib.bd3mg_mg_steps_ws_bytes.argtypes = [G, T, C.c_int]
     lib.bd3mg_mg_steps_ws_bytes.restype = _sz
     lib.bd3mg_mg_steps.argtypes = [G, R, _vp, _vp, T, C.c_int, _vp, _vp, _sz, _vp]
+    S = C.POINTER(Sweep)
+    lib.bd3mg_jacobi_sweep_ws_bytes.argtypes = [G, S]
+    lib.bd3mg_jacobi_sweep_ws_bytes.restype = _sz
+    lib.bd3mg_jacobi_cache_elems.argtypes = [G, S]
+    lib.bd3mg_jacobi_cache_elems.restype = C.c_int64
+    lib.bd3mg_jacobi_sweep.argtypes = [G, R, _vp, _vp, S, _vp, _vp, _vp, _sz, _vp]
     lib.bd3mg_apply_increment.argtypes = [C.c_int32, _vp, _vp, _vp, _i64, _vp]
     lib.bd3mg_problem_create.argtypes = [G, R, _vp, _vp, C.c_int, C.POINTER(C.c_void_p)]
     lib.bd3mg_problem_destroy.argtypes = [_vp]

@@ -190,7 +190,7 @@ int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   const int64_t nr = hi - lo + 1, n = nr * plane;
   const long long crow = conv_rows<T>(g, M_RESID, nr);
   double* parts = ws.take<double>(crow);
-  const int ctas = (int)std::min<int64_t>((n + kEwNT - 1) / kEwNT, 4 * 148);
+  const int ctas = (int)std::min<int64_t>((nr * g->ny + (kEwNT / 32) - 1) / (kEwNT / 32), 4 * 148);
   double* eparts = ws.take<double>((size_t)ctas * kEvalNV);
   double* sums = ws.take<double>(8);
   if (ws.measure) return BD3MG_OK;
@@ -267,9 +267,17 @@ int omega_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* frag, int64
 
 // ---------------------------------------------------------------------------
 // Batched mg_direction (+ optional in-place receive_update).
+// Options of the batched step used by the sweep driver.
+template <typename T>
+struct StepOpts {
+  double* resid_sq = nullptr;  // device: sum of residual^2 over rows [rec_lo, rec_hi] (shared anchor)
+  int64_t rec_lo = 0, rec_hi = -1;
+  T* const* hd = nullptr;      // per task: cached H E_S d_mem over rows [olo, ohi] (updated in place)
+};
+
 template <typename T>
 int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
-                   int nt, double* info_out, Ws& ws, cudaStream_t s) {
+                   int nt, double* info_out, Ws& ws, cudaStream_t s, const StepOpts<T>& opt = StepOpts<T>()) {
   const int64_t nz = g->nz, plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
   std::vector<int64_t> olo(nt), ohi(nt), h(nt);
   bool shared = true, any_d = false;
@@ -310,7 +318,14 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   for (int t = 0; t < nt; ++t) { gb[t] = ws.take<T>(h[t] * plane); wb[t] = ws.take<T>(h[t] * plane); }
   long long gram_work = 0;
   for (int t = 0; t < nt; ++t) gram_work += ohi[t] - olo[t] + 1;
-  const int gmode = any_d ? M_GRAM2 : M_GRAM1;
+  const bool cached = opt.hd != nullptr;
+  const int gmode = cached ? M_GRAMC : (any_d ? M_GRAM2 : M_GRAM1);
+  std::vector<T*> hgb(nt, nullptr);
+  if (cached)
+    for (int t = 0; t < nt; ++t) hgb[t] = ws.take<T>((ohi[t] - olo[t] + 1) * plane);
+  if (opt.resid_sq && !shared) return fail(BD3MG_EINVAL, "recorder residual needs a shared anchor");
+  if (opt.resid_sq && opt.rec_hi >= opt.rec_lo && (opt.rec_lo < u_lo || opt.rec_hi > u_hi))
+    return fail(BD3MG_EINVAL, "recorder rows outside the residual rows");
   const long long conv_part_rows = std::max(conv_rows<T>(g, M_RESID, resid_work), conv_rows<T>(g, gmode, gram_work));
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   // reg partials: ctas per task proportional to block size, capped
@@ -318,7 +333,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   long long reg_rows = 0;
   int max_ctas = 1;
   for (int t = 0; t < nt; ++t) {
-    rctas[t] = (int)std::max<int64_t>(1, std::min<int64_t>((h[t] * plane + 4 * kEwNT - 1) / (4 * kEwNT), 256));
+    rctas[t] = (int)std::max<int64_t>(1, std::min<int64_t>((h[t] * g->ny + 2 * (kEwNT / 32) - 1) / (2 * (kEwNT / 32)), 256));
     reg_rows += rctas[t];
     max_ctas = std::max(max_ctas, rctas[t]);
   }
@@ -350,6 +365,13 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     }
     CU(conv_launch<T>(M_RESID, false, a, (int)resid_work, s));
   launched();
+  }
+  if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
+    const long long tiles = conv_rows<T>(g, M_RESID, 1);
+    if (opt.rec_hi >= opt.rec_lo)
+      CU(reduce(cparts, 1, {{(opt.rec_lo - u_lo) * tiles, (opt.rec_hi - u_lo + 1) * tiles}}, opt.resid_sq, 1, s));
+    else
+      CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
   }
   // (2) g = H^T r + regulariser gradient; omega
   {
@@ -396,6 +418,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       ConvJob<T>& j = a.jobs[t];
       j.src0 = gb[t];
       j.src1 = tasks[t].d_mem ? (const T*)tasks[t].d_mem : gb[t];
+      if (cached) { j.sub = opt.hd[t]; j.dst0 = hgb[t]; }
       j.src_z0 = tasks[t].z_lo; j.src_nz = (int)h[t];
       j.out_lo = (int)olo[t]; j.nout = (int)(ohi[t] - olo[t] + 1); j.work_begin = wbeg;
       granges[t] = {(long long)wbeg * tiles, (long long)(wbeg + j.nout) * tiles};
@@ -405,7 +428,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   launched();
   }
   // (5) reductions
-  CU(reduce(cparts, any_d ? 3 : 1, granges, data3, 3, s));
+  CU(reduce(cparts, gmode == M_GRAM1 ? 1 : 3, granges, data3, 3, s));
   {
     std::vector<std::pair<long long, long long>> rr(nt);
     long long b0 = 0;
@@ -440,6 +463,21 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, info_out); launched();
     CU(cudaGetLastError());
   }
+  // (8) cached H E_S d_mem for the next visit (variant "hd-cache")
+  if (cached) {
+    HdArgs<T> ha;
+    memset(&ha, 0, sizeof(ha));
+    ha.nblocks = nt;
+    int mc = 1;
+    for (int t = 0; t < nt; ++t) {
+      HdBlock<T>& B = ha.blk[t];
+      B.hg = hgb[t]; B.hd = opt.hd[t]; B.n = (ohi[t] - olo[t] + 1) * plane;
+      B.ctas = (int)std::max<int64_t>(1, std::min<int64_t>((B.n + 4 * kEwNT - 1) / (4 * kEwNT), 1024));
+      mc = std::max(mc, B.ctas);
+    }
+    hd_update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ha, info_out); launched();
+    CU(cudaGetLastError());
+  }
   return BD3MG_OK;
 }
 
@@ -459,6 +497,74 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
     peak = std::max(peak, sub.off);
   }
   ws.off = std::max(ws.off, peak);
+  return BD3MG_OK;
+}
+
+// One block-Jacobi sweep (see bd3mg_jacobi_sweep in the header).
+template <typename T>
+int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_sweep_t* sw,
+                      double* terms, double* info, Ws& ws, cudaStream_t s) {
+  if (!sw || sw->nblocks < 1 || sw->nblocks > kMaxJobs)
+    return fail(BD3MG_EINVAL, "jacobi sweep needs 1..%d blocks", kMaxJobs);
+  const int64_t plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
+  T* x = (T*)sw->x;
+  T* dm = (T*)sw->dmem;
+  std::vector<bd3mg_task_t> tasks(sw->nblocks);
+  std::vector<T*> hd(sw->nblocks);
+  int64_t hd_off = 0;
+  for (int b = 0; b < sw->nblocks; ++b) {
+    const int64_t lo = sw->blocks[2 * b], hi = sw->blocks[2 * b + 1];
+    if (lo < sw->frag_z0 || hi >= sw->frag_z0 + sw->nzf) return fail(BD3MG_EINVAL, "block outside the fragment");
+    bd3mg_task_t& t = tasks[b];
+    t.frag = x; t.frag_z0 = sw->frag_z0; t.nzf = sw->nzf; t.z_lo = lo; t.z_hi = hi;
+    t.d_mem = dm ? dm + (lo - sw->frag_z0) * plane : nullptr;
+    t.inc_out = nullptr;
+    t.x_rows = x ? x + (lo - sw->frag_z0) * plane : nullptr;
+    t.dmem_rows = dm ? dm + (lo - sw->frag_z0) * plane : nullptr;
+    const int64_t olo = std::max<int64_t>(0, lo - rz), ohi = std::min<int64_t>(g->nz - 1, hi + rz);
+    hd[b] = sw->hd_cache ? (T*)sw->hd_cache + hd_off : nullptr;
+    hd_off += (ohi - olo + 1) * plane;
+  }
+  const bool rec = sw->rec_hi >= sw->rec_lo;
+  const int64_t nrec = rec ? sw->rec_hi - sw->rec_lo + 1 : 0;
+  const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>((nrec * g->ny + (kEwNT / 32) - 1) / (kEwNT / 32), 4 * 148));
+  double* eparts = ws.take<double>((size_t)ctas * kEvalNV);
+  double* sums = ws.take<double>(8);
+  StepOpts<T> opt;
+  opt.resid_sq = sums;
+  opt.rec_lo = sw->rec_lo;
+  opt.rec_hi = sw->rec_hi;
+  opt.hd = sw->hd_cache ? hd.data() : nullptr;
+  Ws sub = ws;  // the step's scratch follows the recorder's
+  int rc = mg_steps_chunk<T>(g, r, K, y, tasks.data(), sw->nblocks, info, sub, s, opt);
+  ws.off = sub.off;
+  if (rc != BD3MG_OK || ws.measure) return rc;
+  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  return BD3MG_OK;
+}
+
+// The recorder's elementwise terms + snapshot roll, launched BEFORE the step
+// (the step updates x in place).
+template <typename T>
+int jacobi_record_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const bd3mg_sweep_t* sw, double* eparts,
+                       double* sums, int ctas, cudaStream_t s) {
+  const int64_t plane = g->ny * g->nx;
+  if (sw->rec_hi < sw->rec_lo) {
+    CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s));
+    return BD3MG_OK;
+  }
+  const int64_t nrec = sw->rec_hi - sw->rec_lo + 1;
+  if (sw->rec_lo < sw->frag_z0 || sw->rec_hi >= sw->frag_z0 + sw->nzf)
+    return fail(BD3MG_EINVAL, "recorder rows outside the fragment");
+  EvalArgs<T> e;
+  e.x = (const T*)sw->x + (sw->rec_lo - sw->frag_z0) * plane;
+  e.snap = (const T*)sw->snap;
+  e.lo = (int)sw->rec_lo; e.nz = (int)g->nz; e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane;
+  e.n = nrec * plane; e.delta2 = r->delta * r->delta; e.x_min = r->x_min; e.x_max = r->x_max; e.ctas = ctas;
+  eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts); launched();
+  CU(cudaGetLastError());
+  CU(reduce(eparts, kEvalNV, {{0, ctas}}, sums + 1, kEvalNV, s));
+  if (sw->snap) CU(cudaMemcpyAsync(sw->snap, e.x, (size_t)nrec * plane * sizeof(T), cudaMemcpyDeviceToDevice, s));
   return BD3MG_OK;
 }
 
@@ -722,6 +828,54 @@ int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void
                                           hi, (double*)out, ws, (cudaStream_t)stream),
                     majorant_impl<float>(g, r, (const float*)kernels, (const float*)omega, (const float*)v, lo, hi,
                                          (float*)out, ws, (cudaStream_t)stream));
+}
+
+size_t bd3mg_jacobi_sweep_ws_bytes(const bd3mg_geom_t* g, const bd3mg_sweep_t* sw) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, jacobi_sweep_impl<double>(g, &r, nullptr, nullptr, sw, nullptr, nullptr, ws, 0),
+                      jacobi_sweep_impl<float>(g, &r, nullptr, nullptr, sw, nullptr, nullptr, ws, 0));
+  });
+}
+
+int64_t bd3mg_jacobi_cache_elems(const bd3mg_geom_t* g, const bd3mg_sweep_t* sw) {
+  if (check_geom(g) != BD3MG_OK || !sw) return -1;
+  const int64_t plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
+  int64_t n = 0;
+  for (int b = 0; b < sw->nblocks; ++b) {
+    const int64_t lo = sw->blocks[2 * b], hi = sw->blocks[2 * b + 1];
+    n += (std::min<int64_t>(g->nz - 1, hi + rz) - std::max<int64_t>(0, lo - rz) + 1) * plane;
+  }
+  return n;
+}
+
+int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                       const bd3mg_sweep_t* sw, double* terms_out, double* info_out, void* wsp, size_t ws_bytes,
+                       void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !sw || !info_out || !terms_out) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  // scratch layout mirrors jacobi_sweep_impl: [eparts][sums][step scratch]
+  const int64_t nrec = sw->rec_hi >= sw->rec_lo ? sw->rec_hi - sw->rec_lo + 1 : 0;
+  const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>((nrec * g->ny + (kEwNT / 32) - 1) / (kEwNT / 32), 4 * 148));
+  Ws probe = ws;
+  double* eparts = probe.take<double>((size_t)ctas * kEvalNV);
+  double* sums = probe.take<double>(8);
+  rc = DISPATCH_T(g, jacobi_record_impl<double>(g, r, sw, eparts, sums, ctas, s),
+                  jacobi_record_impl<float>(g, r, sw, eparts, sums, ctas, s));
+  if (rc) return rc;
+  rc = DISPATCH_T(g,
+                  jacobi_sweep_impl<double>(g, r, (const double*)kernels, (const double*)y, sw, terms_out, info_out,
+                                            ws, s),
+                  jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
+                                           s));
+  if (rc) return rc;
+  eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms_out); launched();
+  CU(cudaGetLastError());
+  return BD3MG_OK;
 }
 
 size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks) {

@@ -18,6 +18,7 @@ cudaError_t conv_launch(int mode, bool adj, ConvArgs<T>& p, int total_work, cuda
       case M_RESID: return launch_mode<T, M_RESID, false>(p, total_work, s);
       case M_GRAM1: return launch_mode<T, M_GRAM1, false>(p, total_work, s);
       case M_GRAM2: return launch_mode<T, M_GRAM2, false>(p, total_work, s);
+      case M_GRAMC: return launch_mode<T, M_GRAMC, false>(p, total_work, s);
       default: return cudaErrorInvalidValue;
     }
   }

@@ -39,6 +39,7 @@ enum ConvMode : int {
   M_GRAD = 2,   // (adjoint) dst0 = acc + 2eta*box + lam*tv + 2kappa*axial; omega out
   M_GRAM1 = 3,  // partial: sum acc0^2               (+ optional store dst0 = acc0)
   M_GRAM2 = 4,  // partial: acc0^2, acc0*acc1, acc1^2 (dual input, shared taps)
+  M_GRAMC = 5,  // dst0 = acc0 (H E_S g); partial: acc0^2, acc0*c, c^2 with c = sub[o] (cached H E_S d)
 };
 
 constexpr int kMaxJobs = 32;
@@ -77,7 +78,8 @@ struct ConvArgs {
 
 template <int MODE>
 struct ModeNV {
-  static constexpr int value = (MODE == M_RESID || MODE == M_GRAM1) ? 1 : (MODE == M_GRAM2 ? 3 : 0);
+  static constexpr int value =
+      (MODE == M_RESID || MODE == M_GRAM1) ? 1 : ((MODE == M_GRAM2 || MODE == M_GRAMC) ? 3 : 0);
 };
 
 // ---------------------------------------------------------------------------
@@ -149,6 +151,22 @@ BD3MG_D T grad_voxel(T hta, const XView<T>& xv, int z, int y, int x, int nz_glob
   return g;
 }
 
+// Same gradient with w*Dx / w*Dy of the pixel and of its left / upper
+// neighbours precomputed (shared-memory epilogue of the tiled kernel).
+template <typename T>
+BD3MG_D T grad_combine(T hta, const XView<T>& xv, int z, int y, int x, int nz_global, T px0, T pxm, T py0, T pym,
+                       T two_eta, T lam, T two_kappa, T x_min, T x_max) {
+  const T xc = xv.at(z, y, x);
+  const T clipped = xc < x_min ? x_min : (xc > x_max ? x_max : xc);
+  T g = add_rn(hta, mul_rn(two_eta, sub_rn(xc, clipped)));
+  const T tvx = (xv.nx == 1) ? T(0) : (x == 0) ? -px0 : (x == xv.nx - 1) ? pxm : sub_rn(pxm, px0);
+  const T tvy = (xv.ny == 1) ? T(0) : (y == 0) ? -py0 : (y == xv.ny - 1) ? pym : sub_rn(pym, py0);
+  g = add_rn(g, mul_rn(lam, add_rn(tvx, tvy)));
+  const T dzm = (z - 1 >= 0 && z - 1 < nz_global - 1) ? sub_rn(xc, xv.at(z - 1, y, x)) : T(0);
+  const T dzp = (z < nz_global - 1) ? sub_rn(xv.at(z + 1, y, x), xc) : T(0);
+  return add_rn(g, mul_rn(two_kappa, sub_rn(dzm, dzp)));
+}
+
 // ---------------------------------------------------------------------------
 // Tile configuration.  fp64: RX=2 (one 16-byte LDS per 2 window values);
 // fp32: RX=4.  Consecutive lanes of a quarter-warp read consecutive 16-byte
@@ -162,7 +180,7 @@ struct ConvCfg {
   static constexpr int VEC = 16 / sizeof(T);        // elements per 16-byte load
   static constexpr int RX = VEC;                    // outputs per thread in x
   static constexpr int RY = DUAL ? 8 : 16;          // outputs per thread in y
-  static constexpr int WX = 16, WY = 8;
+  static constexpr int WX = 32, WY = 4;             // a warp spans one row group
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
   // TMA boxes must start on a 16-byte boundary in x (measured: odd-element
@@ -337,12 +355,14 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
             v[s][j] = q.x; v[s][j + 1] = q.y; v[s][j + 2] = q.z; v[s][j + 3] = q.w;
           }
         }
+      // c outer, rows inner: consecutive FMAs update different accumulators
+      // (latency hiding); per output the order is still a -> b -> c.
 #pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        const int b = yi - r;
-        if (b < 0 || b >= KY) continue;
+      for (int c = 0; c < KX; ++c) {
 #pragma unroll
-        for (int c = 0; c < KX; ++c) {
+        for (int r = 0; r < RY; ++r) {
+          const int b = yi - r;
+          if (b < 0 || b >= KY) continue;
           const T k = cs[b * KX + c];
 #pragma unroll
           for (int s = 0; s < NIN; ++s)
@@ -362,8 +382,30 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
   const long long orow = (long long)(zo - job.out_lo) * p.plane;
   XView<T> xv;
+  constexpr int EW = Cfg::TX + 1, EH = Cfg::TY + 1;  // w*Dx / w*Dy region incl. left/top neighbours
+  T* pxs = tiles;
+  T* pys = tiles + EH * EW;
   if constexpr (MODE == M_GRAD) {
+    static_assert(2 * EH * EW * sizeof(T) <= 2 * Cfg::TILE_BYTES, "epilogue scratch exceeds tile buffers");
     xv.p = job.xg; xv.z0 = job.xg_z0; xv.nzv = job.xg_nz; xv.ny = p.ny; xv.nx = p.nx; xv.plane = p.plane;
+    // the conv loop ended with a barrier: the tile buffers are free
+    const T d2 = (T)p.delta2;
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < EH * EW; idx += Cfg::NT) {
+      const int r = idx / EW, c = idx - r * EW;
+      const int y = y0 - 1 + r, x = x0 - 1 + c;
+      T px = T(0), py = T(0);
+      if (y >= 0 && y < p.ny && x >= 0 && x < p.nx) {
+        const T dx = fdx(xv, zo, y, x), dy = fdy(xv, zo, y, x);
+        const T w = omega_of(dx, dy, d2);
+        px = mul_rn(w, dx);
+        py = mul_rn(w, dy);
+        if (r >= 1 && c >= 1) job.omega[orow + (long long)y * p.nx + x] = w;  // this tile's own pixel
+      }
+      pxs[idx] = px;
+      pys[idx] = py;
+    }
+    __syncthreads();
   }
 #pragma unroll
   for (int r = 0; r < RY; ++r) {
@@ -382,11 +424,10 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
         if (job.dst0) job.dst0[o] = res;
         part[0] += (double)res * (double)res;
       } else if constexpr (MODE == M_GRAD) {
-        T w;
-        const T g = grad_voxel<T>(a0, xv, zo, y, x, p.nz_global, (T)p.two_eta, (T)p.lam, (T)p.two_kappa,
-                                  (T)p.delta2, (T)p.x_min, (T)p.x_max, &w);
-        job.dst0[o] = g;
-        job.omega[o] = w;
+        const int er = y - y0 + 1, ec = x - x0 + 1;
+        job.dst0[o] = grad_combine<T>(a0, xv, zo, y, x, p.nz_global, pxs[er * EW + ec], pxs[er * EW + ec - 1],
+                                      pys[er * EW + ec], pys[(er - 1) * EW + ec], (T)p.two_eta, (T)p.lam,
+                                      (T)p.two_kappa, (T)p.x_min, (T)p.x_max);
       } else if constexpr (MODE == M_GRAM1) {
         if (job.dst0) job.dst0[o] = a0;
         part[0] += (double)a0 * (double)a0;
@@ -395,6 +436,12 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
         part[0] += (double)a0 * (double)a0;
         part[1] += (double)a0 * (double)a1;
         part[2] += (double)a1 * (double)a1;
+      } else if constexpr (MODE == M_GRAMC) {
+        const double c0 = (double)job.sub[o];
+        job.dst0[o] = a0;
+        part[0] += (double)a0 * (double)a0;
+        part[1] += (double)a0 * c0;
+        part[2] += c0 * c0;
       }
     }
   }
@@ -416,7 +463,7 @@ constexpr int kGenericTX = 32, kGenericTY = 4;
 
 template <typename T, int MODE, bool ADJ>
 __global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_constant__ ConvArgs<T> p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* coef_s = reinterpret_cast<T*>(smem_raw);
   size_t coef_bytes = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
   double* red_s = reinterpret_cast<double*>(smem_raw + coef_bytes);
@@ -472,6 +519,12 @@ __global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_c
       part[0] = (double)acc0 * (double)acc0;
       part[1] = (double)acc0 * (double)acc1;
       part[2] = (double)acc1 * (double)acc1;
+    } else if constexpr (MODE == M_GRAMC) {
+      const double c0 = (double)job.sub[o];
+      job.dst0[o] = acc0;
+      part[0] = (double)acc0 * (double)acc0;
+      part[1] = (double)acc0 * c0;
+      part[2] = c0 * c0;
     }
   }
   if constexpr (NV > 0) {

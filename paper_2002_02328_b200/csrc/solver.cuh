@@ -72,52 +72,57 @@ __global__ void __launch_bounds__(kEwNT) reg_gram_kernel(const __grid_constant__
   const RegBlock<T>& B = p.blk[blockIdx.y];
   if ((int)blockIdx.x >= B.ctas) return;  // uniform per CTA
   const int h = B.hi - B.lo + 1;
-  const long long n = (long long)h * p.plane;
   double v[kRegNV];
 #pragma unroll
   for (int k = 0; k < kRegNV; ++k) v[k] = 0.0;
   const XView<T> gv{B.g, B.lo, h, p.ny, p.nx, p.plane};
   const XView<T> dv{B.d, B.lo, h, p.ny, p.nx, p.plane};
   const bool has_d = B.d != nullptr;
-  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < n; i += (long long)B.ctas * kEwNT) {
-    const int z = B.lo + (int)(i / p.plane);
-    const long long rem = i % p.plane;
-    const int y = (int)(rem / p.nx), x = (int)(rem % p.nx);
-    const T g = gv.at(z, y, x);
-    const T d = has_d ? dv.at(z, y, x) : T(0);
-    const double b0 = -(double)g, b1 = (double)d;
-    v[0] += b0 * b0;
-    v[1] += b0 * b1;
-    v[2] += b1 * b1;
-    const double w = (double)B.omega[i];
-    const double dx0 = -(double)fdx(gv, z, y, x), dy0 = -(double)fdy(gv, z, y, x);
-    const double dx1 = has_d ? (double)fdx(dv, z, y, x) : 0.0, dy1 = has_d ? (double)fdy(dv, z, y, x) : 0.0;
-    v[3] += w * (dx0 * dx0 + dy0 * dy0);
-    v[4] += w * (dx0 * dx1 + dy0 * dy1);
-    v[5] += w * (dx1 * dx1 + dy1 * dy1);
-    // axial row z (between z and z+1) of the block-embedded vector
-    double z0v, z1v;
-    if (z < B.hi) {
-      z0v = -((double)gv.at(z + 1, y, x) - (double)g);
-      z1v = has_d ? (double)dv.at(z + 1, y, x) - (double)d : 0.0;
-    } else if (B.hi < p.nz - 1) {
-      z0v = -b0;  // row hi sees E b[hi+1] = 0
-      z1v = -b1;
-    } else {
-      z0v = 0.0;
-      z1v = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NWARP = kEwNT / 32;
+  // one warp per (z, y) row: one integer division per row, coalesced x
+  const int rows = h * p.ny;
+  for (int row = blockIdx.x * NWARP + warp; row < rows; row += B.ctas * NWARP) {
+    const int z = B.lo + row / p.ny, y = row - (row / p.ny) * p.ny;
+    const long long rbase = (long long)(z - B.lo) * p.plane + (long long)y * p.nx;
+#pragma unroll 4
+    for (int x = lane; x < p.nx; x += 32) {
+      const T g = gv.at(z, y, x);
+      const T d = has_d ? dv.at(z, y, x) : T(0);
+      const double b0 = -(double)g, b1 = (double)d;
+      v[0] += b0 * b0;
+      v[1] += b0 * b1;
+      v[2] += b1 * b1;
+      const double w = (double)B.omega[rbase + x];
+      const double dx0 = -(double)fdx(gv, z, y, x), dy0 = -(double)fdy(gv, z, y, x);
+      const double dx1 = has_d ? (double)fdx(dv, z, y, x) : 0.0, dy1 = has_d ? (double)fdy(dv, z, y, x) : 0.0;
+      v[3] += w * (dx0 * dx0 + dy0 * dy0);
+      v[4] += w * (dx0 * dx1 + dy0 * dy1);
+      v[5] += w * (dx1 * dx1 + dy1 * dy1);
+      // axial row z (between z and z+1) of the block-embedded vector
+      double z0v, z1v;
+      if (z < B.hi) {
+        z0v = -((double)gv.at(z + 1, y, x) - (double)g);
+        z1v = has_d ? (double)dv.at(z + 1, y, x) - (double)d : 0.0;
+      } else if (B.hi < p.nz - 1) {
+        z0v = -b0;  // row hi sees E b[hi+1] = 0
+        z1v = -b1;
+      } else {
+        z0v = 0.0;
+        z1v = 0.0;
+      }
+      v[6] += z0v * z0v;
+      v[7] += z0v * z1v;
+      v[8] += z1v * z1v;
+      if (z == B.lo && B.lo >= 1) {  // row lo-1: E b[lo] - 0
+        v[6] += b0 * b0;
+        v[7] += b0 * b1;
+        v[8] += b1 * b1;
+      }
+      v[9] += (double)g * (double)d;
+      v[10] += (g != T(0)) ? 1.0 : 0.0;
+      v[11] += isfinite((double)g) ? 0.0 : 1.0;
     }
-    v[6] += z0v * z0v;
-    v[7] += z0v * z1v;
-    v[8] += z1v * z1v;
-    if (z == B.lo && B.lo >= 1) {  // row lo-1: E b[lo] - 0
-      v[6] += b0 * b0;
-      v[7] += b0 * b1;
-      v[8] += b1 * b1;
-    }
-    v[9] += (double)g * (double)d;
-    v[10] += (g != T(0)) ? 1.0 : 0.0;
-    v[11] += isfinite((double)g) ? 0.0 : 1.0;
   }
   cta_reduce<kRegNV, kEwNT>(v, red);
   if (threadIdx.x == 0) {
@@ -264,10 +269,14 @@ __global__ void __launch_bounds__(kEwNT) eval_terms_kernel(const __grid_constant
   __shared__ double red[(kEwNT / 32) * kEvalNV];
   double v[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const XView<T> xv{p.x, p.lo, p.nz, p.ny, p.nx, p.plane};
-  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < p.n; i += (long long)p.ctas * kEwNT) {
-    const int z = p.lo + (int)(i / p.plane);
-    const long long rem = i % p.plane;
-    const int y = (int)(rem / p.nx), x = (int)(rem % p.nx);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NWARP = kEwNT / 32;
+  const int rows = (int)(p.n / p.plane) * p.ny;
+  for (int row = blockIdx.x * NWARP + warp; row < rows; row += p.ctas * NWARP)
+#pragma unroll 4
+  for (int x = lane; x < p.nx; x += 32) {
+    const int zl = row / p.ny, y = row - zl * p.ny, z = p.lo + zl;
+    const long long i = (long long)zl * p.plane + (long long)y * p.nx + x;
     const double xc = (double)p.x[i];
     const double cl = xc < p.x_min ? p.x_min : (xc > p.x_max ? p.x_max : xc);
     const double e = xc - cl;
@@ -354,6 +363,32 @@ __global__ void __launch_bounds__(kEwNT) majorant_reg_kernel(const __grid_consta
   else dzp = sub_rn(vv.at(t + 1, y, x), vc);
   o = add_rn(o, mul_rn((T)p.two_kappa, sub_rn(dzm, dzp)));
   p.out[i] = o;
+}
+
+// Cached H E_S d_mem for the next visit: H E_S inc = c_g * H E_S(-g) + c_d * H E_S d
+// (linearity), over the block's output rows.  hd: rows [olo, ohi] per block.
+template <typename T>
+struct HdBlock {
+  const T* hg;  // H E_S g rows
+  T* hd;        // cache rows (in: H E_S d_mem, out: H E_S increment)
+  long long n;
+  int ctas;
+};
+template <typename T>
+struct HdArgs {
+  int nblocks;
+  HdBlock<T> blk[kMaxJobs];
+};
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) hd_update_kernel(const __grid_constant__ HdArgs<T> p,
+                                                           const double* __restrict__ info) {
+  const HdBlock<T>& B = p.blk[blockIdx.y];
+  if ((int)blockIdx.x >= B.ctas) return;
+  const double* o = info + blockIdx.y * kInfoNV;
+  if (o[8] != 0.0) return;
+  const T cg = (T)o[10], cd = (T)o[11];
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < B.n; i += (long long)B.ctas * kEwNT)
+    B.hd[i] = add_rn(mul_rn(-B.hg[i], cg), mul_rn(B.hd[i], cd));
 }
 
 // receive_update's block write (scheduler.py:151-153): x += inc; d_mem = inc.

@@ -10,16 +10,16 @@ span ranks, so a sweep is:
      from their owners (torch.distributed P2P, NCCL over NVLink on GPUs,
      grouped in one batch_isend_irecv); halos can span several ranks when a
      rank owns fewer than kz planes;
-  2. the per-sweep recorder pass on owned rows (f terms + stop-rule norms),
-     then ONE all-reduce of the 7 terms;
-  3. the fused block steps of every owned block at the common anchor
-     (bd3mg_mg_steps, in place).
+  2. ONE bd3mg_jacobi_sweep over the owned blocks: recorder pass of the
+     anchor on owned rows (f terms + stop-rule norms), then the fused block
+     steps at the common anchor (in place);
+  3. ONE all-reduce of the 7 recorder terms.
 
 Per-block arithmetic is identical to the single-GPU sweep (same rows, same
-fixed reduction trees), so the iterate is bitwise independent of P.  The
-recorder pass of sweep k runs at the start of sweep k+1 (after the halo
-exchange that makes x_k current on every rank); ``finish()`` evaluates the
-last one.
+fixed reduction trees), so the iterate is bitwise independent of P.  As on
+one GPU, the recorder pass of sweep k's result runs at the start of sweep
+k+1 (after the halo exchange makes x_k current on every rank); ``finish()``
+evaluates the last one.
 """
 
 from __future__ import annotations
@@ -100,10 +100,14 @@ def exchange_halos(buf: torch.Tensor, z0: int, plan, group=None) -> None:
 
 
 class ShardedJacobi:
-    """GPU block-Jacobi shard of this rank (NCCL halos, fused CUDA steps)."""
+    """GPU block-Jacobi shard of this rank: NCCL halos + one fused
+    ``bd3mg_jacobi_sweep`` over the owned blocks (recorder on owned rows,
+    whose 7 terms are all-reduced)."""
 
     def __init__(self, obj, x0, block_height: int, dtype: torch.dtype = torch.float64, group=None,
-                 rank: int | None = None, world: int | None = None):
+                 rank: int | None = None, world: int | None = None, hd_cache: bool = False):
+        import ctypes as C
+
         from . import _native as N
         from . import device as D
 
@@ -111,7 +115,6 @@ class ShardedJacobi:
         self.obj, self.dtype, self.group = obj, dtype, group
         self.rank = dist.get_rank(group) if rank is None else rank
         self.world = dist.get_world_size(group) if world is None else world
-        self.virtual = rank is not None  # single-process emulation: caller drives exchange/reduce
         dims = obj.dims
         self.layout = SlabLayout.build(dims.nz, obj.psf.kdims.kz, block_height, self.world)
         self.blocks = self.layout.owned_blocks(self.rank)
@@ -123,69 +126,63 @@ class ShardedJacobi:
         self.x = torch.from_numpy(x0[self.l_lo:self.l_hi + 1]).to(dev).to(dtype).contiguous()
         self.y = torch.from_numpy(obj.y[self.l_lo:self.l_hi + 1]).to(dev).to(dtype).contiguous()
         self.prev = torch.zeros_like(self.x)
-        self.snap = self.x.clone()
         self.plane = dims.ny * dims.nx
-        z0 = self.l_lo
+        self.snap = self.x[self.o_lo - self.l_lo:self.o_hi - self.l_lo + 1].clone()
         esz = self.x.element_size()
-        y_shift = self.y.data_ptr() - z0 * self.plane * esz  # y + z*plane is row z (C ABI contract)
-        self.y_shift = y_shift
-
-        def rows(t, b):
-            return t[b.z_lo - z0:b.z_hi - z0 + 1]
-
-        self.tasks = (N.Task * len(self.blocks))(*[
-            N.Task(self.x.data_ptr(), z0, self.x.shape[0], b.z_lo, b.z_hi, rows(self.prev, b).data_ptr(), None,
-                   rows(self.x, b).data_ptr(), rows(self.prev, b).data_ptr()) for b in self.blocks])
+        self.y_shift = self.y.data_ptr() - self.l_lo * self.plane * esz  # y + z*plane = row z (C ABI contract)
+        self._barr = (C.c_int64 * (2 * len(self.blocks)))(*[v for b in self.blocks for v in (b.z_lo, b.z_hi)])
         self.geom = obj.geom(dtype)
         self.reg = D.reg(obj.params)
-        self.ws_bytes = N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(self.geom), self.tasks, len(self.blocks)))
-        self.ev_bytes = N.ws_bytes(N.lib.bd3mg_eval_rows_ws_bytes(D.byref(self.geom), self.o_lo, self.o_hi))
+        self.sw = N.Sweep(self.x.data_ptr(), self.prev.data_ptr(), self.l_lo, self.x.shape[0], self._barr,
+                          len(self.blocks), self.o_lo, self.o_hi, self.snap.data_ptr(), None)
+        self.hd = None
+        if hd_cache:
+            n = N.lib.bd3mg_jacobi_cache_elems(D.byref(self.geom), D.byref(self.sw))
+            self.hd = torch.zeros(n, dtype=dtype, device=dev)
+            self.sw.hd_cache = self.hd.data_ptr()
+        self.ws_bytes = N.ws_bytes(N.lib.bd3mg_jacobi_sweep_ws_bytes(D.byref(self.geom), D.byref(self.sw)))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.ev_bytes = N.ws_bytes(N.lib.bd3mg_eval_rows_ws_bytes(D.byref(self.geom), self.o_lo, self.o_hi))
         self.ews = torch.empty(self.ev_bytes, dtype=torch.uint8, device=dev)
         self.info = torch.empty((len(self.blocks), N.INFO_DOUBLES), dtype=torch.float64, device=dev)
         self.terms = torch.zeros(N.EVAL_DOUBLES, dtype=torch.float64, device=dev)
         self.K = obj.psf.device_kernels(dtype, dev)
         self.k = 0
-        self.sweeps = 0
-        self.log_terms: list[torch.Tensor] = []
 
     @property
     def nblocks(self) -> int:
         return len(self.layout.blocks)
 
-    # -- phases of one sweep (sweep() runs them; a single-process emulation
-    #    of several ranks drives them itself) --------------------------------
+    # -- phases (sweep() runs them; a single-process emulation of several
+    #    ranks drives them itself) -----------------------------------------
     def exchange(self) -> None:
         exchange_halos(self.x, self.l_lo, self.plan, self.group)
 
-    def record_local(self) -> None:
-        """This rank's share of the recorder pass (owned rows)."""
+    def local_sweep(self) -> None:
+        """Recorder terms of the anchor on owned rows (local sums) + the fused
+        steps of the owned blocks."""
         N, D = self.N, self.D
-        esz = self.x.element_size()
-        off = (self.o_lo - self.l_lo) * self.plane * esz
-        N.check(N.lib.bd3mg_eval_rows(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(),
-                                      self.y.data_ptr() + off, self.x.data_ptr(), self.l_lo, self.x.shape[0],
-                                      self.o_lo, self.o_hi, self.snap.data_ptr() + off, self.terms.data_ptr(),
-                                      self.ews.data_ptr(), self.ev_bytes, D.stream_handle()))
-
-    def step(self) -> None:
-        N, D = self.N, self.D
-        N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.y_shift,
-                                     self.tasks, len(self.blocks), self.info.data_ptr(), self.ws.data_ptr(),
-                                     self.ws_bytes, D.stream_handle()))
-        self.sweeps += 1
+        N.check(N.lib.bd3mg_jacobi_sweep(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.y_shift,
+                                         D.byref(self.sw), self.terms.data_ptr(), self.info.data_ptr(),
+                                         self.ws.data_ptr(), self.ws_bytes, D.stream_handle()))
         self.k += self.nblocks
 
     def sweep(self) -> None:
         self.exchange()
-        if self.sweeps > 0:   # recorder pass of the previous sweep (x current everywhere)
-            self.record_local()
-            dist.all_reduce(self.terms, group=self.group)
-            self.snap.copy_(self.x)
-        self.step()
+        self.local_sweep()
+        dist.all_reduce(self.terms, group=self.group)
+
+    def record_local(self) -> None:
+        """Recorder terms of the current iterate on owned rows (halos must be current)."""
+        N, D = self.N, self.D
+        off = (self.o_lo - self.l_lo) * self.plane * self.x.element_size()
+        N.check(N.lib.bd3mg_eval_rows(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(),
+                                      self.y.data_ptr() + off, self.x.data_ptr(), self.l_lo, self.x.shape[0],
+                                      self.o_lo, self.o_hi, self.snap.data_ptr(), self.terms.data_ptr(),
+                                      self.ews.data_ptr(), self.ev_bytes, D.stream_handle()))
 
     def finish(self) -> float:
-        """Recorder pass of the last sweep; returns f(x)."""
+        """Recorder pass of the last sweep's result; returns f(x)."""
         self.exchange()
         self.record_local()
         dist.all_reduce(self.terms, group=self.group)
@@ -204,11 +201,10 @@ class ShardedJacobi:
     def gather(self) -> np.ndarray | None:
         """Full iterate on rank 0 (owned planes from every rank)."""
         own = self.x[self.o_lo - self.l_lo:self.o_hi - self.l_lo + 1].contiguous()
-        sizes = [self.layout.owned(q) for q in range(self.world)]
         if self.rank == 0:
             parts = [own]
             for q in range(1, self.world):
-                lo, hi = sizes[q]
+                lo, hi = self.layout.owned(q)
                 t = torch.empty((hi - lo + 1,) + tuple(own.shape[1:]), dtype=own.dtype, device=own.device)
                 dist.recv(t, q, group=self.group)
                 parts.append(t)

@@ -19,6 +19,7 @@ whole run; per sweep one fused pass returns f(x) and the stop-rule norms.
 from __future__ import annotations
 
 import csv
+import ctypes as C
 import heapq
 import math
 import queue
@@ -447,18 +448,24 @@ def write_log_csv(log: list[IterationLogEntry], sink) -> None:
 # ---------------------------------------------------------------------------
 class JacobiSweeper:
     """Device-resident block-Jacobi driver: ``run_bp3mg_barrier`` with
-    workers = #blocks, where every cycle is one sweep (runtime.py:244-292).
+    workers = #blocks, every cycle one sweep (runtime.py:244-292).
 
-    One sweep = one batched ``bd3mg_mg_steps`` launch set (all blocks at the
-    common anchor, in-place update of x and the memory store) followed by the
-    per-sweep recorder pass (f(x) and the stop-rule norms against the
-    previous sweep's snapshot, runtime.py:120 / scheduler.py:208-219) and the
-    snapshot roll.  All buffers are preallocated and every launch goes to
-    the current stream, so a sweep can be captured as a CUDA graph.
+    One sweep = ONE ``bd3mg_jacobi_sweep`` call: the recorder pass of the
+    anchor x_k (f(x_k) and the stop-rule norms against the previous
+    snapshot, runtime.py:120 / scheduler.py:208-219 -- its data term is the
+    residual the block steps compute anyway), the snapshot roll, and the
+    fused steps of all blocks at the anchor with the in-place update.  The
+    recorder of sweep k's result therefore runs at the start of sweep k+1;
+    ``finish()`` records the last one.  All buffers are preallocated and all
+    launches go to the current stream, so a sweep can be a CUDA graph.
+
+    ``hd_cache=True`` selects the "hd-cache" variant: H E_S d_mem is kept
+    from each block's previous visit (linearity of H) so the Gram needs one
+    forward correlation instead of two.
     """
 
     def __init__(self, obj: Objective, x0, block_height: int, dtype: torch.dtype = torch.float64,
-                 blocks: list | None = None):
+                 blocks: list | None = None, hd_cache: bool = False):
         self.obj = obj
         self.dtype = dtype
         self.x = D.to_device(x0, dtype).clone()
@@ -466,16 +473,20 @@ class JacobiSweeper:
         self.snap = self.x.clone()
         dims = obj.dims
         self.blocks = blocks or scheduler.partition_blocks(dims.nz, block_height)
-        self.tasks = (N.Task * len(self.blocks))(*[
-            N.Task(self.x.data_ptr(), 0, dims.nz, b.z_lo, b.z_hi, _rows(self.prev, b.z_lo, b.z_hi).data_ptr(),
-                   None, _rows(self.x, b.z_lo, b.z_hi).data_ptr(), _rows(self.prev, b.z_lo, b.z_hi).data_ptr())
-            for b in self.blocks])
+        self._barr = (C.c_int64 * (2 * len(self.blocks)))(*[v for b in self.blocks for v in (b.z_lo, b.z_hi)])
         self.geom = obj.geom(dtype)
         self.reg = D.reg(obj.params)
-        self.ws_bytes = N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(self.geom), self.tasks, len(self.blocks)))
-        self.eval_bytes = N.ws_bytes(N.lib.bd3mg_eval_f_ws_bytes(D.byref(self.geom)))
+        self.sw = N.Sweep(self.x.data_ptr(), self.prev.data_ptr(), 0, dims.nz, self._barr, len(self.blocks),
+                          0, dims.nz - 1, self.snap.data_ptr(), None)
         dev = self.x.device
+        self.hd = None
+        if hd_cache:
+            n = N.lib.bd3mg_jacobi_cache_elems(D.byref(self.geom), D.byref(self.sw))
+            self.hd = torch.zeros(n, dtype=dtype, device=dev)
+            self.sw.hd_cache = self.hd.data_ptr()
+        self.ws_bytes = N.ws_bytes(N.lib.bd3mg_jacobi_sweep_ws_bytes(D.byref(self.geom), D.byref(self.sw)))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.eval_bytes = N.ws_bytes(N.lib.bd3mg_eval_f_ws_bytes(D.byref(self.geom)))
         self.ews = torch.empty(self.eval_bytes, dtype=torch.uint8, device=dev)
         self.info = torch.empty((len(self.blocks), N.INFO_DOUBLES), dtype=torch.float64, device=dev)
         self.terms = torch.empty(N.EVAL_DOUBLES, dtype=torch.float64, device=dev)
@@ -489,14 +500,10 @@ class JacobiSweeper:
         return len(self.blocks)
 
     def _launch(self) -> None:
-        s = D.stream_handle()
-        N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
-                                     self.tasks, len(self.blocks), self.info.data_ptr(), self.ws.data_ptr(),
-                                     self.ws_bytes, s))
-        N.check(N.lib.bd3mg_eval_f(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
-                                   self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
-                                   self.ews.data_ptr(), self.eval_bytes, s))
-        self.snap.copy_(self.x)
+        N.check(N.lib.bd3mg_jacobi_sweep(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(),
+                                         self.Y.data_ptr(), D.byref(self.sw), self.terms.data_ptr(),
+                                         self.info.data_ptr(), self.ws.data_ptr(), self.ws_bytes,
+                                         D.stream_handle()))
 
     def capture(self) -> None:
         """Record one sweep as a CUDA graph (after one eager warm-up sweep)."""
@@ -512,9 +519,17 @@ class JacobiSweeper:
             self._launch()
         self.k += len(self.blocks)
 
+    def finish(self) -> float:
+        """Recorder pass of the current iterate (the last sweep's log entry)."""
+        N.check(N.lib.bd3mg_eval_f(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
+                                   self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
+                                   self.ews.data_ptr(), self.eval_bytes, D.stream_handle()))
+        return self.f()
+
     def check(self) -> None:
         if bool((self.info[:, 8] != 0).any().item()):
             raise ValueError("non-finite gradient")
 
     def f(self) -> float:
+        """f of the anchor recorded by the last sweep (or by finish())."""
         return float(self.terms[4].item())
