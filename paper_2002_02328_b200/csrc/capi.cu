@@ -94,6 +94,35 @@ ConvArgs<T> base_args(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K) {
 }
 
 template <typename T>
+StArgs<T> st_args(const bd3mg_geom_t* g, const bd3mg_reg_t* r) {
+  StArgs<T> a;
+  memset(&a, 0, sizeof(a));
+  a.nz = (int)g->nz; a.ny = (int)g->ny; a.nx = (int)g->nx; a.plane = g->ny * g->nx;
+  a.tiles_x = (int)((g->nx + kTS - 1) / kTS);
+  a.tiles_y = (int)((g->ny + kTS - 1) / kTS);
+  if (r) {
+    a.two_eta = 2.0 * r->eta; a.lam = r->lam; a.two_kappa = 2.0 * r->kappa;
+    a.delta2 = r->delta * r->delta; a.x_min = r->x_min; a.x_max = r->x_max;
+  }
+  return a;
+}
+inline long long st_tiles(const bd3mg_geom_t* g) { return ((g->nx + kTS - 1) / kTS) * ((g->ny + kTS - 1) / kTS); }
+
+// Lay jobs out along grid.z (one plane per z index) and launch `kern`.
+template <typename T, typename Kern>
+cudaError_t st_launch(Kern kern, StArgs<T>& a, cudaStream_t s) {
+  int wb = 0;
+  for (int j = 0; j < a.njobs; ++j) {
+    a.jobs[j].work_begin = wb;
+    wb += a.jobs[j].hi - a.jobs[j].lo + 1;
+  }
+  if (wb == 0) return cudaSuccess;
+  kern<<<dim3(a.tiles_x, a.tiles_y, wb), kStNT, 0, s>>>(a);
+  launched();
+  return cudaGetLastError();
+}
+
+template <typename T>
 long long conv_rows(const bd3mg_geom_t* g, int mode, long long work) {
   const ConvGrid cg = conv_grid<T>(g->ky, g->kx, mode, (int)g->ny, (int)g->nx);
   return work * cg.tiles_x * cg.tiles_y;
@@ -153,9 +182,17 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   const int64_t o_lo = std::max<int64_t>(0, lo - rz), o_hi = std::min<int64_t>(nz - 1, hi + rz);
   const int64_t nr = o_hi - o_lo + 1, h = hi - lo + 1;
   T* rbuf = ws.take<T>(nr * plane);
+  T* greg = ws.take<T>(h * plane);
   double* parts = ws.take<double>(conv_rows<T>(g, M_RESID, nr));
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  {
+    StArgs<T> sa = st_args<T>(g, r);
+    sa.njobs = 1;
+    sa.jobs[0].a = frag; sa.jobs[0].a_z0 = frag_z0; sa.jobs[0].lo = (int)lo; sa.jobs[0].hi = (int)hi;
+    sa.jobs[0].out0 = greg; sa.jobs[0].out1 = omega_out;
+    CU(st_launch<T>(greg_kernel<T>, sa, s));
+  }
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
   a.partials = parts;
@@ -168,8 +205,7 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   b.njobs = 1;
   ConvJob<T>& j = b.jobs[0];
   j.src0 = rbuf; j.src_z0 = o_lo; j.src_nz = (int)nr;
-  j.dst0 = g_out; j.omega = omega_out;
-  j.xg = frag; j.xg_z0 = frag_z0; j.xg_nz = (int)nzf;
+  j.dst0 = g_out; j.sub = greg;
   j.out_lo = (int)lo; j.nout = (int)h;
   CU(conv_launch<T>(M_GRAD, true, b, (int)h, s));
   launched();
@@ -190,8 +226,8 @@ int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   const int64_t nr = hi - lo + 1, n = nr * plane;
   const long long crow = conv_rows<T>(g, M_RESID, nr);
   double* parts = ws.take<double>(crow);
-  const int ctas = (int)std::min<int64_t>((nr * g->ny + (kEwNT / 32) - 1) / (kEwNT / 32), 4 * 148);
-  double* eparts = ws.take<double>((size_t)ctas * kEvalNV);
+  const long long erows = nr * st_tiles(g);
+  double* eparts = ws.take<double>((size_t)erows * kEvalNV);
   double* sums = ws.take<double>(8);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
@@ -204,13 +240,12 @@ int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   CU(conv_launch<T>(M_RESID, false, a, (int)nr, s));
   launched();
   CU(reduce(parts, 1, {{0, crow}}, sums, 1, s));
-  EvalArgs<T> e;
-  e.x = frag + (lo - frag_z0) * plane; e.snap = snap_rows; e.lo = (int)lo; e.nz = (int)nz;
-  e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane; e.n = n;
-  e.delta2 = r->delta * r->delta; e.x_min = r->x_min; e.x_max = r->x_max; e.ctas = ctas;
-  eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts); launched();
-  CU(cudaGetLastError());
-  CU(reduce(eparts, kEvalNV, {{0, ctas}}, sums + 1, kEvalNV, s));
+  StArgs<T> e = st_args<T>(g, r);
+  e.njobs = 1;
+  e.jobs[0].a = frag; e.jobs[0].a_z0 = frag_z0; e.jobs[0].b = snap_rows; e.jobs[0].lo = (int)lo; e.jobs[0].hi = (int)hi;
+  e.partials = eparts;
+  CU(st_launch<T>(eval_kernel<T>, e, s));
+  CU(reduce(eparts, kEvalNV, {{0, erows}}, sums + 1, kEvalNV, s));
   eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
@@ -314,8 +349,12 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       resid_work += r_n[t];
     }
   }
-  std::vector<T*> gb(nt), wb(nt);
-  for (int t = 0; t < nt; ++t) { gb[t] = ws.take<T>(h[t] * plane); wb[t] = ws.take<T>(h[t] * plane); }
+  std::vector<T*> gb(nt), wb(nt), grb(nt);
+  for (int t = 0; t < nt; ++t) {
+    gb[t] = ws.take<T>(h[t] * plane);
+    wb[t] = ws.take<T>(h[t] * plane);
+    grb[t] = ws.take<T>(h[t] * plane);
+  }
   long long gram_work = 0;
   for (int t = 0; t < nt; ++t) gram_work += ohi[t] - olo[t] + 1;
   const bool cached = opt.hd != nullptr;
@@ -328,15 +367,9 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     return fail(BD3MG_EINVAL, "recorder rows outside the residual rows");
   const long long conv_part_rows = std::max(conv_rows<T>(g, M_RESID, resid_work), conv_rows<T>(g, gmode, gram_work));
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
-  // reg partials: ctas per task proportional to block size, capped
-  std::vector<int> rctas(nt);
-  long long reg_rows = 0;
-  int max_ctas = 1;
-  for (int t = 0; t < nt; ++t) {
-    rctas[t] = (int)std::max<int64_t>(1, std::min<int64_t>((h[t] * g->ny + 2 * (kEwNT / 32) - 1) / (2 * (kEwNT / 32)), 256));
-    reg_rows += rctas[t];
-    max_ctas = std::max(max_ctas, rctas[t]);
-  }
+  long long hsum = 0;
+  for (int t = 0; t < nt; ++t) hsum += h[t];
+  const long long reg_rows = hsum * st_tiles(g);
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
   double* data3 = ws.take<double>((size_t)nt * 3);
   double* reg12 = ws.take<double>((size_t)nt * kRegNV);
@@ -373,7 +406,17 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     else
       CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
   }
-  // (2) g = H^T r + regulariser gradient; omega
+  // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
+  {
+    StArgs<T> sa = st_args<T>(g, r);
+    sa.njobs = nt;
+    for (int t = 0; t < nt; ++t) {
+      StJob<T>& J = sa.jobs[t];
+      J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
+      J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi; J.out0 = grb[t]; J.out1 = wb[t];
+    }
+    CU(st_launch<T>(greg_kernel<T>, sa, s));
+  }
   {
     ConvArgs<T> a = base_args<T>(g, r, K);
     a.njobs = nt;
@@ -381,30 +424,24 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     for (int t = 0; t < nt; ++t) {
       ConvJob<T>& j = a.jobs[t];
       j.src0 = rb[t]; j.src_z0 = r_z0[t]; j.src_nz = (int)r_n[t];
-      j.dst0 = gb[t]; j.omega = wb[t];
-      j.xg = (const T*)tasks[t].frag; j.xg_z0 = tasks[t].frag_z0; j.xg_nz = (int)tasks[t].nzf;
+      j.dst0 = gb[t]; j.sub = grb[t];
       j.out_lo = (int)tasks[t].z_lo; j.nout = (int)h[t]; j.work_begin = wbeg;
       wbeg += (int)h[t];
     }
-    long long work = 0;
-    for (int t = 0; t < nt; ++t) work += h[t];
-    CU(conv_launch<T>(M_GRAD, true, a, (int)work, s));
-  launched();
+    CU(conv_launch<T>(M_GRAD, true, a, (int)hsum, s));
+    launched();
   }
-  // (3) regulariser Gram terms + rhs + flags
+  // (3) regulariser Gram terms + rhs + flags (tiled stencil)
   {
-    RegArgs<T> ra;
-    memset(&ra, 0, sizeof(ra));
-    ra.ny = (int)g->ny; ra.nx = (int)g->nx; ra.nz = (int)nz; ra.plane = plane; ra.nblocks = nt;
-    long long rb0 = 0;
+    StArgs<T> sa = st_args<T>(g, r);
+    sa.njobs = nt;
+    sa.partials = rparts;
     for (int t = 0; t < nt; ++t) {
-      RegBlock<T>& B = ra.blk[t];
-      B.g = gb[t]; B.d = (const T*)tasks[t].d_mem; B.omega = wb[t];
-      B.lo = (int)tasks[t].z_lo; B.hi = (int)tasks[t].z_hi; B.ctas = rctas[t]; B.row_begin = rb0;
-      rb0 += rctas[t];
+      StJob<T>& J = sa.jobs[t];
+      J.a = gb[t]; J.a_z0 = tasks[t].z_lo; J.b = (const T*)tasks[t].d_mem; J.w = wb[t];
+      J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi;
     }
-    reg_gram_kernel<T><<<dim3(max_ctas, nt), kEwNT, 0, s>>>(ra, rparts); launched();
-    CU(cudaGetLastError());
+    CU(st_launch<T>(reg_gram_kernel<T>, sa, s));
   }
   // (4) data Gram <H b_i, H b_j> (forward only, both columns share the taps)
   std::vector<std::pair<long long, long long>> granges(nt);
@@ -432,7 +469,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   {
     std::vector<std::pair<long long, long long>> rr(nt);
     long long b0 = 0;
-    for (int t = 0; t < nt; ++t) { rr[t] = {b0, b0 + rctas[t]}; b0 += rctas[t]; }
+    const long long tl = st_tiles(g);
+    for (int t = 0; t < nt; ++t) { rr[t] = {b0, b0 + h[t] * tl}; b0 += h[t] * tl; }
     CU(reduce(rparts, kRegNV, rr, reg12, kRegNV, s));
   }
   // (6) 2x2 solves
@@ -527,8 +565,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   }
   const bool rec = sw->rec_hi >= sw->rec_lo;
   const int64_t nrec = rec ? sw->rec_hi - sw->rec_lo + 1 : 0;
-  const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>((nrec * g->ny + (kEwNT / 32) - 1) / (kEwNT / 32), 4 * 148));
-  double* eparts = ws.take<double>((size_t)ctas * kEvalNV);
+  double* eparts = ws.take<double>((size_t)std::max<long long>(1, nrec * st_tiles(g)) * kEvalNV);
   double* sums = ws.take<double>(8);
   StepOpts<T> opt;
   opt.resid_sq = sums;
@@ -547,7 +584,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
 // (the step updates x in place).
 template <typename T>
 int jacobi_record_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const bd3mg_sweep_t* sw, double* eparts,
-                       double* sums, int ctas, cudaStream_t s) {
+                       double* sums, cudaStream_t s) {
   const int64_t plane = g->ny * g->nx;
   if (sw->rec_hi < sw->rec_lo) {
     CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s));
@@ -556,15 +593,16 @@ int jacobi_record_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const bd3mg_
   const int64_t nrec = sw->rec_hi - sw->rec_lo + 1;
   if (sw->rec_lo < sw->frag_z0 || sw->rec_hi >= sw->frag_z0 + sw->nzf)
     return fail(BD3MG_EINVAL, "recorder rows outside the fragment");
-  EvalArgs<T> e;
-  e.x = (const T*)sw->x + (sw->rec_lo - sw->frag_z0) * plane;
-  e.snap = (const T*)sw->snap;
-  e.lo = (int)sw->rec_lo; e.nz = (int)g->nz; e.ny = (int)g->ny; e.nx = (int)g->nx; e.plane = plane;
-  e.n = nrec * plane; e.delta2 = r->delta * r->delta; e.x_min = r->x_min; e.x_max = r->x_max; e.ctas = ctas;
-  eval_terms_kernel<T><<<ctas, kEwNT, 0, s>>>(e, eparts); launched();
-  CU(cudaGetLastError());
-  CU(reduce(eparts, kEvalNV, {{0, ctas}}, sums + 1, kEvalNV, s));
-  if (sw->snap) CU(cudaMemcpyAsync(sw->snap, e.x, (size_t)nrec * plane * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  StArgs<T> e = st_args<T>(g, r);
+  e.njobs = 1;
+  e.jobs[0].a = (const T*)sw->x; e.jobs[0].a_z0 = sw->frag_z0; e.jobs[0].b = (const T*)sw->snap;
+  e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
+  e.partials = eparts;
+  CU(st_launch<T>(eval_kernel<T>, e, s));
+  CU(reduce(eparts, kEvalNV, {{0, nrec * st_tiles(g)}}, sums + 1, kEvalNV, s));
+  if (sw->snap)
+    CU(cudaMemcpyAsync(sw->snap, (const T*)sw->x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
+                       cudaMemcpyDeviceToDevice, s));
   return BD3MG_OK;
 }
 
@@ -860,12 +898,11 @@ int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* 
   cudaStream_t s = (cudaStream_t)stream;
   // scratch layout mirrors jacobi_sweep_impl: [eparts][sums][step scratch]
   const int64_t nrec = sw->rec_hi >= sw->rec_lo ? sw->rec_hi - sw->rec_lo + 1 : 0;
-  const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>((nrec * g->ny + (kEwNT / 32) - 1) / (kEwNT / 32), 4 * 148));
   Ws probe = ws;
-  double* eparts = probe.take<double>((size_t)ctas * kEvalNV);
+  double* eparts = probe.take<double>((size_t)std::max<long long>(1, nrec * st_tiles(g)) * kEvalNV);
   double* sums = probe.take<double>(8);
-  rc = DISPATCH_T(g, jacobi_record_impl<double>(g, r, sw, eparts, sums, ctas, s),
-                  jacobi_record_impl<float>(g, r, sw, eparts, sums, ctas, s));
+  rc = DISPATCH_T(g, jacobi_record_impl<double>(g, r, sw, eparts, sums, s),
+                  jacobi_record_impl<float>(g, r, sw, eparts, sums, s));
   if (rc) return rc;
   rc = DISPATCH_T(g,
                   jacobi_sweep_impl<double>(g, r, (const double*)kernels, (const double*)y, sw, terms_out, info_out,

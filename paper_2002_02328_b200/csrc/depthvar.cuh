@@ -36,7 +36,7 @@ namespace bd3mg {
 enum ConvMode : int {
   M_STORE = 0,  // dst0 = acc
   M_RESID = 1,  // dst0 = acc - sub; partial: sum dst0^2
-  M_GRAD = 2,   // (adjoint) dst0 = acc + 2eta*box + lam*tv + 2kappa*axial; omega out
+  M_GRAD = 2,   // (adjoint) dst0 = acc + sub (sub = regulariser gradient rows, greg_kernel)
   M_GRAM1 = 3,  // partial: sum acc0^2               (+ optional store dst0 = acc0)
   M_GRAM2 = 4,  // partial: acc0^2, acc0*acc1, acc1^2 (dual input, shared taps)
   M_GRAMC = 5,  // dst0 = acc0 (H E_S g); partial: acc0^2, acc0*c, c^2 with c = sub[o] (cached H E_S d)
@@ -109,62 +109,6 @@ template <typename T>
 BD3MG_D T omega_of(T dx, T dy, T delta2) {
   const T s = add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), delta2);
   return T(1) / sqrt(s);
-}
-
-// gradient epilogue at one voxel: objective.py:172-186
-template <typename T>
-BD3MG_D T grad_voxel(T hta, const XView<T>& xv, int z, int y, int x, int nz_global, T two_eta, T lam,
-                     T two_kappa, T delta2, T x_min, T x_max, T* omega_out) {
-  const T xc = xv.at(z, y, x);
-  // 2*eta*(x - clip(x))
-  const T clipped = xc < x_min ? x_min : (xc > x_max ? x_max : xc);
-  T g = add_rn(hta, mul_rn(two_eta, sub_rn(xc, clipped)));
-  // lam * (Dx^T(w Dx x) + Dy^T(w Dy x))
-  const T dx0 = fdx(xv, z, y, x), dy0 = fdy(xv, z, y, x);
-  const T w0 = omega_of(dx0, dy0, delta2);
-  *omega_out = w0;
-  const T px0 = mul_rn(w0, dx0), py0 = mul_rn(w0, dy0);
-  T tvx, tvy;
-  if (xv.nx == 1) {
-    tvx = T(0);
-  } else if (x == 0) {
-    tvx = -px0;
-  } else {
-    const T dxm = fdx(xv, z, y, x - 1), dym = fdy(xv, z, y, x - 1);
-    const T pxm = mul_rn(omega_of(dxm, dym, delta2), dxm);
-    tvx = (x == xv.nx - 1) ? pxm : sub_rn(pxm, px0);
-  }
-  if (xv.ny == 1) {
-    tvy = T(0);
-  } else if (y == 0) {
-    tvy = -py0;
-  } else {
-    const T dxm = fdx(xv, z, y - 1, x), dym = fdy(xv, z, y - 1, x);
-    const T pym = mul_rn(omega_of(dxm, dym, delta2), dym);
-    tvy = (y == xv.ny - 1) ? pym : sub_rn(pym, py0);
-  }
-  g = add_rn(g, mul_rn(lam, add_rn(tvx, tvy)));
-  // 2*kappa*(dz[z-1] - dz[z]), dz[t] = x[t+1]-x[t] for 0 <= t < nz-1
-  const T dzm = (z - 1 >= 0 && z - 1 < nz_global - 1) ? sub_rn(xc, xv.at(z - 1, y, x)) : T(0);
-  const T dzp = (z < nz_global - 1) ? sub_rn(xv.at(z + 1, y, x), xc) : T(0);
-  g = add_rn(g, mul_rn(two_kappa, sub_rn(dzm, dzp)));
-  return g;
-}
-
-// Same gradient with w*Dx / w*Dy of the pixel and of its left / upper
-// neighbours precomputed (shared-memory epilogue of the tiled kernel).
-template <typename T>
-BD3MG_D T grad_combine(T hta, const XView<T>& xv, int z, int y, int x, int nz_global, T px0, T pxm, T py0, T pym,
-                       T two_eta, T lam, T two_kappa, T x_min, T x_max) {
-  const T xc = xv.at(z, y, x);
-  const T clipped = xc < x_min ? x_min : (xc > x_max ? x_max : xc);
-  T g = add_rn(hta, mul_rn(two_eta, sub_rn(xc, clipped)));
-  const T tvx = (xv.nx == 1) ? T(0) : (x == 0) ? -px0 : (x == xv.nx - 1) ? pxm : sub_rn(pxm, px0);
-  const T tvy = (xv.ny == 1) ? T(0) : (y == 0) ? -py0 : (y == xv.ny - 1) ? pym : sub_rn(pym, py0);
-  g = add_rn(g, mul_rn(lam, add_rn(tvx, tvy)));
-  const T dzm = (z - 1 >= 0 && z - 1 < nz_global - 1) ? sub_rn(xc, xv.at(z - 1, y, x)) : T(0);
-  const T dzp = (z < nz_global - 1) ? sub_rn(xv.at(z + 1, y, x), xc) : T(0);
-  return add_rn(g, mul_rn(two_kappa, sub_rn(dzm, dzp)));
 }
 
 // ---------------------------------------------------------------------------
@@ -381,32 +325,6 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
 #pragma unroll
   for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
   const long long orow = (long long)(zo - job.out_lo) * p.plane;
-  XView<T> xv;
-  constexpr int EW = Cfg::TX + 1, EH = Cfg::TY + 1;  // w*Dx / w*Dy region incl. left/top neighbours
-  T* pxs = tiles;
-  T* pys = tiles + EH * EW;
-  if constexpr (MODE == M_GRAD) {
-    static_assert(2 * EH * EW * sizeof(T) <= 2 * Cfg::TILE_BYTES, "epilogue scratch exceeds tile buffers");
-    xv.p = job.xg; xv.z0 = job.xg_z0; xv.nzv = job.xg_nz; xv.ny = p.ny; xv.nx = p.nx; xv.plane = p.plane;
-    // the conv loop ended with a barrier: the tile buffers are free
-    const T d2 = (T)p.delta2;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < EH * EW; idx += Cfg::NT) {
-      const int r = idx / EW, c = idx - r * EW;
-      const int y = y0 - 1 + r, x = x0 - 1 + c;
-      T px = T(0), py = T(0);
-      if (y >= 0 && y < p.ny && x >= 0 && x < p.nx) {
-        const T dx = fdx(xv, zo, y, x), dy = fdy(xv, zo, y, x);
-        const T w = omega_of(dx, dy, d2);
-        px = mul_rn(w, dx);
-        py = mul_rn(w, dy);
-        if (r >= 1 && c >= 1) job.omega[orow + (long long)y * p.nx + x] = w;  // this tile's own pixel
-      }
-      pxs[idx] = px;
-      pys[idx] = py;
-    }
-    __syncthreads();
-  }
 #pragma unroll
   for (int r = 0; r < RY; ++r) {
     const int y = y0 + ty * RY + r;
@@ -424,10 +342,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
         if (job.dst0) job.dst0[o] = res;
         part[0] += (double)res * (double)res;
       } else if constexpr (MODE == M_GRAD) {
-        const int er = y - y0 + 1, ec = x - x0 + 1;
-        job.dst0[o] = grad_combine<T>(a0, xv, zo, y, x, p.nz_global, pxs[er * EW + ec], pxs[er * EW + ec - 1],
-                                      pys[er * EW + ec], pys[(er - 1) * EW + ec], (T)p.two_eta, (T)p.lam,
-                                      (T)p.two_kappa, (T)p.x_min, (T)p.x_max);
+        job.dst0[o] = add_rn(a0, job.sub[o]);
       } else if constexpr (MODE == M_GRAM1) {
         if (job.dst0) job.dst0[o] = a0;
         part[0] += (double)a0 * (double)a0;
@@ -506,12 +421,7 @@ __global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_c
       if (job.dst0) job.dst0[o] = res;
       part[0] = (double)res * (double)res;
     } else if constexpr (MODE == M_GRAD) {
-      XView<T> xv{job.xg, job.xg_z0, job.xg_nz, p.ny, p.nx, p.plane};
-      T w;
-      const T g = grad_voxel<T>(acc0, xv, zo, y, x, p.nz_global, (T)p.two_eta, (T)p.lam, (T)p.two_kappa,
-                                (T)p.delta2, (T)p.x_min, (T)p.x_max, &w);
-      job.dst0[o] = g;
-      job.omega[o] = w;
+      job.dst0[o] = add_rn(acc0, job.sub[o]);
     } else if constexpr (MODE == M_GRAM1) {
       if (job.dst0) job.dst0[o] = acc0;
       part[0] = (double)acc0 * (double)acc0;

@@ -4,14 +4,12 @@
 // deterministic two-level reductions that feed them.
 #pragma once
 
-#include "depthvar.cuh"
+#include "stencil.cuh"
 
 namespace bd3mg {
 
 constexpr int kEwNT = 256;           // threads per CTA, elementwise kernels
-constexpr int kRegNV = 12;           // sums produced per block by reg_gram
 constexpr int kInfoNV = 16;          // doubles of StepInfo per block
-constexpr int kEvalNV = 5;           // box, tv, axial, |x-snap|^2, |snap|^2
 
 // ---------------------------------------------------------------------------
 // Deterministic final reduction: out[j*nv + k] = sum_{r in [begin_j, end_j)}
@@ -39,96 +37,6 @@ __global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __rest
     }
     if (threadIdx.x == 0) out[j * out_stride + k] = s[0];
     __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Regulariser part of the forward-only Gram D^T A_S D for D = [-g, d]
-// (reference directions.py:80-85 with A from objective.py:262-274):
-//   e_ij = <b_i,b_j>, t_ij = sum w (Dx b_i Dx b_j + Dy b_i Dy b_j),
-//   a_ij = <Dz E b_i, Dz E b_j> (block-embedded axial differences)
-// plus rhs pieces <g,d>, and the nonzero / non-finite counts of g.
-template <typename T>
-struct RegBlock {
-  const T* g;      // block rows
-  const T* d;      // block rows or null (zero memory direction)
-  const T* omega;  // block rows
-  int lo, hi;
-  int ctas;        // CTAs assigned to this block
-  long long row_begin;  // first partial row of this block
-};
-template <typename T>
-struct RegArgs {
-  int ny, nx, nz;
-  long long plane;
-  int nblocks;
-  RegBlock<T> blk[kMaxJobs];
-};
-
-template <typename T>
-__global__ void __launch_bounds__(kEwNT) reg_gram_kernel(const __grid_constant__ RegArgs<T> p,
-                                                          double* __restrict__ partials) {
-  __shared__ double red[(kEwNT / 32) * kRegNV];
-  const RegBlock<T>& B = p.blk[blockIdx.y];
-  if ((int)blockIdx.x >= B.ctas) return;  // uniform per CTA
-  const int h = B.hi - B.lo + 1;
-  double v[kRegNV];
-#pragma unroll
-  for (int k = 0; k < kRegNV; ++k) v[k] = 0.0;
-  const XView<T> gv{B.g, B.lo, h, p.ny, p.nx, p.plane};
-  const XView<T> dv{B.d, B.lo, h, p.ny, p.nx, p.plane};
-  const bool has_d = B.d != nullptr;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NWARP = kEwNT / 32;
-  // one warp per (z, y) row: one integer division per row, coalesced x
-  const int rows = h * p.ny;
-  for (int row = blockIdx.x * NWARP + warp; row < rows; row += B.ctas * NWARP) {
-    const int z = B.lo + row / p.ny, y = row - (row / p.ny) * p.ny;
-    const long long rbase = (long long)(z - B.lo) * p.plane + (long long)y * p.nx;
-#pragma unroll 4
-    for (int x = lane; x < p.nx; x += 32) {
-      const T g = gv.at(z, y, x);
-      const T d = has_d ? dv.at(z, y, x) : T(0);
-      const double b0 = -(double)g, b1 = (double)d;
-      v[0] += b0 * b0;
-      v[1] += b0 * b1;
-      v[2] += b1 * b1;
-      const double w = (double)B.omega[rbase + x];
-      const double dx0 = -(double)fdx(gv, z, y, x), dy0 = -(double)fdy(gv, z, y, x);
-      const double dx1 = has_d ? (double)fdx(dv, z, y, x) : 0.0, dy1 = has_d ? (double)fdy(dv, z, y, x) : 0.0;
-      v[3] += w * (dx0 * dx0 + dy0 * dy0);
-      v[4] += w * (dx0 * dx1 + dy0 * dy1);
-      v[5] += w * (dx1 * dx1 + dy1 * dy1);
-      // axial row z (between z and z+1) of the block-embedded vector
-      double z0v, z1v;
-      if (z < B.hi) {
-        z0v = -((double)gv.at(z + 1, y, x) - (double)g);
-        z1v = has_d ? (double)dv.at(z + 1, y, x) - (double)d : 0.0;
-      } else if (B.hi < p.nz - 1) {
-        z0v = -b0;  // row hi sees E b[hi+1] = 0
-        z1v = -b1;
-      } else {
-        z0v = 0.0;
-        z1v = 0.0;
-      }
-      v[6] += z0v * z0v;
-      v[7] += z0v * z1v;
-      v[8] += z1v * z1v;
-      if (z == B.lo && B.lo >= 1) {  // row lo-1: E b[lo] - 0
-        v[6] += b0 * b0;
-        v[7] += b0 * b1;
-        v[8] += b1 * b1;
-      }
-      v[9] += (double)g * (double)d;
-      v[10] += (g != T(0)) ? 1.0 : 0.0;
-      v[11] += isfinite((double)g) ? 0.0 : 1.0;
-    }
-  }
-  cta_reduce<kRegNV, kEwNT>(v, red);
-  if (threadIdx.x == 0) {
-    double* o = partials + (B.row_begin + blockIdx.x) * kRegNV;
-#pragma unroll
-    for (int k = 0; k < kRegNV; ++k) o[k] = v[k];
   }
 }
 
@@ -247,56 +155,6 @@ __global__ void __launch_bounds__(kEwNT) update_kernel(const __grid_constant__ U
     if (B.inc_out) B.inc_out[i] = inc;
     if (B.x) B.x[i] = add_rn(B.x[i], inc);
     if (B.dmem) B.dmem[i] = inc;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Elementwise objective terms over a whole volume (objective.py:148-152) and
-// the stop-rule norms (scheduler.py:218-219).
-template <typename T>
-struct EvalArgs {
-  const T* x;     // row `lo` of the iterate; row lo+1.. follow (axial needs row hi+1)
-  const T* snap;  // row `lo` of the snapshot, may be null
-  int lo, nz, ny, nx;
-  long long plane, n;  // n = rows * plane
-  double delta2, x_min, x_max;
-  int ctas;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(kEwNT) eval_terms_kernel(const __grid_constant__ EvalArgs<T> p,
-                                                            double* __restrict__ partials) {
-  __shared__ double red[(kEwNT / 32) * kEvalNV];
-  double v[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  const XView<T> xv{p.x, p.lo, p.nz, p.ny, p.nx, p.plane};
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NWARP = kEwNT / 32;
-  const int rows = (int)(p.n / p.plane) * p.ny;
-  for (int row = blockIdx.x * NWARP + warp; row < rows; row += p.ctas * NWARP)
-#pragma unroll 4
-  for (int x = lane; x < p.nx; x += 32) {
-    const int zl = row / p.ny, y = row - zl * p.ny, z = p.lo + zl;
-    const long long i = (long long)zl * p.plane + (long long)y * p.nx + x;
-    const double xc = (double)p.x[i];
-    const double cl = xc < p.x_min ? p.x_min : (xc > p.x_max ? p.x_max : xc);
-    const double e = xc - cl;
-    v[0] += e * e;
-    const double dx = (double)fdx(xv, z, y, x), dy = (double)fdy(xv, z, y, x);
-    v[1] += sqrt(dx * dx + dy * dy + p.delta2);
-    if (z < p.nz - 1) {
-      const double dz = (double)p.x[i + p.plane] - xc;
-      v[2] += dz * dz;
-    }
-    if (p.snap) {
-      const double s = (double)p.snap[i];
-      v[3] += (xc - s) * (xc - s);
-      v[4] += s * s;
-    }
-  }
-  cta_reduce<kEvalNV, kEwNT>(v, red);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < kEvalNV; ++k) partials[(long long)blockIdx.x * kEvalNV + k] = v[k];
   }
 }
 

@@ -1,0 +1,237 @@
+// HBM-bound stencil kernels of the block step, 2-D shared-memory tiled:
+// every field is read from DRAM once (neighbours come from the staged tile,
+// the +-1 plane values from L2), every half-quadratic weight is computed once
+// per pixel.
+//
+//   greg_kernel      regulariser gradient 2eta*box + lam*TV + 2kappa*axial and
+//                    the weights omega (reference objective.py:130-137,
+//                    :175-186); the H^T epilogue adds it to H^T r.
+//   reg_gram_kernel  regulariser part of the forward-only Gram for
+//                    D = [-g, d] plus rhs / flags (directions.py:80-85 with A
+//                    from objective.py:262-274).
+//   eval_kernel      box / TV / axial terms of f and the stop-rule norms
+//                    (objective.py:148-152, scheduler.py:218-219).
+#pragma once
+
+#include "depthvar.cuh"
+
+namespace bd3mg {
+
+constexpr int kTS = 32;                 // tile edge (pixels)
+constexpr int kStNT = 256;              // threads: 32 (x) x 8 (y); 4 rows per thread
+constexpr int kStRows = kTS / (kStNT / kTS);
+constexpr int kRegNV = 12;              // sums produced per block by reg_gram
+constexpr int kEvalNV = 5;              // box, tv, axial, |x-snap|^2, |snap|^2
+
+template <typename T>
+struct StJob {
+  const T* a;      // primary field, plane 0 = depth a_z0 (x for greg/eval, g for reg_gram)
+  const T* b;      // reg_gram: d (plane 0 = depth lo) or null; eval: snapshot rows (row 0 = lo) or null
+  const T* w;      // reg_gram: omega rows (row 0 = lo)
+  T* out0;         // greg: regulariser gradient rows (row 0 = lo)
+  T* out1;         // greg: omega rows (row 0 = lo)
+  long long a_z0;
+  int lo, hi;      // rows of the job
+  int work_begin;  // first grid.z index of the job
+  int pad_;
+};
+
+template <typename T>
+struct StArgs {
+  int nz, ny, nx;
+  long long plane;
+  int njobs, tiles_x, tiles_y;
+  double two_eta, lam, two_kappa, delta2, x_min, x_max;
+  double* partials;  // reg_gram / eval: [grid.z * tiles][NV]
+  StJob<T> jobs[kMaxJobs];
+};
+
+template <typename T>
+BD3MG_D int st_find_job(const StArgs<T>& p, int zidx) {
+  int j = 0;
+  while (j + 1 < p.njobs && p.jobs[j + 1].work_begin <= zidx) ++j;
+  return j;
+}
+
+// Load plane rows [y0+oy, y0+oy+H) x cols [x0+ox, x0+ox+W) into s (pitch P);
+// out-of-volume entries are 0 (never used: the far-face rules mask them).
+template <typename T, int H, int W, int P>
+BD3MG_D void st_load(T* s, const T* plane, int y0, int x0, int oy, int ox, int ny, int nx) {
+  for (int i = threadIdx.x; i < H * W; i += kStNT) {
+    const int r = i / W, c = i - r * W;
+    const int y = y0 + oy + r, x = x0 + ox + c;
+    s[r * P + c] = (y >= 0 && y < ny && x >= 0 && x < nx) ? plane[(long long)y * nx + x] : T(0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kStNT) greg_kernel(const __grid_constant__ StArgs<T> p) {
+  constexpr int XP = kTS + 3;  // xs: rows/cols y0-1 .. y0+32
+  constexpr int PP = kTS + 1;  // px/py: rows/cols y0-1 .. y0+31
+  __shared__ T xs[(kTS + 2) * XP];
+  __shared__ T pxs[PP * PP];
+  __shared__ T pys[PP * PP];
+  const StJob<T>& J = p.jobs[st_find_job(p, blockIdx.z)];
+  const int z = J.lo + (blockIdx.z - J.work_begin);
+  const int x0 = blockIdx.x * kTS, y0 = blockIdx.y * kTS;
+  const T* xp = J.a + (long long)(z - J.a_z0) * p.plane;
+  st_load<T, kTS + 2, kTS + 2, XP>(xs, xp, y0, x0, -1, -1, p.ny, p.nx);
+  __syncthreads();
+  const T d2 = (T)p.delta2;
+  const long long orow = (long long)(z - J.lo) * p.plane;
+  for (int i = threadIdx.x; i < PP * PP; i += kStNT) {
+    const int r = i / PP, c = i - r * PP;
+    const int y = y0 - 1 + r, x = x0 - 1 + c;
+    T px = T(0), py = T(0);
+    if (y >= 0 && y < p.ny && x >= 0 && x < p.nx) {
+      const T xc = xs[r * XP + c];
+      const T dx = (x < p.nx - 1) ? sub_rn(xs[r * XP + c + 1], xc) : T(0);
+      const T dy = (y < p.ny - 1) ? sub_rn(xs[(r + 1) * XP + c], xc) : T(0);
+      const T w = omega_of(dx, dy, d2);
+      px = mul_rn(w, dx);
+      py = mul_rn(w, dy);
+      if (r >= 1 && c >= 1) J.out1[orow + (long long)y * p.nx + x] = w;
+    }
+    pxs[i] = px;
+    pys[i] = py;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
+  const T two_eta = (T)p.two_eta, lam = (T)p.lam, two_kappa = (T)p.two_kappa;
+  const T xmin = (T)p.x_min, xmax = (T)p.x_max;
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j) {
+    const int ly = ty + j * (kStNT / kTS);
+    const int y = y0 + ly, x = x0 + tx;
+    if (y >= p.ny || x >= p.nx) continue;
+    const int r = ly + 1, c = tx + 1;
+    const T xc = xs[r * XP + c];
+    const T clipped = xc < xmin ? xmin : (xc > xmax ? xmax : xc);
+    const T box = mul_rn(two_eta, sub_rn(xc, clipped));
+    const T px0 = pxs[r * PP + c], pxm = pxs[r * PP + c - 1];
+    const T py0 = pys[r * PP + c], pym = pys[(r - 1) * PP + c];
+    const T tvx = (p.nx == 1) ? T(0) : (x == 0) ? -px0 : (x == p.nx - 1) ? pxm : sub_rn(pxm, px0);
+    const T tvy = (p.ny == 1) ? T(0) : (y == 0) ? -py0 : (y == p.ny - 1) ? pym : sub_rn(pym, py0);
+    const long long q = (long long)y * p.nx + x;
+    const T dzm = (z - 1 >= 0 && z - 1 < p.nz - 1) ? sub_rn(xc, xp[q - p.plane]) : T(0);
+    const T dzp = (z < p.nz - 1) ? sub_rn(xp[q + p.plane], xc) : T(0);
+    J.out0[orow + q] = add_rn(add_rn(box, mul_rn(lam, add_rn(tvx, tvy))), mul_rn(two_kappa, sub_rn(dzm, dzp)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kStNT) reg_gram_kernel(const __grid_constant__ StArgs<T> p) {
+  constexpr int SP = kTS + 1;  // rows/cols y0 .. y0+32 (right / lower neighbours)
+  __shared__ T gs[SP * SP];
+  __shared__ T dss[SP * SP];
+  __shared__ double red[(kStNT / 32) * kRegNV];
+  const StJob<T>& J = p.jobs[st_find_job(p, blockIdx.z)];
+  const int z = J.lo + (blockIdx.z - J.work_begin);
+  const int x0 = blockIdx.x * kTS, y0 = blockIdx.y * kTS;
+  const bool has_d = J.b != nullptr;
+  const long long orow = (long long)(z - J.lo) * p.plane;
+  st_load<T, SP, SP, SP>(gs, J.a + orow, y0, x0, 0, 0, p.ny, p.nx);
+  if (has_d) st_load<T, SP, SP, SP>(dss, J.b + orow, y0, x0, 0, 0, p.ny, p.nx);
+  __syncthreads();
+  double v[kRegNV];
+#pragma unroll
+  for (int k = 0; k < kRegNV; ++k) v[k] = 0.0;
+  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j) {
+    const int ly = ty + j * (kStNT / kTS);
+    const int y = y0 + ly, x = x0 + tx;
+    if (y >= p.ny || x >= p.nx) continue;
+    const long long q = (long long)y * p.nx + x;
+    const T g = gs[ly * SP + tx];
+    const T d = has_d ? dss[ly * SP + tx] : T(0);
+    const double b0 = -(double)g, b1 = (double)d;
+    v[0] += b0 * b0;
+    v[1] += b0 * b1;
+    v[2] += b1 * b1;
+    const double w = (double)J.w[orow + q];
+    const double dx0 = (x < p.nx - 1) ? -(double)sub_rn(gs[ly * SP + tx + 1], g) : 0.0;
+    const double dy0 = (y < p.ny - 1) ? -(double)sub_rn(gs[(ly + 1) * SP + tx], g) : 0.0;
+    const double dx1 = (has_d && x < p.nx - 1) ? (double)sub_rn(dss[ly * SP + tx + 1], d) : 0.0;
+    const double dy1 = (has_d && y < p.ny - 1) ? (double)sub_rn(dss[(ly + 1) * SP + tx], d) : 0.0;
+    v[3] += w * (dx0 * dx0 + dy0 * dy0);
+    v[4] += w * (dx0 * dx1 + dy0 * dy1);
+    v[5] += w * (dx1 * dx1 + dy1 * dy1);
+    double z0v, z1v;  // axial row z (between z and z+1) of the block-embedded vectors
+    if (z < J.hi) {
+      z0v = -((double)J.a[orow + p.plane + q] - (double)g);
+      z1v = has_d ? (double)J.b[orow + p.plane + q] - (double)d : 0.0;
+    } else if (J.hi < p.nz - 1) {
+      z0v = -b0;
+      z1v = -b1;
+    } else {
+      z0v = 0.0;
+      z1v = 0.0;
+    }
+    v[6] += z0v * z0v;
+    v[7] += z0v * z1v;
+    v[8] += z1v * z1v;
+    if (z == J.lo && J.lo >= 1) {  // row lo-1: E b[lo] - 0
+      v[6] += b0 * b0;
+      v[7] += b0 * b1;
+      v[8] += b1 * b1;
+    }
+    v[9] += (double)g * (double)d;
+    v[10] += (g != T(0)) ? 1.0 : 0.0;
+    v[11] += isfinite((double)g) ? 0.0 : 1.0;
+  }
+  cta_reduce<kRegNV, kStNT>(v, red);
+  if (threadIdx.x == 0) {
+    const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int k = 0; k < kRegNV; ++k) p.partials[cta * kRegNV + k] = v[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kStNT) eval_kernel(const __grid_constant__ StArgs<T> p) {
+  constexpr int SP = kTS + 1;
+  __shared__ T xs[SP * SP];
+  __shared__ double red[(kStNT / 32) * kEvalNV];
+  const StJob<T>& J = p.jobs[st_find_job(p, blockIdx.z)];
+  const int z = J.lo + (blockIdx.z - J.work_begin);
+  const int x0 = blockIdx.x * kTS, y0 = blockIdx.y * kTS;
+  const T* xp = J.a + (long long)(z - J.a_z0) * p.plane;
+  st_load<T, SP, SP, SP>(xs, xp, y0, x0, 0, 0, p.ny, p.nx);
+  __syncthreads();
+  double v[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j) {
+    const int ly = ty + j * (kStNT / kTS);
+    const int y = y0 + ly, x = x0 + tx;
+    if (y >= p.ny || x >= p.nx) continue;
+    const long long q = (long long)y * p.nx + x;
+    const double xc = (double)xs[ly * SP + tx];
+    const double cl = xc < p.x_min ? p.x_min : (xc > p.x_max ? p.x_max : xc);
+    v[0] += (xc - cl) * (xc - cl);
+    const double dx = (x < p.nx - 1) ? (double)xs[ly * SP + tx + 1] - xc : 0.0;
+    const double dy = (y < p.ny - 1) ? (double)xs[(ly + 1) * SP + tx] - xc : 0.0;
+    v[1] += sqrt(dx * dx + dy * dy + p.delta2);
+    if (z < p.nz - 1) {
+      const double dz = (double)xp[q + p.plane] - xc;
+      v[2] += dz * dz;
+    }
+    if (J.b) {
+      const double s = (double)J.b[(long long)(z - J.lo) * p.plane + q];
+      v[3] += (xc - s) * (xc - s);
+      v[4] += s * s;
+    }
+  }
+  cta_reduce<kEvalNV, kStNT>(v, red);
+  if (threadIdx.x == 0) {
+    const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int k = 0; k < kEvalNV; ++k) p.partials[cta * kEvalNV + k] = v[k];
+  }
+}
+
+}  // namespace bd3mg
