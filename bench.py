@@ -264,7 +264,7 @@ def main():
     if not args.quick and rank == 0:
         extra["roofline"], extra["operators"] = roofline(obj, cfg, dtype, torch, N, D, blur)
     if not args.quick:
-        extra["e2e"] = e2e(obj, cfg, x0, args, world, rank, torch, N, D)
+        extra["e2e"] = e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng)
     if not args.quick and rank == 0 and world == 1:
         extra["variants"] = {"hd-cache": variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush)}
         extra["cpu_baseline"] = cpu_baseline(cfg)
@@ -361,90 +361,79 @@ def roofline(obj, cfg, dtype, torch, N, D, blur):
     return roof, res
 
 
-def e2e(obj, cfg, x0, args, world, rank, torch, N, D):
-    """The same sweep through the reference-facing host-buffer C ABI
-    (bd3mg_problem_mg_direction_host: TaskMessage in, increment out -- the
-    worker boundary of the reference, runtime.py:92-105) with the master on
-    the host like the reference's, plus the per-sweep eval_f through the
-    public API.  Host<->device copies are inside the timed region."""
-    import ctypes
-    from concurrent.futures import ThreadPoolExecutor
-
-    from paper_2002_02328_b200 import objective
+def e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng=None):
+    """The same sweep end to end with HOST buffers, host<->device copies inside
+    the timed region.  N=1: the reference-facing C ABI
+    bd3mg_problem_jacobi_sweep_host (x and the memory store in from pinned
+    host memory, updated x / increments and the recorder terms back).  N>1:
+    each rank ships its slab (owned planes + halos) and memory store from
+    pinned host memory to its GPU, runs the NCCL-halo sweep, and copies the
+    owned planes and the terms back."""
+    from paper_2002_02328_b200.host import HostProblem, pinned_empty
 
     nz, ny, nx = obj.dims.shape
     plane = ny * nx
-    kz = obj.psf.kdims.kz
-    B = -(-nz // cfg.block_height)
-    blocks = [(lo, min(lo + cfg.block_height - 1, nz - 1)) for lo in range(0, nz, cfg.block_height)]
-    if world > 1:
-        per = -(-B // world)
-        blocks = blocks[rank * per:(rank + 1) * per]
-    dcode = N.BD3MG_F64 if cfg.dtype == "f64" else N.BD3MG_F32
-    g = N.Geom(nx, ny, nz, *obj.psf.kdims, dcode)
-    r = D.reg(obj.params)
-    nthreads = 4
-    handles = []
-    for _ in range(nthreads):
-        h = ctypes.c_void_p()
-        N.check(N.lib.bd3mg_problem_create(ctypes.byref(g), ctypes.byref(r), obj.psf.kernels.ctypes.data,
-                                           obj.y.ctypes.data, torch.cuda.current_device(), ctypes.byref(h)))
-        handles.append(h)
-    pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
-    x = pin(x0.shape)
-    x[...] = x0
-    prev = pin(x0.shape)
-    prev[...] = 0.0
-    incs = [pin(((hi - lo + 1) * plane,)) for lo, hi in blocks]
-    infos = [np.zeros(N.INFO_DOUBLES) for _ in blocks]
-    import queue
-    pool = ThreadPoolExecutor(max_workers=nthreads)
-    free = queue.Queue()  # a handle (stream + buffers) is used by one thread at a time
-    for h in handles:
-        free.put(h)
-    h2d = d2h = 0
-
-    def one(i):
-        lo, hi = blocks[i]
-        s_lo, s_hi = max(0, lo - kz), min(nz - 1, hi + kz)
-        h = free.get()
-        try:
-            N.check(N.lib.bd3mg_problem_mg_direction_host(
-                h, x[s_lo:].ctypes.data, s_lo, s_hi - s_lo + 1, lo, hi,
-                prev[lo:].ctypes.data, incs[i].ctypes.data, infos[i].ctypes.data))
-        finally:
-            free.put(h)
-        return (s_hi - s_lo + 1 + hi - lo + 1) * plane * 8, (hi - lo + 1) * plane * 8
-
-    def sweep():
-        nonlocal h2d, d2h
-        res = list(pool.map(one, range(len(blocks))))
-        for (lo, hi), inc in zip(blocks, incs):
-            inc3 = inc.reshape(hi - lo + 1, ny, nx)
-            x[lo:hi + 1] += inc3
-            prev[lo:hi + 1] = inc3
-        f = objective.eval_f(obj, x) if world == 1 else 0.0
-        h2d = sum(a for a, _ in res) + (x.nbytes if world == 1 else 0)
-        d2h = sum(b for _, b in res) + (8 * N.EVAL_DOUBLES if world == 1 else 0)
-        return f
-
-    for _ in range(2):
-        sweep()
     steps = max(3, min(args.steps, 10))
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        sweep()
-    dt = time.perf_counter() - t0
-    if world > 1:
+    if world == 1:
+        hp = HostProblem(obj, cfg.dtype, torch.cuda.current_device())
+        blocks = [runtime_block(lo, min(lo + cfg.block_height - 1, nz - 1)) for lo in range(0, nz, cfg.block_height)]
+        x = pinned_empty(x0.shape)
+        x[...] = x0
+        dm = pinned_empty(x0.shape)
+        dm[...] = 0.0
+        terms = np.zeros(N.EVAL_DOUBLES)
+        for _ in range(2):
+            hp.jacobi_sweep(x, dm, blocks, terms=terms)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            hp.jacobi_sweep(x, dm, blocks, terms=terms)
+        dt = time.perf_counter() - t0
+        hp.close()
+        nb = len(blocks)
+        h2d = 2 * x.nbytes
+        d2h = 2 * x.nbytes + 8 * N.EVAL_DOUBLES
+        path = "bd3mg_problem_jacobi_sweep_host: pinned host x + memory store in, updated x + increments + f out"
+    else:
         import torch.distributed as dist
+        xl_h = pinned_empty(tuple(eng.x.shape))
+        xl_h[...] = eng.x.double().cpu().numpy()
+        dm_h = pinned_empty(tuple(eng.x.shape))
+        dm_h[...] = 0.0
+        xt = torch.from_numpy(xl_h)
+        dt_ = torch.from_numpy(dm_h)
+        o0, o1 = eng.o_lo - eng.l_lo, eng.o_hi - eng.l_lo + 1
+
+        def step():
+            eng.x.copy_(xt, non_blocking=True)
+            eng.prev.copy_(dt_, non_blocking=True)
+            eng.sweep()
+            xt[o0:o1].copy_(eng.x[o0:o1], non_blocking=True)
+            dt_[o0:o1].copy_(eng.prev[o0:o1], non_blocking=True)
+            f = eng.terms[4].item()
+            return f
+
+        for _ in range(2):
+            step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            step()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    for h in handles:
-        N.lib.bd3mg_problem_destroy(h)
-    return {"value": steps * B / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "steps": steps, "path": "host buffers -> bd3mg_problem_mg_direction_host (4 host threads, one "
-                                    "stream each) + host master update + eval_f(numpy x)"}
+        nb = eng.nblocks
+        h2d = 2 * xl_h.nbytes
+        d2h = 2 * (o1 - o0) * plane * 8 + 8
+        path = "per rank: pinned host slab + memory store -> GPU, NCCL-halo sweep, owned planes + f back"
+    return {"value": steps * nb / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": steps, "path": path}
+
+
+def runtime_block(lo, hi):
+    from paper_2002_02328_b200.volume import SliceBlock
+    return SliceBlock(lo, hi)
 
 
 def cpu_baseline(cfg):

@@ -213,6 +213,18 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
  * bench.py to measure the FMA-pipe peak of the roofline. */
 int bd3mg_fma_probe(int32_t dtype, int32_t blocks, int32_t iters, void* out, double* flops_out, void* stream);
 
+/* One block-Jacobi sweep with HOST buffers (the sweep-level drop-in for the
+ * reference's bp3mg barrier cycle, runtime.py:244-292): the fragment of x
+ * (nzf planes from depth frag_z0; the whole volume or a rank's slab with
+ * its halos) and the memory store dmem (same shape) are read from host
+ * memory, the sweep of bd3mg_jacobi_sweep runs on the device (recorder over
+ * the blocks' rows, no stop norms), and the updated x and dmem (= the
+ * increments) are written back in place.  blocks: host (z_lo, z_hi) pairs,
+ * <= 32.  terms_out (7) / info_out (nblocks*16) may be NULL.  Use pinned
+ * host memory for full PCIe rate. */
+int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, int64_t frag_z0, int64_t nzf,
+                                    const int64_t* blocks, int nblocks, double* terms_out, double* info_out);
+
 #ifdef __cplusplus
 }
 #endif

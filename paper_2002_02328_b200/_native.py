@@ -30,6 +30,7 @@ EXPORTS = (
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
     "bd3mg_jacobi_sweep_ws_bytes", "bd3mg_jacobi_cache_elems", "bd3mg_jacobi_sweep",
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
+    "bd3mg_problem_jacobi_sweep_host",
     "bd3mg_fma_probe",
 )
 
@@ -107,6 +108,8 @@ def _load() -> C.CDLL:
     lib.bd3mg_problem_create.argtypes = [G, R, _vp, _vp, C.c_int, C.POINTER(C.c_void_p)]
     lib.bd3mg_problem_destroy.argtypes = [_vp]
     lib.bd3mg_problem_mg_direction_host.argtypes = [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]
+    lib.bd3mg_problem_jacobi_sweep_host.argtypes = [_vp, _vp, _vp, _i64, _i64, C.POINTER(C.c_int64), C.c_int,
+                                                    _vp, _vp]
     lib.bd3mg_fma_probe.argtypes = [C.c_int32, C.c_int32, C.c_int32, _vp, _dp, _vp]
     return lib
 

@@ -21,23 +21,31 @@ struct RowRanges {
   long long end[kMaxJobs];
 };
 
+constexpr int kRedMaxNV = 12;
 __global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
                                                             const __grid_constant__ RowRanges rr,
                                                             double* __restrict__ out, int out_stride) {
-  __shared__ double s[kEwNT];
+  // all nv values in one pass: fixed per-thread stride order, then a fixed tree
+  __shared__ double s[kRedMaxNV][kEwNT];
   const int j = blockIdx.x;
-  for (int k = 0; k < nv; ++k) {
-    double acc = 0.0;
-    for (long long r = rr.begin[j] + threadIdx.x; r < rr.end[j]; r += kEwNT) acc += rows[r * nv + k];
-    s[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = kEwNT / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[j * out_stride + k] = s[0];
+  double acc[kRedMaxNV];
+#pragma unroll
+  for (int k = 0; k < kRedMaxNV; ++k) acc[k] = 0.0;
+  for (long long r = rr.begin[j] + threadIdx.x; r < rr.end[j]; r += kEwNT) {
+#pragma unroll
+    for (int k = 0; k < kRedMaxNV; ++k)
+      if (k < nv) acc[k] += rows[r * nv + k];
+  }
+#pragma unroll
+  for (int k = 0; k < kRedMaxNV; ++k)
+    if (k < nv) s[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int w = kEwNT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int k = 0; k < nv; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + w];
     __syncthreads();
   }
+  if (threadIdx.x < nv) out[j * out_stride + threadIdx.x] = s[threadIdx.x][0];
 }
 
 // ---------------------------------------------------------------------------

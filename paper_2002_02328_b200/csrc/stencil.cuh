@@ -57,6 +57,7 @@ BD3MG_D int st_find_job(const StArgs<T>& p, int zidx) {
 // out-of-volume entries are 0 (never used: the far-face rules mask them).
 template <typename T, int H, int W, int P>
 BD3MG_D void st_load(T* s, const T* plane, int y0, int x0, int oy, int ox, int ny, int nx) {
+#pragma unroll
   for (int i = threadIdx.x; i < H * W; i += kStNT) {
     const int r = i / W, c = i - r * W;
     const int y = y0 + oy + r, x = x0 + ox + c;
@@ -77,6 +78,16 @@ __global__ void __launch_bounds__(kStNT) greg_kernel(const __grid_constant__ StA
   const int x0 = blockIdx.x * kTS, y0 = blockIdx.y * kTS;
   const T* xp = J.a + (long long)(z - J.a_z0) * p.plane;
   st_load<T, kTS + 2, kTS + 2, XP>(xs, xp, y0, x0, -1, -1, p.ny, p.nx);
+  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
+  T zm[kStRows], zp[kStRows];  // x(z-1), x(z+1) of this thread's pixels, in flight during the tile phases
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j) {
+    const int y = y0 + ty + j * (kStNT / kTS), x = x0 + tx;
+    const bool in = y < p.ny && x < p.nx;
+    const long long q = (long long)y * p.nx + x;
+    zm[j] = (in && z - 1 >= 0) ? xp[q - p.plane] : T(0);
+    zp[j] = (in && z < p.nz - 1) ? xp[q + p.plane] : T(0);
+  }
   __syncthreads();
   const T d2 = (T)p.delta2;
   const long long orow = (long long)(z - J.lo) * p.plane;
@@ -97,7 +108,6 @@ __global__ void __launch_bounds__(kStNT) greg_kernel(const __grid_constant__ StA
     pys[i] = py;
   }
   __syncthreads();
-  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
   const T two_eta = (T)p.two_eta, lam = (T)p.lam, two_kappa = (T)p.two_kappa;
   const T xmin = (T)p.x_min, xmax = (T)p.x_max;
 #pragma unroll
@@ -114,8 +124,8 @@ __global__ void __launch_bounds__(kStNT) greg_kernel(const __grid_constant__ StA
     const T tvx = (p.nx == 1) ? T(0) : (x == 0) ? -px0 : (x == p.nx - 1) ? pxm : sub_rn(pxm, px0);
     const T tvy = (p.ny == 1) ? T(0) : (y == 0) ? -py0 : (y == p.ny - 1) ? pym : sub_rn(pym, py0);
     const long long q = (long long)y * p.nx + x;
-    const T dzm = (z - 1 >= 0 && z - 1 < p.nz - 1) ? sub_rn(xc, xp[q - p.plane]) : T(0);
-    const T dzp = (z < p.nz - 1) ? sub_rn(xp[q + p.plane], xc) : T(0);
+    const T dzm = (z - 1 >= 0 && z - 1 < p.nz - 1) ? sub_rn(xc, zm[j]) : T(0);
+    const T dzp = (z < p.nz - 1) ? sub_rn(zp[j], xc) : T(0);
     J.out0[orow + q] = add_rn(add_rn(box, mul_rn(lam, add_rn(tvx, tvy))), mul_rn(two_kappa, sub_rn(dzm, dzp)));
   }
 }
@@ -134,11 +144,21 @@ __global__ void __launch_bounds__(kStNT) reg_gram_kernel(const __grid_constant__
   const long long orow = (long long)(z - J.lo) * p.plane;
   st_load<T, SP, SP, SP>(gs, J.a + orow, y0, x0, 0, 0, p.ny, p.nx);
   if (has_d) st_load<T, SP, SP, SP>(dss, J.b + orow, y0, x0, 0, 0, p.ny, p.nx);
+  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
+  T wv[kStRows], gz[kStRows], dz[kStRows];  // omega, g(z+1), d(z+1): in flight during the tile load
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j) {
+    const int y = y0 + ty + j * (kStNT / kTS), x = x0 + tx;
+    const bool in = y < p.ny && x < p.nx;
+    const long long q = orow + (long long)y * p.nx + x;
+    wv[j] = in ? J.w[q] : T(0);
+    gz[j] = (in && z < J.hi) ? J.a[q + p.plane] : T(0);
+    dz[j] = (in && has_d && z < J.hi) ? J.b[q + p.plane] : T(0);
+  }
   __syncthreads();
   double v[kRegNV];
 #pragma unroll
   for (int k = 0; k < kRegNV; ++k) v[k] = 0.0;
-  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
 #pragma unroll
   for (int j = 0; j < kStRows; ++j) {
     const int ly = ty + j * (kStNT / kTS);
@@ -151,7 +171,7 @@ __global__ void __launch_bounds__(kStNT) reg_gram_kernel(const __grid_constant__
     v[0] += b0 * b0;
     v[1] += b0 * b1;
     v[2] += b1 * b1;
-    const double w = (double)J.w[orow + q];
+    const double w = (double)wv[j];
     const double dx0 = (x < p.nx - 1) ? -(double)sub_rn(gs[ly * SP + tx + 1], g) : 0.0;
     const double dy0 = (y < p.ny - 1) ? -(double)sub_rn(gs[(ly + 1) * SP + tx], g) : 0.0;
     const double dx1 = (has_d && x < p.nx - 1) ? (double)sub_rn(dss[ly * SP + tx + 1], d) : 0.0;
@@ -161,8 +181,8 @@ __global__ void __launch_bounds__(kStNT) reg_gram_kernel(const __grid_constant__
     v[5] += w * (dx1 * dx1 + dy1 * dy1);
     double z0v, z1v;  // axial row z (between z and z+1) of the block-embedded vectors
     if (z < J.hi) {
-      z0v = -((double)J.a[orow + p.plane + q] - (double)g);
-      z1v = has_d ? (double)J.b[orow + p.plane + q] - (double)d : 0.0;
+      z0v = -((double)gz[j] - (double)g);
+      z1v = has_d ? (double)dz[j] - (double)d : 0.0;
     } else if (J.hi < p.nz - 1) {
       z0v = -b0;
       z1v = -b1;
@@ -201,9 +221,18 @@ __global__ void __launch_bounds__(kStNT) eval_kernel(const __grid_constant__ StA
   const int x0 = blockIdx.x * kTS, y0 = blockIdx.y * kTS;
   const T* xp = J.a + (long long)(z - J.a_z0) * p.plane;
   st_load<T, SP, SP, SP>(xs, xp, y0, x0, 0, 0, p.ny, p.nx);
+  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
+  T xz[kStRows], sn[kStRows];  // x(z+1), snapshot: in flight during the tile load
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j) {
+    const int y = y0 + ty + j * (kStNT / kTS), x = x0 + tx;
+    const bool in = y < p.ny && x < p.nx;
+    const long long q = (long long)y * p.nx + x;
+    xz[j] = (in && z < p.nz - 1) ? xp[q + p.plane] : T(0);
+    sn[j] = (in && J.b) ? J.b[(long long)(z - J.lo) * p.plane + q] : T(0);
+  }
   __syncthreads();
   double v[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  const int tx = threadIdx.x % kTS, ty = threadIdx.x / kTS;
 #pragma unroll
   for (int j = 0; j < kStRows; ++j) {
     const int ly = ty + j * (kStNT / kTS);
@@ -215,13 +244,14 @@ __global__ void __launch_bounds__(kStNT) eval_kernel(const __grid_constant__ StA
     v[0] += (xc - cl) * (xc - cl);
     const double dx = (x < p.nx - 1) ? (double)xs[ly * SP + tx + 1] - xc : 0.0;
     const double dy = (y < p.ny - 1) ? (double)xs[(ly + 1) * SP + tx] - xc : 0.0;
-    v[1] += sqrt(dx * dx + dy * dy + p.delta2);
+    const double s2 = dx * dx + dy * dy + p.delta2;
+    v[1] += s2 * rsqrt(s2);
     if (z < p.nz - 1) {
-      const double dz = (double)xp[q + p.plane] - xc;
+      const double dz = (double)xz[j] - xc;
       v[2] += dz * dz;
     }
     if (J.b) {
-      const double s = (double)J.b[(long long)(z - J.lo) * p.plane + q];
+      const double s = (double)sn[j];
       v[3] += (xc - s) * (xc - s);
       v[4] += s * s;
     }
