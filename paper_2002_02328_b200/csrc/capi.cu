@@ -5,6 +5,7 @@
 // MajorantOperator.apply (objective.py), mg_direction (directions.py) and the
 // block update of receive_update (scheduler.py).
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -108,6 +109,17 @@ StArgs<T> st_args(const bd3mg_geom_t* g, const bd3mg_reg_t* r) {
 }
 inline long long st_tiles(const bd3mg_geom_t* g) { return ((g->nx + kTS - 1) / kTS) * ((g->ny + kTS - 1) / kTS); }
 
+// One CTA column per job (z-marching kernels): grid.z = njobs.
+template <typename T, typename Kern>
+cudaError_t st_launch_z(Kern kern, StArgs<T>& a, size_t smem, cudaStream_t s) {
+  if (a.njobs == 0) return cudaSuccess;
+  cudaError_t e = ensure_smem_attr(kern, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(a.tiles_x, a.tiles_y, a.njobs), kStNT, smem, s>>>(a);
+  launched();
+  return cudaGetLastError();
+}
+
 // Lay jobs out along grid.z (one plane per z index) and launch `kern`.
 template <typename T, typename Kern>
 cudaError_t st_launch(Kern kern, StArgs<T>& a, cudaStream_t s) {
@@ -191,7 +203,7 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     sa.njobs = 1;
     sa.jobs[0].a = frag; sa.jobs[0].a_z0 = frag_z0; sa.jobs[0].lo = (int)lo; sa.jobs[0].hi = (int)hi;
     sa.jobs[0].out0 = greg; sa.jobs[0].out1 = omega_out;
-    CU(st_launch<T>(greg_kernel<T>, sa, s));
+    CU(st_launch_z<T>(greg_z_kernel<T, false>, sa, greg_z_smem<T>(), s));
   }
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
@@ -308,6 +320,8 @@ struct StepOpts {
   double* resid_sq = nullptr;  // device: sum of residual^2 over rows [rec_lo, rec_hi] (shared anchor)
   int64_t rec_lo = 0, rec_hi = -1;
   T* const* hd = nullptr;      // per task: cached H E_S d_mem over rows [olo, ohi] (updated in place)
+  T* const* greg = nullptr;    // per task: precomputed regulariser gradient rows (skip the greg launch)
+  T* const* omega = nullptr;   // per task: precomputed omega rows
 };
 
 template <typename T>
@@ -350,10 +364,11 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     }
   }
   std::vector<T*> gb(nt), wb(nt), grb(nt);
+  const bool pre = opt.greg != nullptr;
   for (int t = 0; t < nt; ++t) {
     gb[t] = ws.take<T>(h[t] * plane);
-    wb[t] = ws.take<T>(h[t] * plane);
-    grb[t] = ws.take<T>(h[t] * plane);
+    wb[t] = pre ? opt.omega[t] : ws.take<T>(h[t] * plane);
+    grb[t] = pre ? opt.greg[t] : ws.take<T>(h[t] * plane);
   }
   long long gram_work = 0;
   for (int t = 0; t < nt; ++t) gram_work += ohi[t] - olo[t] + 1;
@@ -369,10 +384,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   long long hsum = 0;
   for (int t = 0; t < nt; ++t) hsum += h[t];
-  const long long reg_rows = hsum * st_tiles(g);
+  const long long reg_rows = (long long)nt * st_tiles(g);  // one partial row per (block, tile)
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
-  double* data3 = ws.take<double>((size_t)nt * 3);
-  double* reg12 = ws.take<double>((size_t)nt * kRegNV);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
 
@@ -407,7 +420,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
   }
   // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
-  {
+  if (!pre) {
     StArgs<T> sa = st_args<T>(g, r);
     sa.njobs = nt;
     for (int t = 0; t < nt; ++t) {
@@ -415,7 +428,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
       J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi; J.out0 = grb[t]; J.out1 = wb[t];
     }
-    CU(st_launch<T>(greg_kernel<T>, sa, s));
+    CU(st_launch_z<T>(greg_z_kernel<T, false>, sa, greg_z_smem<T>(), s));
   }
   {
     ConvArgs<T> a = base_args<T>(g, r, K);
@@ -441,7 +454,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       J.a = gb[t]; J.a_z0 = tasks[t].z_lo; J.b = (const T*)tasks[t].d_mem; J.w = wb[t];
       J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi;
     }
-    CU(st_launch<T>(reg_gram_kernel<T>, sa, s));
+    CU(st_launch_z<T>(reg_gram_z_kernel<T>, sa, reg_gram_z_smem<T>(), s));
   }
   // (4) data Gram <H b_i, H b_j> (forward only, both columns share the taps)
   std::vector<std::pair<long long, long long>> granges(nt);
@@ -464,24 +477,21 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     CU(conv_launch<T>(gmode, false, a, (int)gram_work, s));
   launched();
   }
-  // (5) reductions
-  CU(reduce(cparts, gmode == M_GRAM1 ? 1 : 3, granges, data3, 3, s));
-  {
-    std::vector<std::pair<long long, long long>> rr(nt);
-    long long b0 = 0;
-    const long long tl = st_tiles(g);
-    for (int t = 0; t < nt; ++t) { rr[t] = {b0, b0 + h[t] * tl}; b0 += h[t] * tl; }
-    CU(reduce(rparts, kRegNV, rr, reg12, kRegNV, s));
-  }
-  // (6) 2x2 solves
+  // (5)+(6) per-block reductions and the 2x2 solves, one CTA per block
   {
     SolveArgs sa;
     memset(&sa, 0, sizeof(sa));
     sa.nblocks = nt;
     sa.two_eta = 2.0 * r->eta; sa.lam = r->lam; sa.two_kappa = 2.0 * r->kappa;
     sa.prune_tol = kPruneTol; sa.pinv_tol = kPinvTol;
-    for (int t = 0; t < nt; ++t) sa.has_d[t] = tasks[t].d_mem != nullptr;
-    solve2x2_kernel<<<1, 32, 0, s>>>(sa, data3, reg12, info_out); launched();
+    sa.nv_gram = gmode == M_GRAM1 ? 1 : 3;
+    const long long tl = st_tiles(g);
+    for (int t = 0; t < nt; ++t) {
+      sa.has_d[t] = tasks[t].d_mem != nullptr;
+      sa.g_begin[t] = granges[t].first; sa.g_end[t] = granges[t].second;
+      sa.r_begin[t] = t * tl; sa.r_end[t] = (t + 1) * tl;
+    }
+    reduce_solve_kernel<<<nt, kEwNT, 0, s>>>(sa, cparts, rparts, info_out); launched();
     CU(cudaGetLastError());
   }
   // (7) increments / in-place update
@@ -538,7 +548,11 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   return BD3MG_OK;
 }
 
-// One block-Jacobi sweep (see bd3mg_jacobi_sweep in the header).
+// One block-Jacobi sweep (see bd3mg_jacobi_sweep in the header).  When the
+// blocks tile the recorder rows exactly (single GPU, or a rank's owned rows)
+// the recorder pass is fused into the regulariser-gradient stencil (same x
+// tiles); otherwise a separate eval stencil runs first.  Scratch layout:
+// [eval partials][sums][greg, omega per block][step scratch].
 template <typename T>
 int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_sweep_t* sw,
                       double* terms, double* info, Ws& ws, cudaStream_t s) {
@@ -547,12 +561,13 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   const int64_t plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
   T* x = (T*)sw->x;
   T* dm = (T*)sw->dmem;
-  std::vector<bd3mg_task_t> tasks(sw->nblocks);
-  std::vector<T*> hd(sw->nblocks);
-  int64_t hd_off = 0;
-  for (int b = 0; b < sw->nblocks; ++b) {
+  const int nb = sw->nblocks;
+  std::vector<bd3mg_task_t> tasks(nb);
+  std::vector<T*> hd(nb), grb(nb), wb(nb);
+  int64_t hd_off = 0, hsum = 0, bmin = INT64_MAX, bmax = -1;
+  for (int b = 0; b < nb; ++b) {
     const int64_t lo = sw->blocks[2 * b], hi = sw->blocks[2 * b + 1];
-    if (lo < sw->frag_z0 || hi >= sw->frag_z0 + sw->nzf) return fail(BD3MG_EINVAL, "block outside the fragment");
+    if (lo < sw->frag_z0 || hi >= sw->frag_z0 + sw->nzf || hi < lo) return fail(BD3MG_EINVAL, "block outside the fragment");
     bd3mg_task_t& t = tasks[b];
     t.frag = x; t.frag_z0 = sw->frag_z0; t.nzf = sw->nzf; t.z_lo = lo; t.z_hi = hi;
     t.d_mem = dm ? dm + (lo - sw->frag_z0) * plane : nullptr;
@@ -562,47 +577,69 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     const int64_t olo = std::max<int64_t>(0, lo - rz), ohi = std::min<int64_t>(g->nz - 1, hi + rz);
     hd[b] = sw->hd_cache ? (T*)sw->hd_cache + hd_off : nullptr;
     hd_off += (ohi - olo + 1) * plane;
+    hsum += hi - lo + 1;
+    bmin = std::min(bmin, lo);
+    bmax = std::max(bmax, hi);
   }
   const bool rec = sw->rec_hi >= sw->rec_lo;
   const int64_t nrec = rec ? sw->rec_hi - sw->rec_lo + 1 : 0;
-  double* eparts = ws.take<double>((size_t)std::max<long long>(1, nrec * st_tiles(g)) * kEvalNV);
+  bool contiguous = true;  // blocks in order, back to back
+  for (int b = 1; b < nb; ++b) contiguous &= sw->blocks[2 * b] == sw->blocks[2 * b - 1] + 1;
+  const bool fused = rec && contiguous && bmin == sw->rec_lo && bmax == sw->rec_hi && hsum == nrec;
+  if (rec && (sw->rec_lo < sw->frag_z0 || sw->rec_hi >= sw->frag_z0 + sw->nzf))
+    return fail(BD3MG_EINVAL, "recorder rows outside the fragment");
+  const long long erows = std::max<long long>(1, nrec * st_tiles(g));
+  double* eparts = ws.take<double>((size_t)erows * kEvalNV);
   double* sums = ws.take<double>(8);
+  if (fused)
+    for (int b = 0; b < nb; ++b) {
+      const int64_t hb = sw->blocks[2 * b + 1] - sw->blocks[2 * b] + 1;
+      grb[b] = ws.take<T>(hb * plane);
+      wb[b] = ws.take<T>(hb * plane);
+    }
   StepOpts<T> opt;
   opt.resid_sq = sums;
   opt.rec_lo = sw->rec_lo;
   opt.rec_hi = sw->rec_hi;
   opt.hd = sw->hd_cache ? hd.data() : nullptr;
-  Ws sub = ws;  // the step's scratch follows the recorder's
-  int rc = mg_steps_chunk<T>(g, r, K, y, tasks.data(), sw->nblocks, info, sub, s, opt);
+  if (fused) { opt.greg = grb.data(); opt.omega = wb.data(); }
+  if (!ws.measure) {
+    if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+    // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll
+    if (!rec) {
+      CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s));
+    } else {
+      StArgs<T> e = st_args<T>(g, r);
+      e.partials = eparts;
+      if (fused) {
+        e.njobs = nb;
+        for (int b = 0; b < nb; ++b) {
+          StJob<T>& J = e.jobs[b];
+          J.a = x; J.a_z0 = sw->frag_z0; J.lo = (int)sw->blocks[2 * b]; J.hi = (int)sw->blocks[2 * b + 1];
+          J.b = sw->snap ? (const T*)sw->snap + (J.lo - sw->rec_lo) * plane : nullptr;
+          J.out0 = grb[b]; J.out1 = wb[b];
+        }
+        CU(st_launch_z<T>(greg_z_kernel<T, true>, e, greg_z_smem<T>(), s));
+      } else {
+        e.njobs = 1;
+        e.jobs[0].a = x; e.jobs[0].a_z0 = sw->frag_z0; e.jobs[0].b = (const T*)sw->snap;
+        e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
+        CU(st_launch<T>(eval_kernel<T>, e, s));
+      }
+      CU(reduce(eparts, kEvalNV, {{0, (fused ? nb : nrec) * st_tiles(g)}}, sums + 1, kEvalNV, s));
+      if (sw->snap)
+        CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
+                           cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  // (2) the fused block steps at the anchor (x, dmem updated in place)
+  Ws sub = ws;
+  int rc = mg_steps_chunk<T>(g, r, K, y, tasks.data(), nb, info, sub, s, opt);
   ws.off = sub.off;
   if (rc != BD3MG_OK || ws.measure) return rc;
   if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
-  return BD3MG_OK;
-}
-
-// The recorder's elementwise terms + snapshot roll, launched BEFORE the step
-// (the step updates x in place).
-template <typename T>
-int jacobi_record_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const bd3mg_sweep_t* sw, double* eparts,
-                       double* sums, cudaStream_t s) {
-  const int64_t plane = g->ny * g->nx;
-  if (sw->rec_hi < sw->rec_lo) {
-    CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s));
-    return BD3MG_OK;
-  }
-  const int64_t nrec = sw->rec_hi - sw->rec_lo + 1;
-  if (sw->rec_lo < sw->frag_z0 || sw->rec_hi >= sw->frag_z0 + sw->nzf)
-    return fail(BD3MG_EINVAL, "recorder rows outside the fragment");
-  StArgs<T> e = st_args<T>(g, r);
-  e.njobs = 1;
-  e.jobs[0].a = (const T*)sw->x; e.jobs[0].a_z0 = sw->frag_z0; e.jobs[0].b = (const T*)sw->snap;
-  e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
-  e.partials = eparts;
-  CU(st_launch<T>(eval_kernel<T>, e, s));
-  CU(reduce(eparts, kEvalNV, {{0, nrec * st_tiles(g)}}, sums + 1, kEvalNV, s));
-  if (sw->snap)
-    CU(cudaMemcpyAsync(sw->snap, (const T*)sw->x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
-                       cudaMemcpyDeviceToDevice, s));
+  eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms); launched();
+  CU(cudaGetLastError());
   return BD3MG_OK;
 }
 
@@ -896,23 +933,11 @@ int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* 
   if (!r || !sw || !info_out || !terms_out) return fail(BD3MG_EINVAL, "null argument");
   Ws ws = make_ws(wsp, ws_bytes);
   cudaStream_t s = (cudaStream_t)stream;
-  // scratch layout mirrors jacobi_sweep_impl: [eparts][sums][step scratch]
-  const int64_t nrec = sw->rec_hi >= sw->rec_lo ? sw->rec_hi - sw->rec_lo + 1 : 0;
-  Ws probe = ws;
-  double* eparts = probe.take<double>((size_t)std::max<long long>(1, nrec * st_tiles(g)) * kEvalNV);
-  double* sums = probe.take<double>(8);
-  rc = DISPATCH_T(g, jacobi_record_impl<double>(g, r, sw, eparts, sums, s),
-                  jacobi_record_impl<float>(g, r, sw, eparts, sums, s));
-  if (rc) return rc;
-  rc = DISPATCH_T(g,
-                  jacobi_sweep_impl<double>(g, r, (const double*)kernels, (const double*)y, sw, terms_out, info_out,
-                                            ws, s),
-                  jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
-                                           s));
-  if (rc) return rc;
-  eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms_out); launched();
-  CU(cudaGetLastError());
-  return BD3MG_OK;
+  return DISPATCH_T(g,
+                    jacobi_sweep_impl<double>(g, r, (const double*)kernels, (const double*)y, sw, terms_out, info_out,
+                                              ws, s),
+                    jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
+                                             s));
 }
 
 size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks) {

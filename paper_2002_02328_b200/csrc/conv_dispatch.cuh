@@ -5,6 +5,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "depthvar.cuh"
 
@@ -28,18 +30,25 @@ ConvGrid conv_grid(int ky, int kx, int mode, int ny, int nx) {
   return {(nx + TX - 1) / TX, (ny + TY - 1) / TY};
 }
 
-// per-device "max dynamic smem" attribute, raised at most once per kernel
-// instantiation and device (never inside a stream capture after warm-up)
-template <typename Kern>
-inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes, size_t* granted) {
+// Raise a kernel's dynamic-smem limit once per (kernel, device); keyed by the
+// kernel's address (kernels sharing a signature must not share the entry).
+inline cudaError_t ensure_smem_attr_ptr(const void* kern, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 64 && granted[dev] >= bytes) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& g = granted[{kern, dev}];
+  if (g >= bytes) return cudaSuccess;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e == cudaSuccess && dev < 64) granted[dev] = 227 * 1024;
+  if (e == cudaSuccess) g = 227 * 1024;
   return e;
+}
+template <typename Kern>
+inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes) {
+  return ensure_smem_attr_ptr(reinterpret_cast<const void*>(kern), bytes);
 }
 
 // TMA descriptor of a fragment (nx, ny, nz) with a (boxw, boxh, 1) box;
@@ -62,8 +71,7 @@ cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   }
   const size_t sm = Cfg::smem_bytes(p.kz);
   auto kern = conv_tiled_kernel<T, K, K, MODE, ADJ>;
-  static size_t granted[64] = {0};  // one table per instantiation
-  cudaError_t e = ensure_smem_attr(kern, sm, granted);
+  cudaError_t e = ensure_smem_attr(kern, sm);
   if (e != cudaSuccess) return e;
   dim3 grid(p.tiles_x, p.tiles_y, total_work);
   kern<<<grid, Cfg::NT, sm, s>>>(p);
@@ -75,8 +83,7 @@ cudaError_t launch_generic(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   size_t coef = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
   const size_t sm = coef + 8 * (kGenericNT / 32) * sizeof(double);
   auto kern = conv_generic_kernel<T, MODE, ADJ>;
-  static size_t granted[64] = {0};  // one table per instantiation
-  cudaError_t e = ensure_smem_attr(kern, sm, granted);
+  cudaError_t e = ensure_smem_attr(kern, sm);
   if (e != cudaSuccess) return e;
   dim3 grid(p.tiles_x, p.tiles_y, total_work);
   kern<<<grid, kGenericNT, sm, s>>>(p);

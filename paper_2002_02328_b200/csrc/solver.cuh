@@ -22,16 +22,14 @@ struct RowRanges {
 };
 
 constexpr int kRedMaxNV = 12;
-__global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
-                                                            const __grid_constant__ RowRanges rr,
-                                                            double* __restrict__ out, int out_stride) {
-  // all nv values in one pass: fixed per-thread stride order, then a fixed tree
-  __shared__ double s[kRedMaxNV][kEwNT];
-  const int j = blockIdx.x;
+// Deterministic CTA sum of rows[begin:end, 0:nv] (fixed stride classes, then
+// a fixed tree).  Result in res[0:nv] for every thread (after the barrier).
+__device__ __forceinline__ void cta_sum_rows(const double* __restrict__ rows, int nv, long long begin,
+                                             long long end, double (*s)[kEwNT], double* res) {
   double acc[kRedMaxNV];
 #pragma unroll
   for (int k = 0; k < kRedMaxNV; ++k) acc[k] = 0.0;
-  for (long long r = rr.begin[j] + threadIdx.x; r < rr.end[j]; r += kEwNT) {
+  for (long long r = begin + threadIdx.x; r < end; r += kEwNT) {
 #pragma unroll
     for (int k = 0; k < kRedMaxNV; ++k)
       if (k < nv) acc[k] += rows[r * nv + k];
@@ -45,7 +43,19 @@ __global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __rest
       for (int k = 0; k < nv; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x < nv) out[j * out_stride + threadIdx.x] = s[threadIdx.x][0];
+  for (int k = 0; k < nv; ++k) res[k] = s[k][0];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
+                                                            const __grid_constant__ RowRanges rr,
+                                                            double* __restrict__ out, int out_stride) {
+  __shared__ double s[kRedMaxNV][kEwNT];
+  double res[kRedMaxNV];
+  const int j = blockIdx.x;
+  cta_sum_rows(rows, nv, rr.begin[j], rr.end[j], s, res);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nv; ++k) out[j * out_stride + k] = res[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -80,19 +90,17 @@ struct SolveArgs {
   double two_eta, lam, two_kappa;
   double prune_tol, pinv_tol;
   int has_d[kMaxJobs];
+  // fused reduce + solve: partial-row ranges of each block
+  int nv_gram;                       // 1 (GRAM1) or 3 values per conv partial row
+  long long g_begin[kMaxJobs], g_end[kMaxJobs];
+  long long r_begin[kMaxJobs], r_end[kMaxJobs];
 };
 
 // info layout per block (kInfoNV doubles):
 // 0-2 gram (00,01,11 of the kept columns; 1 column -> [0]), 3-4 rhs,
 // 5-6 coeffs, 7 ncols, 8 status (0 ok, 1 non-finite g), 9 |g|, 10 c_g
 // (coefficient of -g), 11 c_d (coefficient of d), 12 column mask (1:-g, 2:d)
-__global__ void solve2x2_kernel(const __grid_constant__ SolveArgs p, const double* __restrict__ data3,
-                                const double* __restrict__ reg12, double* __restrict__ info) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= p.nblocks) return;
-  const double* D = data3 + j * 3;
-  const double* R = reg12 + j * kRegNV;
-  double* o = info + j * kInfoNV;
+__device__ void solve_one(const SolveArgs& p, int j, const double* D, const double* R, double* o) {
   for (int k = 0; k < kInfoNV; ++k) o[k] = 0.0;
   const double gg = R[0], dd = R[2], gd = R[9];
   const double gn = sqrt(gg);
@@ -127,6 +135,21 @@ __global__ void solve2x2_kernel(const __grid_constant__ SolveArgs p, const doubl
   }
   o[10] = cg;
   o[11] = cd;
+}
+
+// One CTA per block: reduce its conv and regulariser partial rows (same
+// deterministic order as reduce_rows_kernel), then the 2x2 solve.
+__global__ void __launch_bounds__(kEwNT) reduce_solve_kernel(const __grid_constant__ SolveArgs p,
+                                                             const double* __restrict__ gram_rows,
+                                                             const double* __restrict__ reg_rows,
+                                                             double* __restrict__ info) {
+  __shared__ double s[kRedMaxNV][kEwNT];
+  const int j = blockIdx.x;
+  double D[kRedMaxNV], R[kRedMaxNV];
+  cta_sum_rows(gram_rows, p.nv_gram, p.g_begin[j], p.g_end[j], s, D);
+  if (p.nv_gram < 3) { D[1] = 0.0; D[2] = 0.0; }
+  cta_sum_rows(reg_rows, kRegNV, p.r_begin[j], p.r_end[j], s, R);
+  if (threadIdx.x == 0) solve_one(p, j, D, R, info + j * kInfoNV);
 }
 
 // ---------------------------------------------------------------------------
