@@ -134,10 +134,15 @@ cudaError_t st_launch(Kern kern, StArgs<T>& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// partial rows (one per CTA) of a conv launch over one job of `nout` planes
 template <typename T>
-long long conv_rows(const bd3mg_geom_t* g, int mode, long long work) {
+long long conv_tiles(const bd3mg_geom_t* g, int mode) {
   const ConvGrid cg = conv_grid<T>(g->ky, g->kx, mode, (int)g->ny, (int)g->nx);
-  return work * cg.tiles_x * cg.tiles_y;
+  return (long long)cg.tiles_x * cg.tiles_y;
+}
+template <typename T>
+long long conv_rows(const bd3mg_geom_t* g, int mode, long long nout) {
+  return conv_zunits<T>(g->ky, g->kx, mode, nout) * conv_tiles<T>(g, mode);
 }
 
 cudaError_t reduce(const double* rows, int nv, const std::vector<std::pair<long long, long long>>& ranges,
@@ -380,7 +385,27 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   if (opt.resid_sq && !shared) return fail(BD3MG_EINVAL, "recorder residual needs a shared anchor");
   if (opt.resid_sq && opt.rec_hi >= opt.rec_lo && (opt.rec_lo < u_lo || opt.rec_hi > u_hi))
     return fail(BD3MG_EINVAL, "recorder rows outside the residual rows");
-  const long long conv_part_rows = std::max(conv_rows<T>(g, M_RESID, resid_work), conv_rows<T>(g, gmode, gram_work));
+  // recorder rows split the shared residual job so its partial rows align
+  std::vector<std::pair<int64_t, int64_t>> rjobs;  // (out_lo, nout) of the residual jobs
+  int rec_job = -1;
+  if (shared) {
+    if (opt.resid_sq && opt.rec_hi >= opt.rec_lo) {
+      if (opt.rec_lo > u_lo) rjobs.push_back({u_lo, opt.rec_lo - u_lo});
+      rec_job = (int)rjobs.size();
+      rjobs.push_back({opt.rec_lo, opt.rec_hi - opt.rec_lo + 1});
+      if (opt.rec_hi < u_hi) rjobs.push_back({opt.rec_hi + 1, u_hi - opt.rec_hi});
+    } else {
+      rjobs.push_back({u_lo, u_hi - u_lo + 1});
+    }
+  } else {
+    for (int t = 0; t < nt; ++t) rjobs.push_back({olo[t], r_n[t]});
+  }
+  long long resid_rows = 0, gram_rows = 0;
+  for (auto& rj : rjobs) resid_rows += conv_rows<T>(g, M_RESID, rj.second);
+  for (int t = 0; t < nt; ++t) gram_rows += conv_rows<T>(g, gmode, ohi[t] - olo[t] + 1);
+  (void)resid_work;
+  (void)gram_work;
+  const long long conv_part_rows = std::max(resid_rows, gram_rows);
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   long long hsum = 0;
   for (int t = 0; t < nt; ++t) hsum += h[t];
@@ -393,31 +418,26 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   {
     ConvArgs<T> a = base_args<T>(g, r, K);
     a.partials = cparts;
-    if (shared) {
-      a.njobs = 1;
-      ConvJob<T>& j = a.jobs[0];
-      j.src0 = (const T*)tasks[0].frag; j.src_z0 = tasks[0].frag_z0; j.src_nz = (int)tasks[0].nzf;
-      j.dst0 = rb[0]; j.sub = y + u_lo * plane; j.out_lo = (int)u_lo; j.nout = (int)(u_hi - u_lo + 1);
-    } else {
-      a.njobs = nt;
-      int wbeg = 0;
-      for (int t = 0; t < nt; ++t) {
-        ConvJob<T>& j = a.jobs[t];
-        j.src0 = (const T*)tasks[t].frag; j.src_z0 = tasks[t].frag_z0; j.src_nz = (int)tasks[t].nzf;
-        j.dst0 = rb[t]; j.sub = y + olo[t] * plane; j.out_lo = (int)olo[t]; j.nout = (int)r_n[t];
-        j.work_begin = wbeg;
-        wbeg += (int)r_n[t];
+    a.njobs = (int)rjobs.size();
+    for (int t = 0; t < a.njobs; ++t) {
+      const bd3mg_task_t& k = tasks[shared ? 0 : t];
+      ConvJob<T>& j = a.jobs[t];
+      j.src0 = (const T*)k.frag; j.src_z0 = k.frag_z0; j.src_nz = (int)k.nzf;
+      j.out_lo = (int)rjobs[t].first; j.nout = (int)rjobs[t].second;
+      j.dst0 = (shared ? rb[0] : rb[t]) + (rjobs[t].first - (shared ? u_lo : olo[t])) * plane;
+      j.sub = y + rjobs[t].first * plane;
+    }
+    CU(conv_launch<T>(M_RESID, false, a, 0, s));
+    launched();
+    if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
+      if (rec_job >= 0) {
+        const long long tl = conv_tiles<T>(g, M_RESID);
+        const long long b0 = (long long)a.jobs[rec_job].work_begin * tl;
+        CU(reduce(cparts, 1, {{b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)}}, opt.resid_sq, 1, s));
+      } else {
+        CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
       }
     }
-    CU(conv_launch<T>(M_RESID, false, a, (int)resid_work, s));
-  launched();
-  }
-  if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
-    const long long tiles = conv_rows<T>(g, M_RESID, 1);
-    if (opt.rec_hi >= opt.rec_lo)
-      CU(reduce(cparts, 1, {{(opt.rec_lo - u_lo) * tiles, (opt.rec_hi - u_lo + 1) * tiles}}, opt.resid_sq, 1, s));
-    else
-      CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
   }
   // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
   if (!pre) {
@@ -433,15 +453,13 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   {
     ConvArgs<T> a = base_args<T>(g, r, K);
     a.njobs = nt;
-    int wbeg = 0;
     for (int t = 0; t < nt; ++t) {
       ConvJob<T>& j = a.jobs[t];
       j.src0 = rb[t]; j.src_z0 = r_z0[t]; j.src_nz = (int)r_n[t];
       j.dst0 = gb[t]; j.sub = grb[t];
-      j.out_lo = (int)tasks[t].z_lo; j.nout = (int)h[t]; j.work_begin = wbeg;
-      wbeg += (int)h[t];
+      j.out_lo = (int)tasks[t].z_lo; j.nout = (int)h[t];
     }
-    CU(conv_launch<T>(M_GRAD, true, a, (int)hsum, s));
+    CU(conv_launch<T>(M_GRAD, true, a, 0, s));
     launched();
   }
   // (3) regulariser Gram terms + rhs + flags (tiled stencil)
@@ -462,20 +480,21 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     ConvArgs<T> a = base_args<T>(g, r, K);
     a.njobs = nt;
     a.partials = cparts;
-    int wbeg = 0;
-    const long long tiles = conv_rows<T>(g, gmode, 1);
     for (int t = 0; t < nt; ++t) {
       ConvJob<T>& j = a.jobs[t];
       j.src0 = gb[t];
       j.src1 = tasks[t].d_mem ? (const T*)tasks[t].d_mem : gb[t];
       if (cached) { j.sub = opt.hd[t]; j.dst0 = hgb[t]; }
       j.src_z0 = tasks[t].z_lo; j.src_nz = (int)h[t];
-      j.out_lo = (int)olo[t]; j.nout = (int)(ohi[t] - olo[t] + 1); j.work_begin = wbeg;
-      granges[t] = {(long long)wbeg * tiles, (long long)(wbeg + j.nout) * tiles};
-      wbeg += j.nout;
+      j.out_lo = (int)olo[t]; j.nout = (int)(ohi[t] - olo[t] + 1);
     }
-    CU(conv_launch<T>(gmode, false, a, (int)gram_work, s));
-  launched();
+    CU(conv_launch<T>(gmode, false, a, 0, s));
+    launched();
+    const long long tiles = conv_tiles<T>(g, gmode);  // partial rows per grid.z unit
+    for (int t = 0; t < nt; ++t) {
+      const long long b0 = (long long)a.jobs[t].work_begin * tiles;
+      granges[t] = {b0, b0 + conv_rows<T>(g, gmode, a.jobs[t].nout)};
+    }
   }
   // (5)+(6) per-block reductions and the 2x2 solves, one CTA per block
   {

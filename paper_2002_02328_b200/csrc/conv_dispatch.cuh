@@ -20,11 +20,34 @@ inline bool conv_tiled_shape(int ky, int kx) {
   return ky == kx && (ky == 3 || ky == 5 || ky == 7 || ky == 9);
 }
 
+// Two output planes per CTA (conv_rz2_kernel) for single-input modes on
+// tiled shapes: used where measured faster -- fp32 (FFMA has the register
+// headroom); in fp64 the second coefficient set does not fit the uniform
+// registers and the one-plane kernel wins.  BD3MG_RZ2=0/1 overrides.
+template <typename T>
+inline bool conv_rz2(int ky, int kx, int mode) {
+  static const int env = [] {
+    const char* e = getenv("BD3MG_RZ2");
+    return e ? atoi(e) : -1;
+  }();
+  const bool want = env < 0 ? (sizeof(T) == 4) : env != 0;
+  return want && conv_tiled_shape(ky, kx) && mode != M_GRAM2;
+}
+
+// grid.z units of a job with `nout` output planes
+template <typename T>
+inline long long conv_zunits(int ky, int kx, int mode, long long nout) {
+  return conv_rz2<T>(ky, kx, mode) ? (nout + 1) / 2 : nout;
+}
+
 template <typename T>
 ConvGrid conv_grid(int ky, int kx, int mode, int ny, int nx) {
   if (!conv_tiled_shape(ky, kx))
     return {(nx + kGenericTX - 1) / kGenericTX, (ny + kGenericTY - 1) / kGenericTY};
-  // all tiled configurations share TX; TY depends on dual vs single input
+  if (conv_rz2<T>(ky, kx, mode)) {
+    constexpr int TX = Rz2Cfg<T, 3, 3, M_STORE>::TX, TY = Rz2Cfg<T, 3, 3, M_STORE>::TY;
+    return {(nx + TX - 1) / TX, (ny + TY - 1) / TY};
+  }
   constexpr int TX = ConvCfg<T, 3, 3, M_STORE>::TX;
   const int TY = (mode == M_GRAM2) ? ConvCfg<T, 3, 3, M_GRAM2>::TY : ConvCfg<T, 3, 3, M_STORE>::TY;
   return {(nx + TX - 1) / TX, (ny + TY - 1) / TY};
@@ -78,6 +101,23 @@ cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <typename T, int K, int MODE, bool ADJ>
+cudaError_t launch_rz2(ConvArgs<T>& p, int total_work, cudaStream_t s) {
+  using Cfg = Rz2Cfg<T, K, K, MODE>;
+  for (int j = 0; j < p.njobs; ++j) {
+    ConvJob<T>& jb = p.jobs[j];
+    jb.use_tma = encode_tmap(&jb.tmap0, jb.src0, sizeof(T) == 8, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH) &&
+                 getenv("BD3MG_NO_TMA") == nullptr;
+  }
+  const size_t sm = Cfg::smem_bytes(p.kz);
+  auto kern = conv_rz2_kernel<T, K, K, MODE, ADJ>;
+  cudaError_t e = ensure_smem_attr(kern, sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.tiles_x, p.tiles_y, total_work);
+  kern<<<grid, Cfg::NT, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <typename T, int MODE, bool ADJ>
 cudaError_t launch_generic(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   size_t coef = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
@@ -93,12 +133,30 @@ cudaError_t launch_generic(ConvArgs<T>& p, int total_work, cudaStream_t s) {
 template <typename T, int MODE, bool ADJ>
 cudaError_t launch_mode(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   if (p.ky == p.kx) {
-    switch (p.ky) {
-      case 3: return launch_tiled<T, 3, MODE, ADJ>(p, total_work, s);
-      case 5: return launch_tiled<T, 5, MODE, ADJ>(p, total_work, s);
-      case 7: return launch_tiled<T, 7, MODE, ADJ>(p, total_work, s);
-      case 9: return launch_tiled<T, 9, MODE, ADJ>(p, total_work, s);
-      default: break;
+    if constexpr (MODE == M_GRAM2) {
+      switch (p.ky) {
+        case 3: return launch_tiled<T, 3, MODE, ADJ>(p, total_work, s);
+        case 5: return launch_tiled<T, 5, MODE, ADJ>(p, total_work, s);
+        case 7: return launch_tiled<T, 7, MODE, ADJ>(p, total_work, s);
+        case 9: return launch_tiled<T, 9, MODE, ADJ>(p, total_work, s);
+        default: break;
+      }
+    } else if (conv_rz2<T>(p.ky, p.kx, MODE)) {
+      switch (p.ky) {
+        case 3: return launch_rz2<T, 3, MODE, ADJ>(p, total_work, s);
+        case 5: return launch_rz2<T, 5, MODE, ADJ>(p, total_work, s);
+        case 7: return launch_rz2<T, 7, MODE, ADJ>(p, total_work, s);
+        case 9: return launch_rz2<T, 9, MODE, ADJ>(p, total_work, s);
+        default: break;
+      }
+    } else {
+      switch (p.ky) {
+        case 3: return launch_tiled<T, 3, MODE, ADJ>(p, total_work, s);
+        case 5: return launch_tiled<T, 5, MODE, ADJ>(p, total_work, s);
+        case 7: return launch_tiled<T, 7, MODE, ADJ>(p, total_work, s);
+        case 9: return launch_tiled<T, 9, MODE, ADJ>(p, total_work, s);
+        default: break;
+      }
     }
   }
   return launch_generic<T, MODE, ADJ>(p, total_work, s);

@@ -8,6 +8,15 @@ namespace bd3mg {
 
 template <typename T>
 cudaError_t conv_launch(int mode, bool adj, ConvArgs<T>& p, int total_work, cudaStream_t s) {
+  // grid.z units: planes, or plane pairs for the two-plane kernel; the
+  // callers' work_begin / total_work are recomputed here
+  (void)total_work;
+  long long wb = 0;
+  for (int j = 0; j < p.njobs; ++j) {
+    p.jobs[j].work_begin = (int)wb;
+    wb += conv_zunits<T>(p.ky, p.kx, mode, p.jobs[j].nout);
+  }
+  total_work = (int)wb;
   if (total_work <= 0) return cudaSuccess;
   const ConvGrid g = conv_grid<T>(p.ky, p.kx, mode, p.ny, p.nx);
   p.tiles_x = g.tiles_x;

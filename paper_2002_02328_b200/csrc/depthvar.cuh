@@ -372,6 +372,238 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Two output planes per CTA (single-input modes).  Each staged input plane
+// zi feeds output zo0 with tap a0 = zi-zo0+rz and output zo0+1 with tap
+// a0-1, so every TMA tile / barrier serves two outputs and each thread keeps
+// 2 x RY x RX independent accumulators.  Per output the taps are still
+// visited in ascending a (then b, c): results are bitwise those of the
+// one-plane kernel.  The two coefficient slices of the current plane are
+// double-buffered in smem next to the tiles (zero where a tap is invalid).
+template <typename T, int KY_, int KX_, int MODE>
+struct Rz2Cfg {
+  static constexpr int KY = KY_, KX = KX_;
+  static constexpr int VEC = 16 / sizeof(T);
+  static constexpr int RX = VEC, RY = 8, RZ = 2;
+  static constexpr int WX = 32, WY = 4, NT = WX * WY;
+  static constexpr int TX = WX * RX, TY = WY * RY;
+  static constexpr int RXH = (KX - 1) / 2, RYH = (KY - 1) / 2;
+  static constexpr int RXA = (RXH + VEC - 1) / VEC * VEC, OFF = RXA - RXH;
+  static constexpr int TXH = TX + KX - 1 + OFF, TYH = TY + KY - 1;
+  static constexpr int PITCH = (TXH + 2 * VEC - 1) / (2 * VEC) * (2 * VEC);
+  static constexpr int ROWQ = 128 / cgcd(PITCH * (int)sizeof(T), 128);
+  static constexpr int BOXH = (TYH + ROWQ - 1) / ROWQ * ROWQ;
+  static constexpr int WIN = RX + KX - 1;
+  static constexpr int WINP = (OFF + WIN + VEC - 1) / VEC * VEC;
+  static constexpr int BOX = BOXH * PITCH;
+  static constexpr int TILE = (BOX + 128 / (int)sizeof(T) - 1) / (128 / (int)sizeof(T)) * (128 / (int)sizeof(T));
+  static constexpr size_t TILE_BYTES = (size_t)TILE * sizeof(T), BOX_BYTES = (size_t)BOX * sizeof(T);
+  static constexpr int NIN = 1;
+  static constexpr int NV = ModeNV<MODE>::value;
+  static constexpr int KS = KY * KX;                       // one tap slice
+  static constexpr size_t SLICE_BYTES = ((size_t)2 * 2 * KS * sizeof(T) + 127) & ~size_t(127);
+  static size_t smem_bytes(int) {
+    return 2 * TILE_BYTES + SLICE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
+  }
+};
+
+template <typename T>
+BD3MG_D bool tap_ok(const ConvArgs<T>& p, bool adj, int zo, int a) {
+  if (a < 0 || a >= p.kz) return false;
+  if (!adj) return true;
+  const int zsrc = zo + a - (p.kz - 1) / 2;
+  return zsrc >= 0 && zsrc < p.nzk;
+}
+
+// coefficient (b, c) of tap a for output plane zo (adjoint: gathered, flipped)
+template <typename T, bool ADJ>
+BD3MG_D T coef_of(const ConvArgs<T>& p, int zo, int a, int b, int c) {
+  const int KYX = p.ky * p.kx, K3 = p.kz * KYX;
+  if (!ADJ) return p.K[(long long)zo * K3 + a * KYX + b * p.kx + c];
+  const int zsrc = zo + a - (p.kz - 1) / 2;
+  return p.K[(long long)zsrc * K3 + (p.kz - 1 - a) * KYX + (p.ky - 1 - b) * p.kx + (p.kx - 1 - c)];
+}
+
+template <typename Cfg, typename T, bool D0, bool D1>
+BD3MG_D void rz2_plane(const T* tb, const T* cs0, const T* cs1, T (&acc)[2][Cfg::RY][Cfg::RX]) {
+  using V = typename Vec16<T>::type;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, VEC = Cfg::VEC, KX = Cfg::KX, KY = Cfg::KY;
+#pragma unroll
+  for (int yi = 0; yi < RY + KY - 1; ++yi) {
+    T v[Cfg::WINP];
+#pragma unroll
+    for (int j = 0; j < Cfg::WINP; j += VEC) {
+      const V q = *reinterpret_cast<const V*>(tb + yi * Cfg::PITCH + j);
+      if constexpr (VEC == 2) {
+        v[j] = q.x; v[j + 1] = q.y;
+      } else {
+        v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < KX; ++c) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const int b = yi - r;
+        if (b < 0 || b >= KY) continue;
+        if constexpr (D0) {
+          const T k = cs0[b * KX + c];
+#pragma unroll
+          for (int i = 0; i < RX; ++i) acc[0][r][i] = fma_rn(k, v[Cfg::OFF + i + c], acc[0][r][i]);
+        }
+        if constexpr (D1) {
+          const T k = cs1[b * KX + c];
+#pragma unroll
+          for (int i = 0; i < RX; ++i) acc[1][r][i] = fma_rn(k, v[Cfg::OFF + i + c], acc[1][r][i]);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int KY, int KX, int MODE, bool ADJ>
+__global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
+    conv_rz2_kernel(const __grid_constant__ ConvArgs<T> p) {
+  using Cfg = Rz2Cfg<T, KY, KX, MODE>;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, KS = Cfg::KS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  T* tiles = reinterpret_cast<T*>(sbase);
+  T* slices = reinterpret_cast<T*>(sbase + 2 * Cfg::TILE_BYTES);  // [buf][out][KS]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * Cfg::TILE_BYTES + Cfg::SLICE_BYTES);
+  double* red_s = reinterpret_cast<double*>(mbar + 2);
+
+  const int zidx = blockIdx.z;
+  const int jid = find_job(p, zidx);
+  const ConvJob<T>& job = p.jobs[jid];
+  const int zo0 = job.out_lo + 2 * (zidx - job.work_begin);
+  const bool has1 = zo0 + 1 < job.out_lo + job.nout;
+  const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
+  const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
+  const int rz = (p.kz - 1) / 2;
+  const bool tma = job.use_tma != 0;
+  // input planes feeding either output, inside the fragment
+  const int zi_lo = (int)max((long long)(zo0 - rz), job.src_z0);
+  const int zi_hi = (int)min((long long)(zo0 + (has1 ? 1 : 0) + rz), job.src_z0 + job.src_nz - 1);
+
+  auto stage_slices = [&](int zi, int b) {  // coefficient slices of input plane zi
+    T* dst = slices + b * 2 * KS;
+    for (int t = threadIdx.x; t < 2 * KS; t += Cfg::NT) {
+      const int o = t / KS, e = t - o * KS;
+      const int zo = zo0 + o, a = zi - zo + rz;
+      T v = T(0);
+      if ((o == 0 || has1) && tap_ok(p, ADJ, zo, a)) v = coef_of<T, ADJ>(p, zo, a, e / KX, e % KX);
+      dst[t] = v;
+    }
+  };
+  auto issue = [&](int zi, int b) {
+    T* dst = tiles + b * Cfg::TILE;
+    if (tma) {
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&mbar[b], (uint32_t)Cfg::BOX_BYTES);
+        tma_load_3d(dst, &job.tmap0, x0 - Cfg::RXA, y0 - Cfg::RYH, (int)(zi - job.src_z0), &mbar[b]);
+      }
+    } else {
+      stage_tile_fallback<Cfg>(dst, job.src0, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
+      cp_async_commit();
+    }
+  };
+
+  if (tma && threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  if (zi_lo <= zi_hi) stage_slices(zi_lo, 0);
+  __syncthreads();
+
+  T acc[2][RY][RX];
+#pragma unroll
+  for (int o = 0; o < 2; ++o)
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int i = 0; i < RX; ++i) acc[o][r][i] = T(0);
+
+  if (zi_lo <= zi_hi) issue(zi_lo, 0);
+  uint32_t phase = 0;
+  int buf = 0;
+  for (int zi = zi_lo; zi <= zi_hi; ++zi) {
+    if (zi < zi_hi) {
+      issue(zi + 1, buf ^ 1);
+      stage_slices(zi + 1, buf ^ 1);  // visible after this iteration's closing barrier
+    }
+    if (tma) {
+      mbar_wait(&mbar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    } else {
+      if (zi < zi_hi) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncthreads();
+    }
+    const bool d0 = tap_ok(p, ADJ, zo0, zi - zo0 + rz);
+    const bool d1 = has1 && tap_ok(p, ADJ, zo0 + 1, zi - zo0 - 1 + rz);
+    const T* tb = tiles + buf * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
+    const T* cs0 = slices + buf * 2 * KS;
+    const T* cs1 = cs0 + KS;
+    if (d0 && d1) rz2_plane<Cfg, T, true, true>(tb, cs0, cs1, acc);
+    else if (d0) rz2_plane<Cfg, T, true, false>(tb, cs0, cs1, acc);
+    else if (d1) rz2_plane<Cfg, T, false, true>(tb, cs0, cs1, acc);
+    __syncthreads();
+    buf ^= 1;
+  }
+
+  // ---- epilogue (both output planes) --------------------------------------
+  constexpr int NV = Cfg::NV;
+  double part[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    if (o == 1 && !has1) break;
+    const long long orow = (long long)(zo0 + o - job.out_lo) * p.plane;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const int y = y0 + ty * RY + r;
+      if (y >= p.ny) continue;
+#pragma unroll
+      for (int i = 0; i < RX; ++i) {
+        const int x = x0 + tx * RX + i;
+        if (x >= p.nx) continue;
+        const long long q = orow + (long long)y * p.nx + x;
+        const T a0 = acc[o][r][i];
+        if constexpr (MODE == M_STORE) {
+          job.dst0[q] = a0;
+        } else if constexpr (MODE == M_RESID) {
+          const T res = sub_rn(a0, job.sub[q]);
+          if (job.dst0) job.dst0[q] = res;
+          part[0] += (double)res * (double)res;
+        } else if constexpr (MODE == M_GRAD) {
+          job.dst0[q] = add_rn(a0, job.sub[q]);
+        } else if constexpr (MODE == M_GRAM1) {
+          if (job.dst0) job.dst0[q] = a0;
+          part[0] += (double)a0 * (double)a0;
+        } else if constexpr (MODE == M_GRAMC) {
+          const double c0 = (double)job.sub[q];
+          job.dst0[q] = a0;
+          part[0] += (double)a0 * (double)a0;
+          part[1] += (double)a0 * c0;
+          part[2] += c0 * c0;
+        }
+      }
+    }
+  }
+  if constexpr (NV > 0) {
+    cta_reduce<NV, Cfg::NT>(part, red_s);
+    if (threadIdx.x == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Generic path for kernel widths without a tuned instantiation: one output
 // voxel per thread, runtime ky/kx, same a->b->c order and same epilogues.
