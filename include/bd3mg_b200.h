@@ -221,7 +221,9 @@ int bd3mg_fma_probe(int32_t dtype, int32_t blocks, int32_t iters, void* out, dou
  * the blocks' rows, no stop norms), and the updated x and dmem (= the
  * increments) are written back in place.  blocks: host (z_lo, z_hi) pairs,
  * <= 32.  terms_out (7) / info_out (nblocks*16) may be NULL.  Use pinned
- * host memory for full PCIe rate. */
+ * host memory for full PCIe rate.  dmem == NULL selects session mode: the
+ * memory store lives on the device inside the handle (zeroed on the first
+ * call for a fragment), so only x crosses PCIe. */
 int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, int64_t frag_z0, int64_t nzf,
                                     const int64_t* blocks, int nblocks, double* terms_out, double* info_out);
 

@@ -1017,6 +1017,8 @@ struct bd3mg_problem {
   int device;
   cudaStream_t s;
   DevBuf K, y, stage, slab, dmem, inc, info, ws, terms;
+  DevBuf dmem_res;          // device-resident memory store (sweep with dmem == NULL)
+  int64_t dmem_res_z0 = -1, dmem_res_n = 0;
 };
 
 static int download_f64(bd3mg_problem* p, const DevBuf& src, size_t n, double* host) {
@@ -1128,24 +1130,35 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
 
 int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, int64_t frag_z0, int64_t nzf,
                                     const int64_t* blocks, int nblocks, double* terms_out, double* info_out) {
-  if (!p || !x || !dmem || !blocks || nblocks < 1) return fail(BD3MG_EINVAL, "null argument");
+  if (!p || !x || !blocks || nblocks < 1) return fail(BD3MG_EINVAL, "null argument");
   CU(cudaSetDevice(p->device));
   const bd3mg_geom_t* g = &p->g;
   if (frag_z0 < 0 || nzf < 1 || frag_z0 + nzf > g->nz) return fail(BD3MG_EINVAL, "invalid fragment");
   const size_t n = (size_t)nzf * g->ny * g->nx;
+  const size_t esz = g->dtype == BD3MG_F64 ? 8 : 4;
   int64_t rec_lo = blocks[0], rec_hi = blocks[1];
   for (int b = 1; b < nblocks; ++b) {
     rec_lo = std::min(rec_lo, blocks[2 * b]);
     rec_hi = std::max(rec_hi, blocks[2 * b + 1]);
   }
   int rc = upload_f64(p, x, n, p->slab);
-  if (!rc) rc = upload_f64(p, dmem, n, p->dmem);
+  if (!rc && dmem) rc = upload_f64(p, dmem, n, p->dmem);
   if (rc) return rc;
+  DevBuf* dm = &p->dmem;
+  if (!dmem) {  // session mode: memory store stays on the device between calls
+    if (p->dmem_res_z0 != frag_z0 || p->dmem_res_n != nzf) {
+      CU(p->dmem_res.reserve(n * esz));
+      CU(cudaMemsetAsync(p->dmem_res.p, 0, n * esz, p->s));
+      p->dmem_res_z0 = frag_z0;
+      p->dmem_res_n = nzf;
+    }
+    dm = &p->dmem_res;
+  }
   CU(p->info.reserve((size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double)));
   CU(p->terms.reserve(BD3MG_EVAL_DOUBLES * sizeof(double)));
   bd3mg_sweep_t sw;
   memset(&sw, 0, sizeof(sw));
-  sw.x = p->slab.p; sw.dmem = p->dmem.p; sw.frag_z0 = frag_z0; sw.nzf = nzf;
+  sw.x = p->slab.p; sw.dmem = dm->p; sw.frag_z0 = frag_z0; sw.nzf = nzf;
   sw.blocks = blocks; sw.nblocks = nblocks; sw.rec_lo = rec_lo; sw.rec_hi = rec_hi; sw.snap = nullptr;
   const size_t wsb = bd3mg_jacobi_sweep_ws_bytes(g, &sw);
   if (wsb == (size_t)-1) return BD3MG_EINVAL;
@@ -1153,7 +1166,7 @@ int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, i
   rc = bd3mg_jacobi_sweep(g, &p->r, p->K.p, p->y.p, &sw, (double*)p->terms.p, (double*)p->info.p, p->ws.p, wsb, p->s);
   if (rc) return rc;
   rc = download_f64(p, p->slab, n, x);
-  if (!rc) rc = download_f64(p, p->dmem, n, dmem);
+  if (!rc && dmem) rc = download_f64(p, p->dmem, n, dmem);
   if (rc) return rc;
   std::vector<double> info((size_t)nblocks * BD3MG_INFO_DOUBLES);
   CU(cudaMemcpyAsync(info.data(), p->info.p, info.size() * sizeof(double), cudaMemcpyDeviceToHost, p->s));

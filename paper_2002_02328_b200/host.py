@@ -74,17 +74,19 @@ class HostProblem:
                                                       inc.ctypes.data, None if info is None else info.ctypes.data))
         return inc
 
-    def jacobi_sweep(self, x: np.ndarray, dmem: np.ndarray, blocks, frag_z0: int = 0,
+    def jacobi_sweep(self, x: np.ndarray, dmem: np.ndarray | None, blocks, frag_z0: int = 0,
                      terms: np.ndarray | None = None, info: np.ndarray | None = None) -> np.ndarray:
         """In place on C-contiguous float64 x / dmem; returns the anchor's
-        recorder terms [data, box, tv, axial, f, 0, 0]."""
+        recorder terms [data, box, tv, axial, f, 0, 0].  dmem=None keeps the
+        memory store on the device between calls (session mode)."""
         for a in (x, dmem):
-            if a.dtype != np.float64 or not a.flags.c_contiguous:
+            if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous):
                 raise ValueError("x and dmem must be C-contiguous float64")
         barr = (C.c_int64 * (2 * len(blocks)))(*[v for b in blocks for v in (b.z_lo, b.z_hi)])
         if terms is None:
             terms = np.zeros(N.EVAL_DOUBLES)
-        N.check(N.lib.bd3mg_problem_jacobi_sweep_host(self.h, x.ctypes.data, dmem.ctypes.data, frag_z0, x.shape[0],
+        N.check(N.lib.bd3mg_problem_jacobi_sweep_host(self.h, x.ctypes.data, None if dmem is None else dmem.ctypes.data,
+                                                      frag_z0, x.shape[0],
                                                       barr, len(blocks), terms.ctypes.data,
                                                       None if info is None else info.ctypes.data))
         return terms

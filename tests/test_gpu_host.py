@@ -66,3 +66,18 @@ def test_host_sweep_fp32(c1obj):
     ref = eng.x.cpu().numpy()
     assert np.linalg.norm(x - ref) <= 1e-5 * np.linalg.norm(ref)
     hp.close()
+
+
+def test_host_sweep_session_mode(c1obj):
+    """dmem=None keeps the memory store on the device: same iterates."""
+    from paper_2002_02328_b200 import runtime
+    from paper_2002_02328_b200.host import HostProblem
+    obj, x0, cfg = c1obj
+    eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, torch.float64)
+    hp = HostProblem(obj)
+    x = x0.copy()
+    for _ in range(4):
+        eng.sweep()
+        hp.jacobi_sweep(x, None, eng.blocks)
+    assert np.array_equal(x, eng.x.cpu().numpy())
+    hp.close()
