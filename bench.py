@@ -34,6 +34,15 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "BD3MG block-iterations/sec (C2 256x256x64 fp64, PSF 5x5x11, 8 blocks x 8 planes, block-Jacobi sweeps)"
+
+
+def metric_of(cfg) -> str:
+    if cfg.name == "C2":
+        return METRIC
+    B = -(-cfg.dims.nz // cfg.block_height)
+    return (f"BD3MG block-iterations/sec ({cfg.name} {cfg.dims.nx}x{cfg.dims.ny}x{cfg.dims.nz} {cfg.dtype}, PSF "
+            f"{cfg.kdims[0]}x{cfg.kdims[1]}x{cfg.kdims[2]}, {B} blocks x {cfg.block_height} planes, "
+            "block-Jacobi sweeps)")
 UNIT = "block-it/s"
 
 
@@ -167,7 +176,7 @@ def reference_arm(args, cfg_name):
               f"bp3mg barrier, {threads} worker threads; core: "
               + ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if kind == "reference"
                  else "oracle/bd3mg_oracle.c (bitwise the reference core)"))
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config_dict(cfg, world),
@@ -293,7 +302,7 @@ def main():
         extra["cpu_baseline"] = cpu_baseline(cfg)
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if (world > 1 and args.strong) else "weak", "vs_baseline": None,
                 "dtype": cfg.dtype, "data": "synthetic (seeded ellipsoid phantom, BASELINE PSF family)",

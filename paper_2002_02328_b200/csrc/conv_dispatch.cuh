@@ -45,7 +45,8 @@ ConvGrid conv_grid(int ky, int kx, int mode, int ny, int nx) {
   if (!conv_tiled_shape(ky, kx))
     return {(nx + kGenericTX - 1) / kGenericTX, (ny + kGenericTY - 1) / kGenericTY};
   if (conv_rz2<T>(ky, kx, mode)) {
-    constexpr int TX = Rz2Cfg<T, 3, 3, M_STORE>::TX, TY = Rz2Cfg<T, 3, 3, M_STORE>::TY;
+    constexpr int TX = Rz2Cfg<T, 3, 3, M_STORE>::TX;
+    const int TY = ky <= 5 ? Rz2Cfg<T, 3, 3, M_STORE>::TY : Rz2Cfg<T, 7, 7, M_STORE>::TY;
     return {(nx + TX - 1) / TX, (ny + TY - 1) / TY};
   }
   constexpr int TX = ConvCfg<T, 3, 3, M_STORE>::TX;

@@ -385,7 +385,9 @@ template <typename T, int KY_, int KX_, int MODE>
 struct Rz2Cfg {
   static constexpr int KY = KY_, KX = KX_;
   static constexpr int VEC = 16 / sizeof(T);
-  static constexpr int RX = VEC, RY = 8, RZ = 2;
+  // rows per thread: measured on B200 (scripts/prof_h_cfg.py) -- 8 for the
+  // 5x5 taps, 4 for 7x7 / 9x9 (fewer live coefficients and a smaller body)
+  static constexpr int RX = VEC, RY = (KY <= 5) ? 8 : 4, RZ = 2;
   static constexpr int WX = 32, WY = 4, NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
   static constexpr int RXH = (KX - 1) / 2, RYH = (KY - 1) / 2;
@@ -542,14 +544,12 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
       else cp_async_wait<0>();
       __syncthreads();
     }
-    const bool d0 = tap_ok(p, ADJ, zo0, zi - zo0 + rz);
-    const bool d1 = has1 && tap_ok(p, ADJ, zo0 + 1, zi - zo0 - 1 + rz);
+    // one code body for both outputs (invalid taps have zero coefficients:
+    // exact no-ops for finite inputs); three specialised bodies overflow
+    // the instruction cache for the 7x7 / 9x9 instantiations (measured)
     const T* tb = tiles + buf * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
     const T* cs0 = slices + buf * 2 * KS;
-    const T* cs1 = cs0 + KS;
-    if (d0 && d1) rz2_plane<Cfg, T, true, true>(tb, cs0, cs1, acc);
-    else if (d0) rz2_plane<Cfg, T, true, false>(tb, cs0, cs1, acc);
-    else if (d1) rz2_plane<Cfg, T, false, true>(tb, cs0, cs1, acc);
+    rz2_plane<Cfg, T, true, true>(tb, cs0, cs0 + KS, acc);
     __syncthreads();
     buf ^= 1;
   }

@@ -150,15 +150,18 @@ def ellipsoid_phantom(dims: Dims3, n: int, seed: int, amplitude: str = "uniform"
     else:
         raise ValueError(f"unknown amplitude law {amplitude!r}")
     vol = np.zeros(dims.shape)
-    yy = np.arange(ny, dtype=np.float64)[:, None]
-    xx = np.arange(nx, dtype=np.float64)[None, :]
     for (cz, cy, cx), (az, ay, ax), amp in zip(centres, axes, amps):
         z0 = max(0, int(math.floor(cz - az)))
         z1 = min(nz - 1, int(math.ceil(cz + az)))
+        # bounding box in y, x (mask evaluated only there)
+        y0, y1 = max(0, int(math.floor(cy - ay))), min(ny - 1, int(math.ceil(cy + ay)))
+        x0, x1 = max(0, int(math.floor(cx - ax))), min(nx - 1, int(math.ceil(cx + ax)))
+        yy = np.arange(y0, y1 + 1, dtype=np.float64)[:, None]
+        xx = np.arange(x0, x1 + 1, dtype=np.float64)[None, :]
+        q = ((yy - cy) / ay) ** 2 + ((xx - cx) / ax) ** 2
         for z in range(z0, z1 + 1):
             tz = ((z - cz) / az) ** 2
             if tz > 1.0:
                 continue
-            mask = ((yy - cy) / ay) ** 2 + ((xx - cx) / ax) ** 2 <= 1.0 - tz
-            vol[z][mask] += amp
+            vol[z, y0:y1 + 1, x0:x1 + 1][q <= 1.0 - tz] += amp
     return vol
