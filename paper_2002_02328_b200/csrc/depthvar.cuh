@@ -119,13 +119,15 @@ BD3MG_D T omega_of(T dx, T dy, T delta2) {
 // chunks of one dense smem row, so every window load is conflict-free.
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
+
 template <typename T, int KY_, int KX_, int MODE>
 struct ConvCfg {
   static constexpr bool DUAL = (MODE == M_GRAM2);
   static constexpr int KY = KY_, KX = KX_;
   static constexpr int VEC = 16 / sizeof(T);        // elements per 16-byte load
   static constexpr int RX = VEC;                    // outputs per thread in x
-  static constexpr int RY = DUAL ? 8 : 16;          // outputs per thread in y
+  // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32)
+  static constexpr int RY = DUAL ? (sizeof(T) == 8 ? 8 : 4) : 16;
   static constexpr int WX = 32, WY = 4;             // a warp spans one row group
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
