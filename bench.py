@@ -69,15 +69,20 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while the GPU
+    is under load; a reader thread keeps the samples live so the caller can
+    keep the GPU busy (untimed sweeps) until the timed region is bracketed."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.rows: list[list[str]] = []
+        self.thread = None
 
     def start(self):
         try:
@@ -86,25 +91,35 @@ class Clocks:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def count(self) -> int:
+        return len(self.rows) if self.proc is not None else 10**9
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
+        for parts in self.rows:
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for name, v in zip(names, parts[3:7]):
+            for name, v in zip(self.NAMES, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
@@ -266,10 +281,16 @@ def main():
     clocks = Clocks(local)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks.start()
+    t_end = time.time() + 5.0
+    while clocks.count() < 2 and time.time() < t_end:  # load the GPU until sampling runs (untimed)
+        for _ in range(20):
+            eng.sweep()
+        torch.cuda.synchronize()
+    n_before = clocks.count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     for i in range(args.steps):
         flush.zero_()
         starts[i].record()
@@ -278,7 +299,13 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    t_end = time.time() + 5.0
+    while clocks.count() < n_before + 3 and time.time() < t_end:  # keep loading until samples bracket it
+        for _ in range(20):
+            eng.sweep()
+        torch.cuda.synchronize()
     clk = clocks.stop()
+    clk["window"] = "samples from 2 before to 3 after the timed region, GPU kept under the same sweep load"
     eng.check()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     t_max = ms
@@ -385,11 +412,18 @@ def roofline(obj, cfg, dtype, torch, N, D, blur):
     torch.cuda.synchronize()
     peak = fl.value * 5 / (s.elapsed_time(e) / 1e3) / 1e12
     achieved = res["H"]["tflops"]
+    traffic = None
+    try:
+        traffic = json.load(open(ROOT / "profiles" / "ncu_traffic.json"))[cfg.name]["traffic_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     roof = {"bound": "fp64_fma" if dtype == torch.float64 else "fp32_fma", "kernel": "conv_tiled_kernel (H, full volume)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": "measured: bd3mg_fma_probe (dense FMA chains) on this GPU, this run "
                            "(MEASURED_PEAKS.json has no FP64/FP32 entry)",
-            "algorithmic_flops_per_launch": flops, "traffic": None}
+            "algorithmic_flops_per_launch": flops,
+            "algorithmic_bytes_per_launch": 2 * obj.dims.count * x.element_size(),
+            "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram read+write)"}
     return roof, res
 
 
