@@ -260,3 +260,212 @@ class OracleShardedJacobi:
             return torch.cat(parts).numpy()
         dist.send(own, 0, group=self.group)
         return None
+
+
+# ---------------------------------------------------------------------------
+# Asynchronous mode: stale peer halos with a bounded delay.
+#
+# Each rank walks its own blocks cyclically without global barriers.  After
+# every block update it ships the planes each neighbour keeps as halo (the
+# fixed per-pair range of SlabLayout.transfers) with version = its update
+# count.  Before updating a block whose slab reaches a
+# neighbour's planes, it takes the newest halo that has arrived and waits
+# only if that version lags its own update count by more than `max_delay`
+# (the stale-synchronous rule; BASELINE C4: max delay <= 2 block updates).
+# The staleness used at every update is logged like the reference's
+# TraceEvent ledger (scheduler.py:60-67, :156-160).
+
+class TorchP2P:
+    """Halo transport over torch.distributed (NCCL on GPUs, gloo on CPUs)."""
+
+    def __init__(self, buf: torch.Tensor, z0: int, plan, group=None):
+        self.buf, self.z0, self.group = buf, z0, group
+        self.recvs = {}   # peer -> (lo, hi, staging, header, [reqs])
+        self.sends = {}   # peer -> (lo, hi)
+        for peer, lo, hi, kind in plan:
+            if kind == "recv":
+                self.recvs.setdefault(peer, []).append((lo, hi))
+            else:
+                self.sends.setdefault(peer, []).append((lo, hi))
+        self.pending = {}
+        self.inflight = []
+        for peer in self.recvs:
+            self._post(peer)
+
+    def _planes(self, ranges):
+        return torch.cat([self.buf[lo - self.z0:hi - self.z0 + 1] for lo, hi in ranges])
+
+    def _post(self, peer):
+        shape = self._planes(self.recvs[peer]).shape
+        stage = torch.empty(shape, dtype=self.buf.dtype, device=self.buf.device)
+        hdr = torch.zeros(1, dtype=torch.int64, device=self.buf.device)
+        reqs = [dist.irecv(hdr, peer, group=self.group), dist.irecv(stage, peer, group=self.group)]
+        self.pending[peer] = (stage, hdr, reqs)
+
+    def neighbours_sent_to(self):
+        return list(self.sends)
+
+    def send(self, peer, version: int):
+        data = self._planes(self.sends[peer]).contiguous()
+        hdr = torch.tensor([version], dtype=torch.int64, device=self.buf.device)
+        self.inflight.append((data, hdr, [dist.isend(hdr, peer, group=self.group),
+                                          dist.isend(data, peer, group=self.group)]))
+        self.inflight = [m for m in self.inflight if not all(r.is_completed() for r in m[2])]
+
+    def _apply(self, peer, stage):
+        off = 0
+        for lo, hi in self.recvs[peer]:
+            n = hi - lo + 1
+            self.buf[lo - self.z0:hi - self.z0 + 1].copy_(stage[off:off + n])
+            off += n
+
+    DONE = -1  # version of the terminating message
+
+    def poll(self, peer, need: int | None = None, until_done: bool = False) -> int | None:
+        """Apply every halo message from `peer` that has arrived; block while
+        the newest version is below `need` (or, with until_done, until the
+        peer's terminating message).  Returns the newest version seen."""
+        newest = None
+        while peer in self.pending:
+            stage, hdr, reqs = self.pending[peer]
+            if not all(r.is_completed() for r in reqs):
+                satisfied = need is None or (newest is not None and newest >= need)
+                if satisfied and not until_done:
+                    break
+                for r in reqs:
+                    r.wait()
+            v = int(hdr.item())
+            self._apply(peer, stage)
+            if v == self.DONE:        # the peer has stopped: no more receives from it
+                del self.pending[peer]
+                break
+            newest = v
+            self._post(peer)
+        return newest
+
+    def finish(self):
+        """End-of-run protocol: send a terminating copy of the halo planes to
+        every neighbour, drain every neighbour up to its terminator (so every
+        posted receive is matched), then complete the sends."""
+        for peer in self.sends:
+            self.send(peer, self.DONE)
+        for peer in list(self.pending):
+            self.poll(peer, until_done=True)
+        for data, hdr, reqs in self.inflight:
+            for r in reqs:
+                r.wait()
+        self.inflight = []
+
+
+class AsyncShard:
+    """One rank of the asynchronous block schedule.  `step_fn(shard, block)`
+    updates x / prev of the block in place from the local slab (fused CUDA
+    step on GPUs; the oracle in CPU tests)."""
+
+    def __init__(self, layout: SlabLayout, rank: int, x_local: torch.Tensor, prev_local: torch.Tensor, transport,
+                 step_fn, max_delay: int = 2):
+        self.layout, self.rank = layout, rank
+        self.x, self.prev = x_local, prev_local
+        self.blocks = layout.owned_blocks(rank)
+        self.o_lo, self.o_hi = layout.owned(rank)
+        self.l_lo, self.l_hi = layout.local(rank)
+        self.net = transport
+        self.step_fn = step_fn
+        self.max_delay = max_delay
+        self.t = 0                      # local block updates
+        self.version = {q: 0 for q in {p for p, _, _, k in layout.transfers(rank) if k == "recv"}}
+        self.recv_ranges = {}
+        for p, lo, hi, k in layout.transfers(rank):
+            if k == "recv":
+                self.recv_ranges.setdefault(p, []).append((lo, hi))
+        self.send_ranges = {}
+        for p, lo, hi, k in layout.transfers(rank):
+            if k == "send":
+                self.send_ranges.setdefault(p, []).append((lo, hi))
+        self.staleness: list[int] = []  # per update: max over used halos of (t - version)
+        self.waits = 0
+        self.infos: list = []
+
+    def _needs(self, block):
+        s_lo = max(0, block.z_lo - self.layout.kz)
+        s_hi = min(self.layout.nz - 1, block.z_hi + self.layout.kz)
+        return [q for q, rs in self.recv_ranges.items() if any(lo <= s_hi and hi >= s_lo for lo, hi in rs)]
+
+    def update(self) -> None:
+        block = self.blocks[self.t % len(self.blocks)]
+        stale = 0
+        for q in self.recv_ranges:
+            v = self.net.poll(q)
+            if v is not None:
+                self.version[q] = v
+        for q in self._needs(block):
+            need = self.t - self.max_delay
+            if self.version[q] < need:
+                self.waits += 1
+                v = self.net.poll(q, need)
+                if v is not None:
+                    self.version[q] = v
+            stale = max(stale, max(0, self.t - self.version[q]))
+        self.staleness.append(stale)
+        self.step_fn(self, block)
+        self.t += 1
+        # every update publishes the neighbour-facing planes with version t,
+        # so a version always equals the sender's update count
+        for q in self.send_ranges:
+            self.net.send(q, self.t)
+
+    def run(self, sweeps: int) -> None:
+        for _ in range(sweeps * len(self.blocks)):
+            self.update()
+        self.net.finish()
+
+
+class LocalP2P:
+    """In-process transport between the AsyncShards of one process (several
+    virtual ranks on one device): the same message discipline as TorchP2P,
+    without blocking -- the driver's schedule must respect the delay bound."""
+
+    def __init__(self, mailbox: dict, me: int, buf: torch.Tensor, z0: int, plan):
+        self.box, self.me, self.buf, self.z0 = mailbox, me, buf, z0
+        self.recvs, self.sends = {}, {}
+        for peer, lo, hi, kind in plan:
+            (self.recvs if kind == "recv" else self.sends).setdefault(peer, []).append((lo, hi))
+
+    def send(self, peer, version: int):
+        data = torch.cat([self.buf[lo - self.z0:hi - self.z0 + 1] for lo, hi in self.sends[peer]]).clone()
+        self.box.setdefault((self.me, peer), []).append((version, data))
+
+    def poll(self, peer, need: int | None = None) -> int | None:
+        q = self.box.get((peer, self.me), [])
+        newest = None
+        while q:
+            v, data = q.pop(0)
+            off = 0
+            for lo, hi in self.recvs[peer]:
+                n = hi - lo + 1
+                self.buf[lo - self.z0:hi - self.z0 + 1].copy_(data[off:off + n])
+                off += n
+            newest = v
+        if need is not None and (newest is None or newest < need):
+            raise RuntimeError("virtual schedule violated the delay bound (would block)")
+        return newest
+
+    def finish(self):
+        pass
+
+
+def cuda_block_step(obj, dtype: torch.dtype = torch.float64):
+    """Fused in-place block step on the shard's local slab (bd3mg_mg_steps;
+    the observation is the device copy of the full y)."""
+    from . import _native as N
+    from .directions import mg_steps_device
+
+    def step(shard: AsyncShard, block: SliceBlock) -> None:
+        z0 = shard.l_lo
+        rows = slice(block.z_lo - z0, block.z_hi - z0 + 1)
+        task = N.Task(shard.x.data_ptr(), z0, shard.x.shape[0], block.z_lo, block.z_hi,
+                      shard.prev[rows].data_ptr(), None, shard.x[rows].data_ptr(), shard.prev[rows].data_ptr())
+        info = mg_steps_device(obj, [task], dtype)
+        shard.infos.append(info)
+
+    return step

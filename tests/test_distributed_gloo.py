@@ -83,3 +83,69 @@ def test_sharded_jacobi_matches_single_process(world, tmp_path, oracle_mod):
     B = -(-x0.shape[0] // h)
     want, _, _ = oracle_mod.run_bp3mg(crit, x0, B, h, max_updates=sweeps * B)
     assert np.array_equal(got, want)
+
+
+def _async_worker(rank, world, port, sweeps, max_delay, out_path):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2002_02328_b200.distributed import AsyncShard, SlabLayout, TorchP2P
+        O.core("c", threads=1)
+        crit, x0, h = _problem(O)
+        lay = SlabLayout.build(x0.shape[0], crit.kz, h, world)
+        lo, hi = lay.local(rank)
+        x = torch.from_numpy(np.ascontiguousarray(x0[lo:hi + 1])).clone()
+        prev = torch.zeros_like(x)
+
+        def step(shard, b):  # oracle block step on the local slab
+            z0 = shard.l_lo
+            s_lo, s_hi = O.support(lay.nz, crit.kz, b.z_lo, b.z_hi)
+            xl = shard.x.numpy()
+            inc = O.mg_direction(crit, xl[s_lo - z0:s_hi - z0 + 1].copy(), s_lo, b.z_lo, b.z_hi,
+                                 shard.prev.numpy()[b.z_lo - z0:b.z_hi - z0 + 1].ravel().copy())
+            inc = torch.from_numpy(inc.reshape((b.height,) + tuple(shard.x.shape[1:])))
+            shard.x[b.z_lo - z0:b.z_hi - z0 + 1] += inc
+            shard.prev[b.z_lo - z0:b.z_hi - z0 + 1] = inc
+
+        shard = AsyncShard(lay, rank, x, prev, TorchP2P(x, lo, lay.transfers(rank)), step, max_delay)
+        shard.run(sweeps)
+        dist.barrier()
+        own = x[shard.o_lo - lo:shard.o_hi - lo + 1].contiguous()
+        stale = torch.tensor([max(shard.staleness)], dtype=torch.int64)
+        dist.all_reduce(stale, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            parts = [own]
+            for q in range(1, world):
+                qlo, qhi = lay.owned(q)
+                t = torch.empty((qhi - qlo + 1,) + tuple(own.shape[1:]), dtype=own.dtype)
+                dist.recv(t, q)
+                parts.append(t)
+            np.save(out_path, torch.cat(parts).numpy())
+            np.save(str(out_path) + ".stale.npy", stale.numpy())
+        else:
+            dist.send(own, 0)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_async_bounded_delay_gloo(world, tmp_path, oracle_mod):
+    """Real asynchronous ranks (gloo P2P, no barriers between updates):
+    staleness stays within the bound and the objective descends."""
+    sweeps, max_delay = 3, 2
+    out = tmp_path / "xa.npy"
+    mp.start_processes(_async_worker, args=(world, _free_port(), sweeps, max_delay, str(out)), nprocs=world,
+                       join=True, start_method="spawn")
+    got = np.load(out)
+    stale = int(np.load(str(out) + ".stale.npy")[0])
+    crit, x0, h = _problem(oracle_mod)
+    assert stale <= max_delay
+    assert crit.value(got) < crit.value(x0)
+    B = -(-x0.shape[0] // h)
+    sync, _, _ = oracle_mod.run_bp3mg(crit, x0, B, h, max_updates=sweeps * B)
+    assert abs(crit.value(got) - crit.value(sync)) <= 0.05 * crit.value(sync)
