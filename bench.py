@@ -36,13 +36,17 @@ sys.path.insert(0, str(ROOT))
 METRIC = "BD3MG block-iterations/sec (C2 256x256x64 fp64, PSF 5x5x11, 8 blocks x 8 planes, block-Jacobi sweeps)"
 
 
-def metric_of(cfg) -> str:
-    if cfg.name == "C2":
+SCHEDULES = {"jacobi": "block-Jacobi sweeps", "cyclic": "deterministic cyclic sweeps",
+             "async": "asynchronous bounded-delay sweeps"}
+
+
+def metric_of(cfg, mode: str = "jacobi") -> str:
+    if cfg.name == "C2" and mode == "jacobi":
         return METRIC
     B = -(-cfg.dims.nz // cfg.block_height)
     return (f"BD3MG block-iterations/sec ({cfg.name} {cfg.dims.nx}x{cfg.dims.ny}x{cfg.dims.nz} {cfg.dtype}, PSF "
             f"{cfg.kdims[0]}x{cfg.kdims[1]}x{cfg.kdims[2]}, {B} blocks x {cfg.block_height} planes, "
-            "block-Jacobi sweeps)")
+            f"{SCHEDULES[mode]})")
 UNIT = "block-it/s"
 
 
@@ -57,6 +61,9 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip e2e / cpu baseline / roofline (profiling runs)")
     ap.add_argument("--strong", action="store_true",
                     help="N>1: split the N=1 volume over the ranks (default: weak scaling, the config per GPU)")
+    ap.add_argument("--mode", default="jacobi", choices=["jacobi", "cyclic", "async"],
+                    help="schedule: block-Jacobi sweeps (default), deterministic cyclic (N=1), or the "
+                         "asynchronous bounded-delay mode (stale NCCL halos, max delay 2)")
     return ap.parse_args()
 
 
@@ -260,7 +267,14 @@ def main():
     obj = objective.Objective(psf, y, params)
     B = -(-cfg.dims.nz // cfg.block_height)
 
-    if world > 1:
+    if args.mode == "async":
+        from paper_2002_02328_b200 import distributed
+        eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2)
+    elif args.mode == "cyclic":
+        if world > 1:
+            raise SystemExit("--mode cyclic is the single-worker schedule (N=1)")
+        eng = runtime.CyclicSweeper(obj, x0, cfg.block_height, dtype)
+    elif world > 1:
         from paper_2002_02328_b200 import distributed
         eng = distributed.ShardedJacobi(obj, x0, cfg.block_height, dtype)
     else:
@@ -320,6 +334,13 @@ def main():
     sweep_flops = blur.flops_jacobi_sweep(cfg.dims, cfg.kdims, blocks_all)
 
     extra = {}
+    if args.mode == "async":
+        eng.finish()
+        st = eng.shard.staleness
+        extra["async"] = {"max_delay_bound": 2, "staleness_max": max(st) if st else 0,
+                          "staleness_mean": float(np.mean(st)) if st else 0.0, "waits": eng.shard.waits}
+    if args.mode != "jacobi":
+        args.quick = True  # e2e / roofline / baselines are defined on the default schedule
     if not args.quick and rank == 0:
         extra["roofline"], extra["operators"] = roofline(obj, cfg, dtype, torch, N, D, blur)
     if not args.quick:
@@ -329,12 +350,13 @@ def main():
         extra["cpu_baseline"] = cpu_baseline(cfg)
 
     if rank == 0:
-        line = {"metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": metric_of(cfg, args.mode), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if (world > 1 and args.strong) else "weak", "vs_baseline": None,
                 "dtype": cfg.dtype, "data": "synthetic (seeded ellipsoid phantom, BASELINE PSF family)",
                 "config": _config_dict(cfg, world), "clocks": clk,
                 "gpu_launches": int(launches_per_step * args.steps),
+                "schedule": args.mode,
                 "sweep": {"variant": "exact (residual, gradient and both Gram columns recomputed every visit)",
                           "correlation_flops_per_step": sweep_flops,
                           "achieved_tflops": sweep_flops / (t_max / args.steps / 1e3) / 1e12},

@@ -469,3 +469,59 @@ def cuda_block_step(obj, dtype: torch.dtype = torch.float64):
         shard.infos.append(info)
 
     return step
+
+
+class _NoPeers:
+    """Transport of a single rank (nothing to exchange)."""
+
+    def send(self, peer, version):
+        pass
+
+    def poll(self, peer, need=None, until_done=False):
+        return None
+
+    def finish(self):
+        pass
+
+
+class AsyncEngine:
+    """bench/runtime driver of the asynchronous mode on this rank: one
+    ``sweep()`` = one pass over the rank's own blocks, no global barrier."""
+
+    def __init__(self, obj, x0, block_height: int, dtype: torch.dtype = torch.float64, max_delay: int = 2,
+                 group=None):
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.layout = SlabLayout.build(obj.dims.nz, obj.psf.kdims.kz, block_height, world)
+        lo, hi = self.layout.local(rank)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x = torch.from_numpy(np.ascontiguousarray(x0[lo:hi + 1], dtype=np.float64)).to(dev).to(dtype).contiguous()
+        prev = torch.zeros_like(x)
+        net = TorchP2P(x, lo, self.layout.transfers(rank), group) if world > 1 else _NoPeers()
+        self.shard = AsyncShard(self.layout, rank, x, prev, net, cuda_block_step(obj, dtype), max_delay)
+        self.x = x
+        self.nblocks_local = len(self.shard.blocks)
+
+    @property
+    def nblocks(self) -> int:
+        return len(self.layout.blocks)
+
+    def sweep(self) -> None:
+        for _ in range(self.nblocks_local):
+            self.shard.update()
+        if len(self.shard.infos) > 4 * self.nblocks_local:
+            self.shard.infos = self.shard.infos[-self.nblocks_local:]
+
+    def capture(self) -> None:
+        """Host-driven schedule (polls between launches): stays eager."""
+
+    def check(self) -> None:
+        for info in self.shard.infos:
+            if bool((info[:, 8] != 0).any().item()):
+                raise ValueError("non-finite gradient")
+
+    def f(self) -> float:
+        return float("nan")
+
+    def finish(self) -> None:
+        self.shard.net.finish()

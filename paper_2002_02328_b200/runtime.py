@@ -533,3 +533,71 @@ class JacobiSweeper:
     def f(self) -> float:
         """f of the anchor recorded by the last sweep (or by finish())."""
         return float(self.terms[4].item())
+
+
+class CyclicSweeper:
+    """Device-resident deterministic cyclic schedule (reference bd3mg with one
+    worker: blocks 0..B-1 in order, each step seeing every earlier update,
+    runtime.py:158-180) followed by the per-sweep recorder.  One fused
+    ``bd3mg_mg_steps`` launch set per block (in place); capturable as a
+    CUDA graph like JacobiSweeper."""
+
+    def __init__(self, obj: Objective, x0, block_height: int, dtype: torch.dtype = torch.float64):
+        self.obj, self.dtype = obj, dtype
+        self.x = D.to_device(x0, dtype).clone()
+        self.prev = torch.zeros_like(self.x)
+        self.snap = self.x.clone()
+        dims = obj.dims
+        self.blocks = scheduler.partition_blocks(dims.nz, block_height)
+        self.geom = obj.geom(dtype)
+        self.reg = D.reg(obj.params)
+        self.tasks = [(N.Task * 1)(N.Task(self.x.data_ptr(), 0, dims.nz, b.z_lo, b.z_hi,
+                                          _rows(self.prev, b.z_lo, b.z_hi).data_ptr(), None,
+                                          _rows(self.x, b.z_lo, b.z_hi).data_ptr(),
+                                          _rows(self.prev, b.z_lo, b.z_hi).data_ptr())) for b in self.blocks]
+        self.ws_bytes = max(N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(self.geom), t, 1)) for t in self.tasks)
+        dev = self.x.device
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.eval_bytes = N.ws_bytes(N.lib.bd3mg_eval_f_ws_bytes(D.byref(self.geom)))
+        self.ews = torch.empty(self.eval_bytes, dtype=torch.uint8, device=dev)
+        self.info = torch.empty((len(self.blocks), N.INFO_DOUBLES), dtype=torch.float64, device=dev)
+        self.terms = torch.empty(N.EVAL_DOUBLES, dtype=torch.float64, device=dev)
+        self.K = obj.psf.device_kernels(dtype, dev)
+        self.Y = obj.device_y(dtype, dev)
+        self.k = 0
+        self.graph = None
+
+    @property
+    def nblocks(self) -> int:
+        return len(self.blocks)
+
+    def _launch(self) -> None:
+        s = D.stream_handle()
+        for i, t in enumerate(self.tasks):
+            N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
+                                         t, 1, self.info[i].data_ptr(), self.ws.data_ptr(), self.ws_bytes, s))
+        N.check(N.lib.bd3mg_eval_f(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
+                                   self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
+                                   self.ews.data_ptr(), self.eval_bytes, s))
+        self.snap.copy_(self.x)
+
+    def capture(self) -> None:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch()
+        self.graph = g
+
+    def sweep(self) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch()
+        self.k += len(self.blocks)
+
+    def check(self) -> None:
+        if bool((self.info[:, 8] != 0).any().item()):
+            raise ValueError("non-finite gradient")
+
+    def f(self) -> float:
+        """f after the last sweep (the reference's per-sweep log value)."""
+        return float(self.terms[4].item())

@@ -80,3 +80,22 @@ def test_hd_cache_variant_tracks_exact(oracle_mod):
     xa, xb = a.x.cpu().numpy(), b.x.cpu().numpy()
     assert np.linalg.norm(xa - xb) <= 1e-10 * np.linalg.norm(xa)
     assert abs(a.finish() - b.finish()) <= 1e-11 * abs(a.f())
+
+
+def test_cyclic_sweeper_matches_runtime():
+    """Device cyclic sweeps == runtime.run(bd3mg, workers=1) iterate and log."""
+    from paper_2002_02328_b200 import configs, objective, runtime
+    cfg = configs.CONFIGS["C1"]
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    obj = objective.Objective(psf, y, params)
+    eng = runtime.CyclicSweeper(obj, x0, cfg.block_height, torch.float64)
+    eng.sweep()
+    eng.capture()
+    fs = [eng.f()]
+    for _ in range(4):
+        eng.sweep()
+        fs.append(eng.f())
+    res = runtime.run(obj, x0, runtime.RunConfig(method="bd3mg", workers=1, block_height=8, tol=1e-30,
+                                                 max_updates=15))
+    np.testing.assert_allclose(fs, [e.f_value for e in res.log], rtol=1e-13)
+    assert np.array_equal(eng.x.cpu().numpy(), res.x_final)
