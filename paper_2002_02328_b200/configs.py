@@ -73,6 +73,11 @@ def make_problem(cfg: Config | str, y_from=None):
         cfg = CONFIGS[cfg]
     psf = depth_variant_stack(cfg.dims, cfg.kdims, cfg.sigma_xy, cfg.sigma_z)
     truth = truth_of(cfg)
+    if y_from is None and cfg.dtype == "f32":
+        # fp32 configs: the observation is blurred in fp32 on the GPU (the fp64
+        # H of C5 alone is ~1.7 TFLOP); every consumer reads this same y
+        import torch
+        y_from = lambda p, t: apply_H(p, torch.from_numpy(t).cuda().float()).double().cpu().numpy()
     blurred = (y_from or apply_H)(psf, truth)
     y = add_gaussian_noise(blurred, cfg.noise, cfg.seed + 2)
     x0 = init_uniform(cfg.dims, float(np.max(y)), cfg.seed + 3)
