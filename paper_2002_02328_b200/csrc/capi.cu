@@ -319,6 +319,35 @@ int omega_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* frag, int64
 
 // ---------------------------------------------------------------------------
 // Batched mg_direction (+ optional in-place receive_update).
+// A side stream (+ fork/join events) per (device, main stream): the sweep
+// runs its HBM-bound stencils next to the FMA-bound correlations.  Event
+// record / wait is legal inside CUDA-graph capture (the side stream joins the
+// capture and is joined back before the sweep returns).
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+cudaError_t side_stream(cudaStream_t main, SideStream** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SideStream> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& ss = cache[{dev, main}];
+  if (!ss.side) {
+    e = cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  *out = &ss;
+  return cudaSuccess;
+}
+inline cudaError_t hop(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+  cudaError_t e = cudaEventRecord(ev, from);
+  return e == cudaSuccess ? cudaStreamWaitEvent(to, ev, 0) : e;
+}
+
 // Options of the batched step used by the sweep driver.
 template <typename T>
 struct StepOpts {
@@ -327,6 +356,7 @@ struct StepOpts {
   T* const* hd = nullptr;      // per task: cached H E_S d_mem over rows [olo, ohi] (updated in place)
   T* const* greg = nullptr;    // per task: precomputed regulariser gradient rows (skip the greg launch)
   T* const* omega = nullptr;   // per task: precomputed omega rows
+  SideStream* ss = nullptr;    // run reg_gram next to the Gram correlation
 };
 
 template <typename T>
@@ -439,6 +469,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       }
     }
   }
+  // join the recorder / regulariser-gradient stencil of the side stream
+  if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
   // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
   if (!pre) {
     StArgs<T> sa = st_args<T>(g, r);
@@ -462,7 +494,13 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     CU(conv_launch<T>(M_GRAD, true, a, 0, s));
     launched();
   }
-  // (3) regulariser Gram terms + rhs + flags (tiled stencil)
+  // (3) regulariser Gram terms + rhs + flags (tiled stencil); on the side
+  //     stream when available, concurrent with the Gram correlation (4)
+  cudaStream_t s3 = s;
+  if (opt.ss) {
+    CU(hop(s, opt.ss->side, opt.ss->ev[2]));
+    s3 = opt.ss->side;
+  }
   {
     StArgs<T> sa = st_args<T>(g, r);
     sa.njobs = nt;
@@ -472,7 +510,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       J.a = gb[t]; J.a_z0 = tasks[t].z_lo; J.b = (const T*)tasks[t].d_mem; J.w = wb[t];
       J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi;
     }
-    CU(st_launch_z<T>(reg_gram_z_kernel<T>, sa, reg_gram_z_smem<T>(), s));
+    CU(st_launch_z<T>(reg_gram_z_kernel<T>, sa, reg_gram_z_smem<T>(), s3));
   }
   // (4) data Gram <H b_i, H b_j> (forward only, both columns share the taps)
   std::vector<std::pair<long long, long long>> granges(nt);
@@ -496,6 +534,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       granges[t] = {b0, b0 + conv_rows<T>(g, gmode, a.jobs[t].nout)};
     }
   }
+  if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[3]));  // join the side stream
   // (5)+(6) per-block reductions and the 2x2 solves, one CTA per block
   {
     SolveArgs sa;
@@ -622,11 +661,19 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   opt.rec_hi = sw->rec_hi;
   opt.hd = sw->hd_cache ? hd.data() : nullptr;
   if (fused) { opt.greg = grb.data(); opt.omega = wb.data(); }
+  SideStream* ss = nullptr;
+  cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
   if (!ws.measure) {
     if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+    if (fused && !getenv("BD3MG_NO_SIDE_STREAM")) {
+      CU(side_stream(s, &ss));
+      opt.ss = ss;
+      CU(hop(s, ss->side, ss->ev[0]));  // fork: the stencil runs next to the residual correlation
+      s1 = ss->side;
+    }
     // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll
     if (!rec) {
-      CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s));
+      CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s1));
     } else {
       StArgs<T> e = st_args<T>(g, r);
       e.partials = eparts;
@@ -638,17 +685,17 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
           J.b = sw->snap ? (const T*)sw->snap + (J.lo - sw->rec_lo) * plane : nullptr;
           J.out0 = grb[b]; J.out1 = wb[b];
         }
-        CU(st_launch_z<T>(greg_z_kernel<T, true>, e, greg_z_smem<T>(), s));
+        CU(st_launch_z<T>(greg_z_kernel<T, true>, e, greg_z_smem<T>(), s1));
       } else {
         e.njobs = 1;
         e.jobs[0].a = x; e.jobs[0].a_z0 = sw->frag_z0; e.jobs[0].b = (const T*)sw->snap;
         e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
-        CU(st_launch<T>(eval_kernel<T>, e, s));
+        CU(st_launch<T>(eval_kernel<T>, e, s1));
       }
-      CU(reduce(eparts, kEvalNV, {{0, (fused ? nb : nrec) * st_tiles(g)}}, sums + 1, kEvalNV, s));
+      CU(reduce(eparts, kEvalNV, {{0, (fused ? nb : nrec) * st_tiles(g)}}, sums + 1, kEvalNV, s1));
       if (sw->snap)
         CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
-                           cudaMemcpyDeviceToDevice, s));
+                           cudaMemcpyDeviceToDevice, s1));
     }
   }
   // (2) the fused block steps at the anchor (x, dmem updated in place)
