@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbd3mg_b200.so"
+LIB_PATH = Path(os.environ.get("BD3MG_LIB") or Path(__file__).resolve().parent / "_lib" / "libbd3mg_b200.so")
 
 BD3MG_OK, BD3MG_EINVAL, BD3MG_ECUDA, BD3MG_EWORKSPACE, BD3MG_ENONFINITE = range(5)
 BD3MG_F64, BD3MG_F32 = 0, 1

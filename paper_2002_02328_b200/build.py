@@ -16,14 +16,16 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-LIBDIR = PKG / "_lib"
+# BD3MG_BUILD_DIR / BD3MG_DEFS: out-of-tree experiment builds (tuning variants)
+LIBDIR = Path(os.environ.get("BD3MG_BUILD_DIR") or PKG / "_lib")
 OBJDIR = LIBDIR / "obj"
 LIB = LIBDIR / "libbd3mg_b200.so"
 INCLUDE = PKG.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
+         *os.environ.get("BD3MG_DEFS", "").split()]
 UNITS = ["capi.cu", "conv_f64.cu", "conv_f32.cu", "microbench.cu"]
 
 

@@ -18,6 +18,7 @@
 #include "../../include/bd3mg_b200.h"
 #include "conv_dispatch.cuh"
 #include "solver.cuh"
+#include "stencil_tma.cuh"
 
 using namespace bd3mg;
 
@@ -120,6 +121,70 @@ cudaError_t st_launch_z(Kern kern, StArgs<T>& a, size_t smem, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// TMA-staged stencils when every row is a whole number of 16-byte chunks.
+template <typename T>
+bool st_use_tma(long long nx) {
+  static const bool off = getenv("BD3MG_NO_TMA") != nullptr;
+  return !off && (nx * (long long)sizeof(T)) % 16 == 0;
+}
+// partial rows per job of the z-marching stencils (greg / reg_gram)
+template <typename T>
+long long z_tiles(const bd3mg_geom_t* g) {
+  return st_use_tma<T>(g->nx) ? tm_tiles(g->ny, g->nx) : st_tiles(g);
+}
+
+// Regulariser gradient (+ omega, + recorder terms when `eval`) of every job.
+template <typename T>
+int launch_greg(StArgs<T>& a, bool eval, cudaStream_t s) {
+  if (a.njobs == 0) return BD3MG_OK;
+  if (!st_use_tma<T>(a.nx)) {
+    CU(st_launch_z<T>(eval ? greg_z_kernel<T, true> : greg_z_kernel<T, false>, a, greg_z_smem<T>(), s));
+    return BD3MG_OK;
+  }
+  using G = GregGeo<T>;
+  static StTma<T> tm;  // host staging of the descriptors (copied into the launch)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int j = 0; j < a.njobs; ++j) {
+    const StJob<T>& J = a.jobs[j];
+    const long long zl = std::min<long long>(J.hi + 1, a.nz - 1);
+    if (!encode_tmap(&tm.a[j], J.a, sizeof(T) == 8, a.nx, a.ny, zl - J.a_z0 + 1, G::BW, G::BH))
+      return fail(BD3MG_EINVAL, "greg: TMA descriptor rejected (job %d)", j);
+  }
+  auto kern = eval ? greg_t_kernel<T, true> : greg_t_kernel<T, false>;
+  CU(ensure_smem_attr(kern, G::smem()));
+  kern<<<dim3((a.nx + kTmX - 1) / kTmX, (a.ny + kTmY - 1) / kTmY, a.njobs), kTmNT, G::smem(), s>>>(a, tm);
+  launched();
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+// Regulariser Gram terms of every job (a = g rows, b = d rows, w = omega rows).
+template <typename T>
+int launch_reg_gram(StArgs<T>& a, cudaStream_t s) {
+  if (a.njobs == 0) return BD3MG_OK;
+  if (!st_use_tma<T>(a.nx)) {
+    CU(st_launch_z<T>(reg_gram_z_kernel<T>, a, reg_gram_z_smem<T>(), s));
+    return BD3MG_OK;
+  }
+  using G = RgGeo<T>;
+  static StTma<T> tm;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int j = 0; j < a.njobs; ++j) {
+    const StJob<T>& J = a.jobs[j];
+    const long long h = J.hi - J.lo + 1;
+    if (!encode_tmap(&tm.a[j], J.a, sizeof(T) == 8, a.nx, a.ny, h, G::BW, G::BH) ||
+        (J.b && !encode_tmap(&tm.b[j], J.b, sizeof(T) == 8, a.nx, a.ny, h, G::BW, G::BH)))
+      return fail(BD3MG_EINVAL, "reg_gram: TMA descriptor rejected (job %d)", j);
+  }
+  CU(ensure_smem_attr(reg_gram_t_kernel<T>, G::smem()));
+  reg_gram_t_kernel<T><<<dim3((a.nx + kTmX - 1) / kTmX, (a.ny + kTmY - 1) / kTmY, a.njobs), kTmNT, G::smem(), s>>>(a, tm);
+  launched();
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
 // Lay jobs out along grid.z (one plane per z index) and launch `kern`.
 template <typename T, typename Kern>
 cudaError_t st_launch(Kern kern, StArgs<T>& a, cudaStream_t s) {
@@ -208,7 +273,8 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     sa.njobs = 1;
     sa.jobs[0].a = frag; sa.jobs[0].a_z0 = frag_z0; sa.jobs[0].lo = (int)lo; sa.jobs[0].hi = (int)hi;
     sa.jobs[0].out0 = greg; sa.jobs[0].out1 = omega_out;
-    CU(st_launch_z<T>(greg_z_kernel<T, false>, sa, greg_z_smem<T>(), s));
+    int rc = launch_greg<T>(sa, false, s);
+    if (rc) return rc;
   }
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
@@ -439,7 +505,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   long long hsum = 0;
   for (int t = 0; t < nt; ++t) hsum += h[t];
-  const long long reg_rows = (long long)nt * st_tiles(g);  // one partial row per (block, tile)
+  const long long reg_rows = (long long)nt * z_tiles<T>(g);  // one partial row per (block, tile)
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
@@ -480,7 +546,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
       J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi; J.out0 = grb[t]; J.out1 = wb[t];
     }
-    CU(st_launch_z<T>(greg_z_kernel<T, false>, sa, greg_z_smem<T>(), s));
+    int rc = launch_greg<T>(sa, false, s);
+    if (rc) return rc;
   }
   {
     ConvArgs<T> a = base_args<T>(g, r, K);
@@ -510,7 +577,10 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       J.a = gb[t]; J.a_z0 = tasks[t].z_lo; J.b = (const T*)tasks[t].d_mem; J.w = wb[t];
       J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi;
     }
-    CU(st_launch_z<T>(reg_gram_z_kernel<T>, sa, reg_gram_z_smem<T>(), s3));
+#ifndef BD3MG_EXP_SKIP_REGGRAM
+    int rc = launch_reg_gram<T>(sa, s3);
+    if (rc) return rc;
+#endif
   }
   // (4) data Gram <H b_i, H b_j> (forward only, both columns share the taps)
   std::vector<std::pair<long long, long long>> granges(nt);
@@ -543,7 +613,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     sa.two_eta = 2.0 * r->eta; sa.lam = r->lam; sa.two_kappa = 2.0 * r->kappa;
     sa.prune_tol = kPruneTol; sa.pinv_tol = kPinvTol;
     sa.nv_gram = gmode == M_GRAM1 ? 1 : 3;
-    const long long tl = st_tiles(g);
+    const long long tl = z_tiles<T>(g);
     for (int t = 0; t < nt; ++t) {
       sa.has_d[t] = tasks[t].d_mem != nullptr;
       sa.g_begin[t] = granges[t].first; sa.g_end[t] = granges[t].second;
@@ -566,7 +636,9 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       B.ctas = (int)std::max<int64_t>(1, std::min<int64_t>((B.n + 4 * kEwNT - 1) / (4 * kEwNT), 1024));
       mc = std::max(mc, B.ctas);
     }
+#ifndef BD3MG_EXP_SKIP_UPDATE
     update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, info_out); launched();
+#endif
     CU(cudaGetLastError());
   }
   // (8) cached H E_S d_mem for the next visit (variant "hd-cache")
@@ -646,7 +718,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   const bool fused = rec && contiguous && bmin == sw->rec_lo && bmax == sw->rec_hi && hsum == nrec;
   if (rec && (sw->rec_lo < sw->frag_z0 || sw->rec_hi >= sw->frag_z0 + sw->nzf))
     return fail(BD3MG_EINVAL, "recorder rows outside the fragment");
-  const long long erows = std::max<long long>(1, nrec * st_tiles(g));
+  const long long erows = std::max<long long>(1, std::max<long long>(nrec * st_tiles(g), nb * z_tiles<T>(g)));
   double* eparts = ws.take<double>((size_t)erows * kEvalNV);
   double* sums = ws.take<double>(8);
   if (fused)
@@ -685,14 +757,17 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
           J.b = sw->snap ? (const T*)sw->snap + (J.lo - sw->rec_lo) * plane : nullptr;
           J.out0 = grb[b]; J.out1 = wb[b];
         }
-        CU(st_launch_z<T>(greg_z_kernel<T, true>, e, greg_z_smem<T>(), s1));
+#ifndef BD3MG_EXP_SKIP_GREG
+        int rc = launch_greg<T>(e, true, s1);
+        if (rc) return rc;
+#endif
       } else {
         e.njobs = 1;
         e.jobs[0].a = x; e.jobs[0].a_z0 = sw->frag_z0; e.jobs[0].b = (const T*)sw->snap;
         e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
         CU(st_launch<T>(eval_kernel<T>, e, s1));
       }
-      CU(reduce(eparts, kEvalNV, {{0, (fused ? nb : nrec) * st_tiles(g)}}, sums + 1, kEvalNV, s1));
+      CU(reduce(eparts, kEvalNV, {{0, fused ? nb * z_tiles<T>(g) : nrec * st_tiles(g)}}, sums + 1, kEvalNV, s1));
       if (sw->snap)
         CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
                            cudaMemcpyDeviceToDevice, s1));

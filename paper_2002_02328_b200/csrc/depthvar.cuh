@@ -120,6 +120,9 @@ BD3MG_D T omega_of(T dx, T dy, T delta2) {
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
 
+#ifndef BD3MG_RY1
+#define BD3MG_RY1 16  // rows per thread of the single-input modes
+#endif
 template <typename T, int KY_, int KX_, int MODE>
 struct ConvCfg {
   static constexpr bool DUAL = (MODE == M_GRAM2);
@@ -127,7 +130,7 @@ struct ConvCfg {
   static constexpr int VEC = 16 / sizeof(T);        // elements per 16-byte load
   static constexpr int RX = VEC;                    // outputs per thread in x
   // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32)
-  static constexpr int RY = DUAL ? (sizeof(T) == 8 ? 8 : 4) : 16;
+  static constexpr int RY = DUAL ? (sizeof(T) == 8 ? 8 : 4) : BD3MG_RY1;
   static constexpr int WX = 32, WY = 4;             // a warp spans one row group
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;

@@ -1,0 +1,323 @@
+// TMA-staged z-marching stencils (used when a row is a whole number of
+// 16-byte chunks, i.e. nx * sizeof(T) % 16 == 0; stencil.cuh keeps the
+// cp.async kernels for the other shapes).
+//
+// One CTA owns a 32 x 16 pixel tile of all rows of a job and walks them in
+// depth.  Plane tiles (with the halo the stencil needs) arrive by one
+// cp.async.bulk.tensor per plane into a ring of mbarrier-tracked slots, so
+// the load path costs one instruction per plane instead of an address
+// computation and a predicate per element; out-of-volume halo entries are
+// zero-filled by the TMA unit.  Each thread owns 4 pixels of a column and
+// keeps their values in registers between the two passes of a plane.
+//
+//   greg_t_kernel      = greg_z_kernel   (regulariser gradient, omega, recorder terms)
+//   reg_gram_t_kernel  = reg_gram_z_kernel (regulariser Gram terms, rhs, flags)
+//
+// Arithmetic is operation-for-operation that of the cp.async kernels
+// (reference objective.py:130-137, :175-186, :262-274; directions.py:80-85).
+#pragma once
+
+#include <cuda.h>
+
+#include "stencil.cuh"
+
+namespace bd3mg {
+
+constexpr int kTmX = 32;                   // tile width  (one warp row)
+constexpr int kTmY = 16;                   // tile height
+constexpr int kTmNT = 128;                 // 4 warps
+constexpr int kTmR = kTmY / (kTmNT / 32);  // pixels (rows) per thread
+
+template <typename T>
+struct StTma {
+  CUtensorMap a[kMaxJobs];  // greg: x fragment; reg_gram: g rows
+  CUtensorMap b[kMaxJobs];  // reg_gram: d rows
+};
+
+// Box geometry: width padded to an even number of 16-byte chunks, height so
+// the box is a whole number of 128-byte lines (scripts/tma_probe.py).
+template <typename T>
+struct GregGeo {
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  // x from x0 - VEC to x0 + 32 (pixel x0-1 needs its right neighbour x0 .. ;
+  // pixel x0+31 needs x0+32); rows y0-1 .. y0+16
+  static constexpr int BW = (kTmX + 1 + VEC + 2 * VEC - 1) / (2 * VEC) * (2 * VEC);
+  static constexpr int ROWQ = 128 / cgcd(BW * (int)sizeof(T), 128);
+  static constexpr int BH = (kTmY + 2 + ROWQ - 1) / ROWQ * ROWQ;
+  static constexpr int PL = BW * BH;
+  static constexpr int RING = 4;  // z-1, z, z+1 resident, z+2 in flight
+  static constexpr int PP = kTmX + 1;  // px/py region cols x0-1 .. x0+31
+  static constexpr size_t smem() {
+    return 128 + (size_t)RING * PL * sizeof(T) + 2 * (size_t)(kTmY + 1) * PP * sizeof(T) +
+           (kTmNT / 32) * kEvalNV * 8 + RING * 8;
+  }
+};
+
+template <typename T>
+struct RgGeo {
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  // x from x0 to x0 + 32, rows y0 .. y0 + 16
+  static constexpr int BW = (kTmX + 1 + 2 * VEC - 1) / (2 * VEC) * (2 * VEC);
+  static constexpr int ROWQ = 128 / cgcd(BW * (int)sizeof(T), 128);
+  static constexpr int BH = (kTmY + 1 + ROWQ - 1) / ROWQ * ROWQ;
+  static constexpr int PL = BW * BH;
+  static constexpr int RING = 3;  // z, z+1 resident, z+2 in flight
+  static constexpr size_t smem() {
+    return 128 + 2 * (size_t)RING * PL * sizeof(T) + (kTmNT / 32) * kRegNV * 8 + RING * 8;
+  }
+};
+
+// Partial rows are job-major like the cp.async kernels, on this tiling.
+inline long long tm_tiles(long long ny, long long nx) {
+  return ((nx + kTmX - 1) / kTmX) * ((ny + kTmY - 1) / kTmY);
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, bool EVAL>
+__global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ StArgs<T> p,
+                                                       const __grid_constant__ StTma<T> tm) {
+  using G = GregGeo<T>;
+  constexpr int VEC = G::VEC, PP = G::PP;
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  unsigned char* base = st_smem + ((128 - (smem_u32(st_smem) & 127)) & 127);
+  T (*xs)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base);
+  T* pxs = reinterpret_cast<T*>(base + G::RING * G::PL * sizeof(T));
+  T* pys = pxs + (kTmY + 1) * PP;
+  double* red = reinterpret_cast<double*>(pys + (kTmY + 1) * PP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kEvalNV);
+
+  const int job = blockIdx.z;
+  const StJob<T>& J = p.jobs[job];
+  const int x0 = blockIdx.x * kTmX, y0 = blockIdx.y * kTmY;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int zfirst = max(J.lo - 1, 0), zlast = min(J.hi + 1, p.nz - 1);
+  const int nx = p.nx, ny = p.ny;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G::RING; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto slot = [&](int z) { return (z - zfirst) % G::RING; };
+  auto phase = [&](int z) { return (uint32_t)((z - zfirst) / G::RING) & 1u; };
+  auto issue = [&](int z) {  // thread 0
+    const int s = slot(z);
+    mbar_expect_tx(&bars[s], G::PL * sizeof(T));
+    tma_load_3d(xs[s], &tm.a[job], x0 - VEC, y0 - 1, (int)(z - J.a_z0), &bars[s]);
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm.a[job]);
+    for (int z = zfirst; z <= min(J.lo + 1, zlast); ++z) issue(z);
+  }
+  for (int z = zfirst; z <= J.lo; ++z) mbar_wait(&bars[slot(z)], phase(z));
+
+  const T d2 = (T)p.delta2;
+  const T two_eta = (T)p.two_eta, lam = (T)p.lam, two_kappa = (T)p.two_kappa;
+  const T xmin = (T)p.x_min, xmax = (T)p.x_max;
+  const int x = x0 + lane;
+  double ev[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  // extra px/py item of this thread: region row 0 (c = 0..32) or column 0 (r = 1..16)
+  constexpr int NEXTRA = PP + kTmY;
+  const int er = threadIdx.x < PP ? 0 : threadIdx.x - PP + 1;
+  const int ec = threadIdx.x < PP ? threadIdx.x : 0;
+  const int ey = y0 - 1 + er, ex = x0 - 1 + ec;
+
+  for (int z = J.lo; z <= J.hi; ++z) {
+    const long long orow = (long long)(z - J.lo) * p.plane;
+    T sn[kTmR];
+    if constexpr (EVAL) {
+#pragma unroll
+      for (int j = 0; j < kTmR; ++j) {
+        const int y = y0 + warp * kTmR + j;
+        sn[j] = (J.b && y < ny && x < nx) ? J.b[orow + (long long)y * nx + x] : T(0);
+      }
+    }
+    if (threadIdx.x == 0 && z + 2 <= zlast) issue(z + 2);
+    if (z + 1 <= zlast) mbar_wait(&bars[slot(z + 1)], phase(z + 1));
+    const T* xc_t = xs[slot(z)];
+    // pass 1: omega, w*dx, w*dy of the own pixels (kept in registers) and of
+    // the row-above / column-left halo (shared with the neighbours)
+    T xc[kTmR], px[kTmR], py[kTmR];
+#pragma unroll
+    for (int j = 0; j < kTmR; ++j) {
+      const int ly = warp * kTmR + j, y = y0 + ly;
+      const int si = (ly + 1) * G::BW + lane + VEC;
+      xc[j] = xc_t[si];
+      const T dx = (x < nx - 1) ? sub_rn(xc_t[si + 1], xc[j]) : T(0);
+      const T dy = (y < ny - 1) ? sub_rn(xc_t[si + G::BW], xc[j]) : T(0);
+      const T sq = add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), d2);
+      const T w = rsqrt(sq);
+      px[j] = mul_rn(w, dx);
+      py[j] = mul_rn(w, dy);
+      pxs[(ly + 1) * PP + lane + 1] = px[j];
+      pys[(ly + 1) * PP + lane + 1] = py[j];
+      if (y < ny && x < nx) {
+        J.out1[orow + (long long)y * nx + x] = w;
+        if constexpr (EVAL) ev[1] += (double)sq * (double)w;
+      }
+    }
+    if (threadIdx.x < NEXTRA) {
+      T ex_px = T(0), ex_py = T(0);
+      if (ey >= 0 && ex >= 0 && ey < ny && ex < nx) {
+        const int si = er * G::BW + ec - 1 + VEC;
+        const T c = xc_t[si];
+        const T dx = (ex < nx - 1) ? sub_rn(xc_t[si + 1], c) : T(0);
+        const T dy = (ey < ny - 1) ? sub_rn(xc_t[si + G::BW], c) : T(0);
+        const T w = rsqrt(add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), d2));
+        ex_px = mul_rn(w, dx);
+        ex_py = mul_rn(w, dy);
+      }
+      pxs[er * PP + ec] = ex_px;
+      pys[er * PP + ec] = ex_py;
+    }
+    __syncthreads();
+    // pass 2: box + TV divergence + axial terms
+    const T* xm_t = xs[slot(max(z - 1, zfirst))];
+    const T* xp_t = xs[slot(min(z + 1, zlast))];
+    const bool has_m = z >= 1, has_p = z < p.nz - 1;
+#pragma unroll
+    for (int j = 0; j < kTmR; ++j) {
+      const int ly = warp * kTmR + j, y = y0 + ly;
+      if (y >= ny || x >= nx) continue;
+      const int si = (ly + 1) * G::BW + lane + VEC;
+      const T clipped = xc[j] < xmin ? xmin : (xc[j] > xmax ? xmax : xc[j]);
+      const T box = mul_rn(two_eta, sub_rn(xc[j], clipped));
+      const T pxm = pxs[(ly + 1) * PP + lane], pym = pys[ly * PP + lane + 1];
+      const T tvx = (nx == 1) ? T(0) : sub_rn(pxm, px[j]);
+      const T tvy = (ny == 1) ? T(0) : sub_rn(pym, py[j]);
+      const T xzp = has_p ? xp_t[si] : T(0);
+      const T dzm = has_m ? sub_rn(xc[j], xm_t[si]) : T(0);
+      const T dzp = has_p ? sub_rn(xzp, xc[j]) : T(0);
+      J.out0[orow + (long long)y * nx + x] =
+          add_rn(add_rn(box, mul_rn(lam, add_rn(tvx, tvy))), mul_rn(two_kappa, sub_rn(dzm, dzp)));
+      if constexpr (EVAL) {
+        const double e = (double)xc[j] - (double)clipped;
+        ev[0] += e * e;
+        if (has_p) ev[2] += ((double)xzp - (double)xc[j]) * ((double)xzp - (double)xc[j]);
+        if (J.b) {
+          ev[3] += ((double)xc[j] - (double)sn[j]) * ((double)xc[j] - (double)sn[j]);
+          ev[4] += (double)sn[j] * (double)sn[j];
+        }
+      }
+    }
+    __syncthreads();  // px/py rewritten and the slot of z-1 refilled next iteration
+  }
+  if constexpr (EVAL) {
+    cta_reduce<kEvalNV, kTmNT>(ev, red);
+    if (threadIdx.x == 0) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+      for (int k = 0; k < kEvalNV; ++k) p.partials[cta * kEvalNV + k] = ev[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant__ StArgs<T> p,
+                                                           const __grid_constant__ StTma<T> tm) {
+  using G = RgGeo<T>;
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  unsigned char* base = st_smem + ((128 - (smem_u32(st_smem) & 127)) & 127);
+  T (*gs)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base);
+  T (*dss)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base + G::RING * G::PL * sizeof(T));
+  double* red = reinterpret_cast<double*>(base + 2 * G::RING * G::PL * sizeof(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kRegNV);
+
+  const int job = blockIdx.z;
+  const StJob<T>& J = p.jobs[job];
+  const int x0 = blockIdx.x * kTmX, y0 = blockIdx.y * kTmY;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool has_d = J.b != nullptr;
+  const int nx = p.nx, ny = p.ny;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G::RING; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto slot = [&](int z) { return (z - J.lo) % G::RING; };
+  auto phase = [&](int z) { return (uint32_t)((z - J.lo) / G::RING) & 1u; };
+  auto issue = [&](int z) {  // thread 0
+    const int s = slot(z);
+    mbar_expect_tx(&bars[s], (has_d ? 2 : 1) * G::PL * sizeof(T));
+    tma_load_3d(gs[s], &tm.a[job], x0, y0, z - J.lo, &bars[s]);
+    if (has_d) tma_load_3d(dss[s], &tm.b[job], x0, y0, z - J.lo, &bars[s]);
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm.a[job]);
+    if (has_d) tma_prefetch_desc(&tm.b[job]);
+    issue(J.lo);
+    if (J.lo + 1 <= J.hi) issue(J.lo + 1);
+  }
+  mbar_wait(&bars[slot(J.lo)], phase(J.lo));
+
+  double v[kRegNV];
+#pragma unroll
+  for (int k = 0; k < kRegNV; ++k) v[k] = 0.0;
+  const int x = x0 + lane;
+  for (int z = J.lo; z <= J.hi; ++z) {
+    const long long orow = (long long)(z - J.lo) * p.plane;
+    T wv[kTmR];
+#pragma unroll
+    for (int j = 0; j < kTmR; ++j) {
+      const int y = y0 + warp * kTmR + j;
+      wv[j] = (y < ny && x < nx) ? J.w[orow + (long long)y * nx + x] : T(0);
+    }
+    if (threadIdx.x == 0 && z + 2 <= J.hi) issue(z + 2);
+    if (z + 1 <= J.hi) mbar_wait(&bars[slot(z + 1)], phase(z + 1));
+    const T* g0 = gs[slot(z)];
+    const T* d0 = dss[slot(z)];
+    const T* g1 = gs[slot(min(z + 1, J.hi))];
+    const T* d1 = dss[slot(min(z + 1, J.hi))];
+#pragma unroll
+    for (int j = 0; j < kTmR; ++j) {
+      const int ly = warp * kTmR + j, y = y0 + ly;
+      if (y >= ny || x >= nx) continue;
+      const int q = ly * G::BW + lane;
+      const T g = g0[q];
+      const T d = has_d ? d0[q] : T(0);
+      const double b0 = -(double)g, b1 = (double)d;
+      v[0] += b0 * b0;
+      v[1] += b0 * b1;
+      v[2] += b1 * b1;
+      const double w = (double)wv[j];
+      const double dx0 = (x < nx - 1) ? -(double)sub_rn(g0[q + 1], g) : 0.0;
+      const double dy0 = (y < ny - 1) ? -(double)sub_rn(g0[q + G::BW], g) : 0.0;
+      const double dx1 = (has_d && x < nx - 1) ? (double)sub_rn(d0[q + 1], d) : 0.0;
+      const double dy1 = (has_d && y < ny - 1) ? (double)sub_rn(d0[q + G::BW], d) : 0.0;
+      v[3] += w * (dx0 * dx0 + dy0 * dy0);
+      v[4] += w * (dx0 * dx1 + dy0 * dy1);
+      v[5] += w * (dx1 * dx1 + dy1 * dy1);
+      double z0v, z1v;  // axial row z of the block-embedded vectors
+      if (z < J.hi) {
+        z0v = -((double)g1[q] - (double)g);
+        z1v = has_d ? (double)d1[q] - (double)d : 0.0;
+      } else if (J.hi < p.nz - 1) {
+        z0v = -b0;
+        z1v = -b1;
+      } else {
+        z0v = 0.0;
+        z1v = 0.0;
+      }
+      v[6] += z0v * z0v;
+      v[7] += z0v * z1v;
+      v[8] += z1v * z1v;
+      if (z == J.lo && J.lo >= 1) {
+        v[6] += b0 * b0;
+        v[7] += b0 * b1;
+        v[8] += b1 * b1;
+      }
+      v[9] += (double)g * (double)d;
+      v[10] += (g != T(0)) ? 1.0 : 0.0;
+      v[11] += isfinite((double)g) ? 0.0 : 1.0;
+    }
+    __syncthreads();  // slot of z is refilled next iteration
+  }
+  cta_reduce<kRegNV, kTmNT>(v, red);
+  if (threadIdx.x == 0) {
+    const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int k = 0; k < kRegNV; ++k) p.partials[cta * kRegNV + k] = v[k];
+  }
+}
+
+}  // namespace bd3mg
