@@ -32,7 +32,9 @@ enum {
   BD3MG_EINVAL = 1,      /* bad shape / range / coverage (reference: ValueError) */
   BD3MG_ECUDA = 2,       /* CUDA runtime failure */
   BD3MG_EWORKSPACE = 3,  /* workspace smaller than *_ws_bytes reported */
-  BD3MG_ENONFINITE = 4   /* non-finite gradient (directions.py:64-65) */
+  BD3MG_ENONFINITE = 4,  /* non-finite gradient (directions.py:64-65) */
+  BD3MG_EFORMAT = 5,     /* container payload violates the format (volume.py:31 FormatError) */
+  BD3MG_EIO = 6          /* file open / read / write failure (reference: OSError) */
 };
 
 enum { BD3MG_F64 = 0, BD3MG_F32 = 1 };
@@ -226,6 +228,25 @@ int bd3mg_fma_probe(int32_t dtype, int32_t blocks, int32_t iters, void* out, dou
  * call for a fragment), so only x crosses PCIe. */
 int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, int64_t frag_z0, int64_t nzf,
                                     const int64_t* blocks, int nblocks, double* terms_out, double* info_out);
+
+/* ---- BD3MGVOL / BD3MGPSF payloads straight to / from device memory ----
+ * The containers (reference volume.py:104-145 write_volume/read_volume,
+ * blur.py:201-236 write_psf/read_psf) are a little-endian header and a
+ * float64 payload; the host parses the header, these move the payload
+ * through two alternating pinned 16 MiB chunks (file read overlapped with the
+ * H2D copy).  dtype selects the device element type (fp32: narrowed on the
+ * device after the float64 finiteness check). */
+/* Read n float64 values at byte `offset` of `path` into dev_out.  Synchronous.
+ * BD3MG_EFORMAT: "truncated payload ..." (file too short) or "non-finite
+ * payload" (volume.py:142-143); BD3MG_EIO: open/read failure. */
+int bd3mg_payload_read_device(const char* path, int64_t offset, int64_t n, void* dev_out, int32_t dtype,
+                              void* stream);
+/* Append n values of dev_in to `path` as float64 (the caller wrote the header).
+ * Synchronous. */
+int bd3mg_payload_write_device(const char* path, const void* dev_in, int64_t n, int32_t dtype, void* stream);
+/* *bad_out = 1 if any of the n device values is NaN/Inf (check_volume,
+ * volume.py:87-94).  Synchronous. */
+int bd3mg_field_nonfinite(const void* dev, int64_t n, int32_t dtype, int32_t* bad_out, void* stream);
 
 #ifdef __cplusplus
 }

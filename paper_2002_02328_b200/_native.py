@@ -13,7 +13,7 @@ from pathlib import Path
 
 LIB_PATH = Path(os.environ.get("BD3MG_LIB") or Path(__file__).resolve().parent / "_lib" / "libbd3mg_b200.so")
 
-BD3MG_OK, BD3MG_EINVAL, BD3MG_ECUDA, BD3MG_EWORKSPACE, BD3MG_ENONFINITE = range(5)
+BD3MG_OK, BD3MG_EINVAL, BD3MG_ECUDA, BD3MG_EWORKSPACE, BD3MG_ENONFINITE, BD3MG_EFORMAT, BD3MG_EIO = range(7)
 BD3MG_F64, BD3MG_F32 = 0, 1
 INFO_DOUBLES = 16
 EVAL_DOUBLES = 7
@@ -32,6 +32,7 @@ EXPORTS = (
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
     "bd3mg_problem_jacobi_sweep_host",
     "bd3mg_fma_probe",
+    "bd3mg_payload_read_device", "bd3mg_payload_write_device", "bd3mg_field_nonfinite",
 )
 
 
@@ -111,6 +112,9 @@ def _load() -> C.CDLL:
     lib.bd3mg_problem_jacobi_sweep_host.argtypes = [_vp, _vp, _vp, _i64, _i64, C.POINTER(C.c_int64), C.c_int,
                                                     _vp, _vp]
     lib.bd3mg_fma_probe.argtypes = [C.c_int32, C.c_int32, C.c_int32, _vp, _dp, _vp]
+    lib.bd3mg_payload_read_device.argtypes = [C.c_char_p, _i64, _i64, _vp, C.c_int32, _vp]
+    lib.bd3mg_payload_write_device.argtypes = [C.c_char_p, _vp, _i64, C.c_int32, _vp]
+    lib.bd3mg_field_nonfinite.argtypes = [_vp, _i64, C.c_int32, C.POINTER(C.c_int32), _vp]
     return lib
 
 
@@ -126,6 +130,11 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == BD3MG_ENONFINITE:
         raise ValueError("non-finite gradient")
+    if rc == BD3MG_EFORMAT:
+        from .volume import FormatError
+        raise FormatError(msg)
+    if rc == BD3MG_EIO:
+        raise OSError(msg)
     raise NativeError(rc, msg)
 
 

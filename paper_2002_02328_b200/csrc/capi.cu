@@ -17,6 +17,7 @@
 
 #include "../../include/bd3mg_b200.h"
 #include "conv_dispatch.cuh"
+#include "errors.h"
 #include "solver.cuh"
 #include "stencil_tma.cuh"
 
@@ -804,6 +805,9 @@ Ws make_ws(void* p, size_t n) {
 
 // ---------------------------------------------------------------------------
 namespace bd3mg {
+int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+void count_launches(int n) { launched(n); }
+
 bool encode_tmap(CUtensorMap* map, const void* base, bool f64, long long nx, long long ny, long long nz, int boxw,
                  int boxh) {
   static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {

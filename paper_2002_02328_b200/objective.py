@@ -54,7 +54,11 @@ class Objective:
 
     def __post_init__(self):
         if D.is_tensor(self.y):
-            self.y = self.y.detach().to("cpu", torch.float64).numpy()
+            t = self.y.detach()
+            if t.is_cuda and t.dtype in (torch.float64, torch.float32):
+                # already resident (e.g. volume.read_volume(..., device=)): reuse it
+                self._dev[(t.dtype, t.device.index)] = t.contiguous()
+            self.y = t.to("cpu", torch.float64).numpy()
         self.y = np.ascontiguousarray(self.y, dtype=np.float64)
         if dims_of(self.y) != self.psf.dims:
             raise ValueError("observation dims do not match PSF dims")

@@ -13,10 +13,22 @@ blobs/spheres/boxes); it is the BASELINE.json generator for configs C1-C5.
 from __future__ import annotations
 
 import math
+import os
+import struct
+from contextlib import contextmanager
 from dataclasses import dataclass
 from typing import NamedTuple
 
 import numpy as np
+
+
+VOLUME_MAGIC = b"BD3MGVOL"
+FORMAT_VERSION = 1
+HEADER_BYTES = 8 + 4 + 12
+
+
+class FormatError(ValueError):
+    """A binary container violated the volume/PSF format (reference `volume.py:31-32`)."""
 
 
 class Dims3(NamedTuple):
@@ -77,6 +89,135 @@ def check_volume(vol) -> np.ndarray:
     if not np.isfinite(arr).all():
         raise ValueError("volume contains non-finite entries")
     return arr
+
+
+@contextmanager
+def _as_stream(source, mode):
+    if hasattr(source, "read") or hasattr(source, "write"):
+        yield source
+    else:
+        with open(source, mode) as fh:
+            yield fh
+
+
+def _read_exact(fh, n: int, what: str) -> bytes:
+    buf = fh.read(n)
+    if len(buf) != n:
+        raise FormatError(f"truncated {what}: expected {n} bytes, got {len(buf)}")
+    return buf
+
+
+def _read_header(fh, magic_want: bytes, version_want: int) -> tuple[int, int, int]:
+    magic = _read_exact(fh, 8, "header")
+    if magic != magic_want:
+        raise FormatError(f"bad magic {magic!r}")
+    (version,) = struct.unpack("<I", _read_exact(fh, 4, "header"))
+    if version != version_want:
+        raise FormatError(f"unsupported version {version}")
+    nx, ny, nz = struct.unpack("<III", _read_exact(fh, 12, "header"))
+    if min(nx, ny, nz) < 1:
+        raise FormatError(f"invalid dimensions ({nx}, {ny}, {nz})")
+    return nx, ny, nz
+
+
+def _payload_extent(path, offset: int, nbytes: int) -> None:
+    """Truncation / trailing-data checks of a file payload from its size
+    (the order and wording of reference `volume.py:138-141`)."""
+    have = os.stat(path).st_size - offset
+    if have < nbytes:
+        raise FormatError(f"truncated payload: expected {nbytes} bytes, got {max(have, 0)}")
+    if have > nbytes:
+        raise FormatError("payload length mismatch: trailing data")
+
+
+def _is_device_tensor(vol) -> bool:
+    return type(vol).__module__.startswith("torch") and getattr(vol, "is_cuda", False)
+
+
+def write_volume(vol, sink) -> None:
+    """BD3MGVOL container: 8-byte magic, u32 version, u32 nx/ny/nz, float64
+    payload, little-endian (reference `volume.py:104-114`).
+
+    A CUDA tensor (float64 or float32) written to a path streams straight
+    from device memory through the native payload writer; the finiteness check
+    runs on the device first, so a rejected volume creates no file."""
+    if _is_device_tensor(vol) and not (hasattr(sink, "read") or hasattr(sink, "write")):
+        from . import _native as N
+        import ctypes
+
+        if vol.dim() != 3:
+            raise ValueError(f"volume must be 3-dimensional, got shape {tuple(vol.shape)}")
+        import torch
+
+        t = vol.contiguous()
+        if t.dtype not in (torch.float64, torch.float32):
+            t = t.double()
+        dt = N.BD3MG_F64 if t.dtype == torch.float64 else N.BD3MG_F32
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+        bad = ctypes.c_int32(0)
+        with torch.cuda.device(t.device):
+            N.check(N.lib.bd3mg_field_nonfinite(t.data_ptr(), t.numel(), dt, ctypes.byref(bad), stream))
+            if bad.value:
+                raise ValueError("volume contains non-finite entries")
+            nz, ny, nx = t.shape
+            with open(sink, "wb") as fh:
+                fh.write(VOLUME_MAGIC)
+                fh.write(struct.pack("<I", FORMAT_VERSION))
+                fh.write(struct.pack("<III", nx, ny, nz))
+            N.check(N.lib.bd3mg_payload_write_device(os.fsencode(sink), t.data_ptr(), t.numel(), dt, stream))
+        return
+    arr = check_volume(vol)
+    d = dims_of(arr)
+    with _as_stream(sink, "wb") as fh:
+        fh.write(VOLUME_MAGIC)
+        fh.write(struct.pack("<I", FORMAT_VERSION))
+        fh.write(struct.pack("<III", d.nx, d.ny, d.nz))
+        fh.write(arr.astype("<f8", copy=False).tobytes())
+
+
+def read_volume(source, device=None, dtype=None):
+    """Inverse of :func:`write_volume` with the reference's distinct errors
+    for bad magic, version mismatch, truncation, trailing data and a
+    non-finite payload (reference `volume.py:124-145`).
+
+    ``device=None``: a float64 numpy array, as the reference returns.
+    ``device="cuda"`` (or a torch device) with a path: the payload streams
+    file -> pinned chunks -> device through ``bd3mg_payload_read_device`` into
+    a CUDA tensor of ``dtype`` (torch.float64 default, or torch.float32,
+    narrowed on the device after the float64 finiteness check)."""
+    if device is None:
+        with _as_stream(source, "rb") as fh:
+            nx, ny, nz = _read_header(fh, VOLUME_MAGIC, FORMAT_VERSION)
+            n = nx * ny * nz
+            payload = _read_exact(fh, 8 * n, "payload")
+            if fh.read(1):
+                raise FormatError("payload length mismatch: trailing data")
+        data = np.frombuffer(payload, dtype="<f8").astype(np.float64)
+        if not np.isfinite(data).all():
+            raise FormatError("non-finite payload")
+        return np.ascontiguousarray(data.reshape(nz, ny, nx))
+    import torch
+
+    dtype = torch.float64 if dtype is None else dtype
+    if dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"device volumes are float64 or float32, got {dtype}")
+    dev = torch.device(device)
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    if hasattr(source, "read"):  # a stream: parse on the host, then upload
+        return torch.from_numpy(read_volume(source)).to(dev).to(dtype)
+    from . import _native as N
+
+    with open(source, "rb") as fh:
+        nx, ny, nz = _read_header(fh, VOLUME_MAGIC, FORMAT_VERSION)
+    n = nx * ny * nz
+    _payload_extent(source, HEADER_BYTES, 8 * n)
+    out = torch.empty((nz, ny, nx), dtype=dtype, device=dev)
+    dt = N.BD3MG_F64 if dtype == torch.float64 else N.BD3MG_F32
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        N.check(N.lib.bd3mg_payload_read_device(os.fsencode(source), HEADER_BYTES, n, out.data_ptr(), dt, stream))
+    return out
 
 
 def philox(seed: int) -> np.random.Generator:

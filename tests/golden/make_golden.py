@@ -170,8 +170,25 @@ def c1_case(blur, objective, runtime, volume):
     return out
 
 
+def io_cases(blur, volume):
+    """Container files written by the reference's own writers
+    (volume.py:104-114, blur.py:201-211) plus the arrays they hold."""
+    d = OUT / "io"
+    d.mkdir(exist_ok=True)
+    vol = philox(41).uniform(-2.0, 3.0, (3, 4, 5))          # (nz, ny, nx)
+    volume.write_volume(vol, d / "vol_5x4x3.bd3mgvol")
+    idx = np.arange(8, dtype=np.float64).reshape(2, 2, 2)
+    volume.write_volume(idx, d / "vol_2x2x2.bd3mgvol")
+    psf = blur.generate_psf_stack(volume.Dims3(6, 5, 4), blur.KernelDims(3, 3, 5), seed=7)
+    blur.write_psf(psf, d / "psf_6x5x4_k3x3x5.bd3mgpsf")
+    np.savez_compressed(d / "io.npz", vol=vol, idx=idx, psf_kernels=psf.kernels, psf_params=psf.params)
+
+
 def main():
     blur, directions, kernels, objective, runtime, volume = load_reference()
+    if "--only-io" in sys.argv:
+        io_cases(blur, volume)
+        return
     print("reference backend:", kernels.backend_name())
     cases = {}
     cases.update(blur_cases(blur, kernels, volume))
@@ -180,6 +197,7 @@ def main():
     np.savez_compressed(OUT / "objective.npz", **{f"{c}/{k}": v for c, d in oc.items() for k, v in d.items()})
     c1 = c1_case(blur, objective, runtime, volume)
     np.savez_compressed(OUT / "c1.npz", **c1)
+    io_cases(blur, volume)
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
