@@ -278,10 +278,22 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
       for (int i = 0; i < RX; ++i) acc[s][r][i] = T(0);
 
   if (a_lo <= a_hi) issue(a_lo, 0);
+  // the epilogue operand rows of this tile are pulled into L2 two taps before
+  // the end, so the epilogue's loads do not wait on DRAM
+  constexpr bool kEpiLoad = MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC;
+  const long long orow = (long long)(zo - job.out_lo) * p.plane;
+  const bool vec_io = (p.nx % VEC) == 0;  // rows are whole 16-byte chunks
+  const int a_pf = max(a_lo, a_hi - 1);
   uint32_t phase = 0;  // bit b = parity of buffer b
   int buf = 0;
   for (int a = a_lo; a <= a_hi; ++a) {
     if (a < a_hi) issue(a + 1, buf ^ 1);
+    if constexpr (kEpiLoad) {
+      if (a == a_pf && vec_io && job.sub && threadIdx.x < Cfg::TY) {
+        const int y = y0 + threadIdx.x, w = min(Cfg::TX, p.nx - x0);
+        if (y < p.ny && w > 0) prefetch_l2_bulk(job.sub + orow + (long long)y * p.nx + x0, (uint32_t)(w * sizeof(T)));
+      }
+    }
     if (tma) {
       mbar_wait(&mbar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
@@ -331,7 +343,39 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   double part[NV > 0 ? NV : 1];
 #pragma unroll
   for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
-  const long long orow = (long long)(zo - job.out_lo) * p.plane;
+  const int xt = x0 + tx * RX;
+  // 16-byte loads / stores of the thread's RX outputs where the row allows
+  constexpr bool kVecEpi = RX == VEC && (MODE == M_STORE || MODE == M_RESID || MODE == M_GRAD);
+  const bool vec_here = kVecEpi && vec_io && xt + RX <= p.nx;
+  if constexpr (kVecEpi) {
+    if (vec_here) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const int y = y0 + ty * RY + r;
+        if (y >= p.ny) continue;
+        const long long o = orow + (long long)y * p.nx + xt;
+        T res[RX];
+        if constexpr (MODE == M_STORE) {
+#pragma unroll
+          for (int i = 0; i < RX; ++i) res[i] = acc[0][r][i];
+        } else {
+          const V q = *reinterpret_cast<const V*>(job.sub + o);
+          const T* qs = reinterpret_cast<const T*>(&q);
+#pragma unroll
+          for (int i = 0; i < RX; ++i) {
+            if constexpr (MODE == M_RESID) {
+              res[i] = sub_rn(acc[0][r][i], qs[i]);
+              part[0] += (double)res[i] * (double)res[i];
+            } else {
+              res[i] = add_rn(acc[0][r][i], qs[i]);
+            }
+          }
+        }
+        if (MODE != M_RESID || job.dst0) *reinterpret_cast<V*>(job.dst0 + o) = *reinterpret_cast<const V*>(res);
+      }
+    }
+  }
+  if (!vec_here) {
 #pragma unroll
   for (int r = 0; r < RY; ++r) {
     const int y = y0 + ty * RY + r;
@@ -367,6 +411,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
       }
     }
   }
+  }  // !vec_here
   if constexpr (NV > 0) {
     cta_reduce<NV, Cfg::NT>(part, red_s);
     if (threadIdx.x == 0) {
