@@ -518,7 +518,8 @@ template <typename T, int KY, int KX, int MODE, bool ADJ>
 __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     conv_rz2_kernel(const __grid_constant__ ConvArgs<T> p) {
   using Cfg = Rz2Cfg<T, KY, KX, MODE>;
-  constexpr int RX = Cfg::RX, RY = Cfg::RY, KS = Cfg::KS;
+  using V = typename Vec16<T>::type;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, KS = Cfg::KS, VEC = Cfg::VEC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* tiles = reinterpret_cast<T*>(sbase);
@@ -579,12 +580,24 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
       for (int i = 0; i < RX; ++i) acc[o][r][i] = T(0);
 
   if (zi_lo <= zi_hi) issue(zi_lo, 0);
+  // epilogue operand rows of both output planes pulled into L2 two planes early
+  constexpr bool kEpiLoad = MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC;
+  const bool vec_io = (p.nx % VEC) == 0;
+  const int zi_pf = max(zi_lo, zi_hi - 1);
   uint32_t phase = 0;
   int buf = 0;
   for (int zi = zi_lo; zi <= zi_hi; ++zi) {
     if (zi < zi_hi) {
       issue(zi + 1, buf ^ 1);
       stage_slices(zi + 1, buf ^ 1);  // visible after this iteration's closing barrier
+    }
+    if constexpr (kEpiLoad) {
+      if (zi == zi_pf && vec_io && job.sub && threadIdx.x < 2 * Cfg::TY) {
+        const int o = threadIdx.x / Cfg::TY, y = y0 + threadIdx.x % Cfg::TY, w = min(Cfg::TX, p.nx - x0);
+        if ((o == 0 || has1) && y < p.ny && w > 0)
+          prefetch_l2_bulk(job.sub + (long long)(zo0 + o - job.out_lo) * p.plane + (long long)y * p.nx + x0,
+                           (uint32_t)(w * sizeof(T)));
+      }
     }
     if (tma) {
       mbar_wait(&mbar[buf], (phase >> buf) & 1u);
@@ -609,10 +622,42 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   double part[NV > 0 ? NV : 1];
 #pragma unroll
   for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
+  const int xt = x0 + tx * RX;
+  constexpr bool kVecEpi = MODE == M_STORE || MODE == M_RESID || MODE == M_GRAD;
+  const bool vec_here = kVecEpi && vec_io && xt + RX <= p.nx;  // RX == VEC: one 16-byte access per row
 #pragma unroll
   for (int o = 0; o < 2; ++o) {
     if (o == 1 && !has1) break;
     const long long orow = (long long)(zo0 + o - job.out_lo) * p.plane;
+    if constexpr (kVecEpi) {
+      if (vec_here) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          const int y = y0 + ty * RY + r;
+          if (y >= p.ny) continue;
+          const long long q = orow + (long long)y * p.nx + xt;
+          T res[RX];
+          if constexpr (MODE == M_STORE) {
+#pragma unroll
+            for (int i = 0; i < RX; ++i) res[i] = acc[o][r][i];
+          } else {
+            const V v = *reinterpret_cast<const V*>(job.sub + q);
+            const T* vs = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int i = 0; i < RX; ++i) {
+              if constexpr (MODE == M_RESID) {
+                res[i] = sub_rn(acc[o][r][i], vs[i]);
+                part[0] += (double)res[i] * (double)res[i];
+              } else {
+                res[i] = add_rn(acc[o][r][i], vs[i]);
+              }
+            }
+          }
+          if (MODE != M_RESID || job.dst0) *reinterpret_cast<V*>(job.dst0 + q) = *reinterpret_cast<const V*>(res);
+        }
+        continue;
+      }
+    }
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
       const int y = y0 + ty * RY + r;
