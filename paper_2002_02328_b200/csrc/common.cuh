@@ -39,6 +39,32 @@ BD3MG_D float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 BD3MG_D double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 BD3MG_D float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
+// ---- packed fp32 pairs (FFMA2, sm_100a): two correctly rounded FMAs per
+// instruction, bitwise equal to two fmaf_rn; halves the FMA issue slots.
+BD3MG_D unsigned long long pk2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+BD3MG_D float2 unpk2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// acc + kp * v per half (v broadcast to both halves)
+BD3MG_D unsigned long long ffma2_pair(unsigned long long kp, float v, unsigned long long acc) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(kp), "l"(pk2(v, v)), "l"(acc));
+  return r;
+}
+
+// acc + k * vp per half (k broadcast)
+BD3MG_D unsigned long long ffma2_bcast(float k, unsigned long long vp, unsigned long long acc) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(vp), "l"(pk2(k, k)), "l"(acc));
+  return r;
+}
+
 // ---- deterministic CTA reduction of NV doubles --------------------------
 // Fixed shuffle tree inside each warp, then warps summed in index order by
 // thread 0.  Result valid in thread 0 only.  `scratch` needs NW*NV doubles.

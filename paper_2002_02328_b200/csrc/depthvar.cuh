@@ -120,6 +120,12 @@ BD3MG_D T omega_of(T dx, T dy, T delta2) {
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
 
+#ifndef BD3MG_FFMA2
+#define BD3MG_FFMA2 1  // packed fp32 FMAs (FFMA2) in the fp32 two-plane correlation kernel
+#endif
+#ifndef BD3MG_RZ2_RY5
+#define BD3MG_RZ2_RY5 4  // rows per thread of the two-plane kernel for 3x3 / 5x5 taps (measured: 4 >= 8 with FFMA2)
+#endif
 #ifndef BD3MG_RY1
 #define BD3MG_RY1 16  // rows per thread of the single-input modes
 #endif
@@ -437,7 +443,7 @@ struct Rz2Cfg {
   static constexpr int VEC = 16 / sizeof(T);
   // rows per thread: measured on B200 (scripts/prof_h_cfg.py) -- 8 for the
   // 5x5 taps, 4 for 7x7 / 9x9 (fewer live coefficients and a smaller body)
-  static constexpr int RX = VEC, RY = (KY <= 5) ? 8 : 4, RZ = 2;
+  static constexpr int RX = VEC, RY = (KY <= 5) ? BD3MG_RZ2_RY5 : 4, RZ = 2;
   static constexpr int WX = 32, WY = 4, NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
   static constexpr int RXH = (KX - 1) / 2, RYH = (KY - 1) / 2;
@@ -514,6 +520,37 @@ BD3MG_D void rz2_plane(const T* tb, const T* cs0, const T* cs1, T (&acc)[2][Cfg:
   }
 }
 
+// fp32 twin of rz2_plane with the two output planes packed into one FFMA2
+// lane pair: acc[r][i] = (plane zo0, plane zo0+1) of output (r, i).  The
+// input value is broadcast to both lanes and the coefficient pair (k0, k1) is
+// one aligned 64-bit load from the interleaved slices, so no register moves
+// are needed; each lane is the fmaf_rn of rz2_plane, bit for bit.
+template <typename Cfg>
+BD3MG_D void rz2_plane_pp(const float* tb, const unsigned long long* cp,
+                          unsigned long long (&acc)[Cfg::RY][Cfg::RX]) {
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, KX = Cfg::KX, KY = Cfg::KY;
+#pragma unroll
+  for (int yi = 0; yi < RY + KY - 1; ++yi) {
+    float v[Cfg::WINP];
+#pragma unroll
+    for (int j = 0; j < Cfg::WINP; j += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(tb + yi * Cfg::PITCH + j);
+      v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+    }
+#pragma unroll
+    for (int c = 0; c < KX; ++c) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const int b = yi - r;
+        if (b < 0 || b >= KY) continue;
+        const unsigned long long kp = cp[b * KX + c];
+#pragma unroll
+        for (int i = 0; i < RX; ++i) acc[r][i] = ffma2_pair(kp, v[Cfg::OFF + i + c], acc[r][i]);
+      }
+    }
+  }
+}
+
 template <typename T, int KY, int KX, int MODE, bool ADJ>
 __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     conv_rz2_kernel(const __grid_constant__ ConvArgs<T> p) {
@@ -540,6 +577,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   const int zi_lo = (int)max((long long)(zo0 - rz), job.src_z0);
   const int zi_hi = (int)min((long long)(zo0 + (has1 ? 1 : 0) + rz), job.src_z0 + job.src_nz - 1);
 
+  constexpr bool kPacked = sizeof(T) == 4 && BD3MG_FFMA2;  // FFMA2 over the plane pair
   auto stage_slices = [&](int zi, int b) {  // coefficient slices of input plane zi
     T* dst = slices + b * 2 * KS;
     for (int t = threadIdx.x; t < 2 * KS; t += Cfg::NT) {
@@ -547,7 +585,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
       const int zo = zo0 + o, a = zi - zo + rz;
       T v = T(0);
       if ((o == 0 || has1) && tap_ok(p, ADJ, zo, a)) v = coef_of<T, ADJ>(p, zo, a, e / KX, e % KX);
-      dst[t] = v;
+      dst[kPacked ? 2 * e + o : t] = v;  // packed: (k0, k1) pairs
     }
   };
   auto issue = [&](int zi, int b) {
@@ -578,6 +616,11 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     for (int r = 0; r < RY; ++r)
 #pragma unroll
       for (int i = 0; i < RX; ++i) acc[o][r][i] = T(0);
+  unsigned long long accp[RY][RX];  // packed (plane 0, plane 1) accumulators
+#pragma unroll
+  for (int r = 0; r < RY; ++r)
+#pragma unroll
+    for (int i = 0; i < RX; ++i) accp[r][i] = 0ull;
 
   if (zi_lo <= zi_hi) issue(zi_lo, 0);
   // epilogue operand rows of both output planes pulled into L2 two planes early
@@ -612,9 +655,22 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     // the instruction cache for the 7x7 / 9x9 instantiations (measured)
     const T* tb = tiles + buf * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
     const T* cs0 = slices + buf * 2 * KS;
-    rz2_plane<Cfg, T, true, true>(tb, cs0, cs0 + KS, acc);
+    if constexpr (kPacked)
+      rz2_plane_pp<Cfg>(reinterpret_cast<const float*>(tb), reinterpret_cast<const unsigned long long*>(cs0), accp);
+    else
+      rz2_plane<Cfg, T, true, true>(tb, cs0, cs0 + KS, acc);
     __syncthreads();
     buf ^= 1;
+  }
+  if constexpr (kPacked) {
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int i = 0; i < RX; ++i) {
+        const float2 f = unpk2(accp[r][i]);
+        acc[0][r][i] = (T)f.x;
+        acc[1][r][i] = (T)f.y;
+      }
   }
 
   // ---- epilogue (both output planes) --------------------------------------
