@@ -441,8 +441,8 @@ template <typename T, int KY_, int KX_, int MODE>
 struct Rz2Cfg {
   static constexpr int KY = KY_, KX = KX_;
   static constexpr int VEC = 16 / sizeof(T);
-  // rows per thread: measured on B200 (scripts/prof_h_cfg.py) -- 8 for the
-  // 5x5 taps, 4 for 7x7 / 9x9 (fewer live coefficients and a smaller body)
+  // rows per thread: measured on B200 (scripts/prof_h_cfg.py, scripts/cmp_h.sh)
+  // -- 4 (BD3MG_RZ2_RY5) for 3x3 / 5x5 taps, 4 for 7x7 / 9x9
   static constexpr int RX = VEC, RY = (KY <= 5) ? BD3MG_RZ2_RY5 : 4, RZ = 2;
   static constexpr int WX = 32, WY = 4, NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
