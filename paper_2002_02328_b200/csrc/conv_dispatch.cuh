@@ -31,7 +31,8 @@ inline bool conv_rz2(int ky, int kx, int mode) {
     return e ? atoi(e) : -1;
   }();
   const bool want = env < 0 ? (sizeof(T) == 4) : env != 0;
-  return want && conv_tiled_shape(ky, kx) && mode != M_GRAM2;
+  // the dual-input (Gram) variant exists as the fp32 packed-pair kernel only
+  return want && conv_tiled_shape(ky, kx) && (mode != M_GRAM2 || (sizeof(T) == 4 && BD3MG_FFMA2));
 }
 
 // grid.z units of a job with `nout` output planes
@@ -111,6 +112,13 @@ cudaError_t launch_rz2(ConvArgs<T>& p, int total_work, cudaStream_t s) {
                  getenv("BD3MG_NO_TMA") == nullptr;
   }
   const size_t sm = Cfg::smem_bytes(p.kz);
+  if constexpr (Cfg::NIN == 2) {
+    for (int j = 0; j < p.njobs; ++j) {
+      ConvJob<T>& jb = p.jobs[j];
+      jb.use_tma = jb.use_tma &&
+                   encode_tmap(&jb.tmap1, jb.src1, sizeof(T) == 8, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH);
+    }
+  }
   auto kern = conv_rz2_kernel<T, K, K, MODE, ADJ>;
   cudaError_t e = ensure_smem_attr(kern, sm);
   if (e != cudaSuccess) return e;
@@ -135,6 +143,17 @@ template <typename T, int MODE, bool ADJ>
 cudaError_t launch_mode(ConvArgs<T>& p, int total_work, cudaStream_t s) {
   if (p.ky == p.kx) {
     if constexpr (MODE == M_GRAM2) {
+      if constexpr (sizeof(T) == 4 && BD3MG_FFMA2) {
+        if (conv_rz2<T>(p.ky, p.kx, MODE)) {
+          switch (p.ky) {
+            case 3: return launch_rz2<T, 3, MODE, ADJ>(p, total_work, s);
+            case 5: return launch_rz2<T, 5, MODE, ADJ>(p, total_work, s);
+            case 7: return launch_rz2<T, 7, MODE, ADJ>(p, total_work, s);
+            case 9: return launch_rz2<T, 9, MODE, ADJ>(p, total_work, s);
+            default: break;
+          }
+        }
+      }
       switch (p.ky) {
         case 3: return launch_tiled<T, 3, MODE, ADJ>(p, total_work, s);
         case 5: return launch_tiled<T, 5, MODE, ADJ>(p, total_work, s);

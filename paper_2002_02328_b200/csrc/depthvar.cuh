@@ -457,12 +457,12 @@ struct Rz2Cfg {
   static constexpr int BOX = BOXH * PITCH;
   static constexpr int TILE = (BOX + 128 / (int)sizeof(T) - 1) / (128 / (int)sizeof(T)) * (128 / (int)sizeof(T));
   static constexpr size_t TILE_BYTES = (size_t)TILE * sizeof(T), BOX_BYTES = (size_t)BOX * sizeof(T);
-  static constexpr int NIN = 1;
+  static constexpr int NIN = (MODE == M_GRAM2) ? 2 : 1;  // dual input: fp32 packed path only
   static constexpr int NV = ModeNV<MODE>::value;
   static constexpr int KS = KY * KX;                       // one tap slice
   static constexpr size_t SLICE_BYTES = ((size_t)2 * 2 * KS * sizeof(T) + 127) & ~size_t(127);
   static size_t smem_bytes(int) {
-    return 2 * TILE_BYTES + SLICE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
+    return 2 * NIN * TILE_BYTES + SLICE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
   }
 };
 
@@ -525,18 +525,22 @@ BD3MG_D void rz2_plane(const T* tb, const T* cs0, const T* cs1, T (&acc)[2][Cfg:
 // input value is broadcast to both lanes and the coefficient pair (k0, k1) is
 // one aligned 64-bit load from the interleaved slices, so no register moves
 // are needed; each lane is the fmaf_rn of rz2_plane, bit for bit.
+// With two inputs (Gram mode) both share the coefficient pair:
+// acc[s][r][i] is input s's (plane zo0, plane zo0+1) pair.
 template <typename Cfg>
 BD3MG_D void rz2_plane_pp(const float* tb, const unsigned long long* cp,
-                          unsigned long long (&acc)[Cfg::RY][Cfg::RX]) {
-  constexpr int RX = Cfg::RX, RY = Cfg::RY, KX = Cfg::KX, KY = Cfg::KY;
+                          unsigned long long (&acc)[Cfg::NIN][Cfg::RY][Cfg::RX]) {
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, KX = Cfg::KX, KY = Cfg::KY, NIN = Cfg::NIN;
 #pragma unroll
   for (int yi = 0; yi < RY + KY - 1; ++yi) {
-    float v[Cfg::WINP];
+    float v[NIN][Cfg::WINP];
 #pragma unroll
-    for (int j = 0; j < Cfg::WINP; j += 4) {
-      const float4 q = *reinterpret_cast<const float4*>(tb + yi * Cfg::PITCH + j);
-      v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
-    }
+    for (int s = 0; s < NIN; ++s)
+#pragma unroll
+      for (int j = 0; j < Cfg::WINP; j += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(tb + s * Cfg::TILE + yi * Cfg::PITCH + j);
+        v[s][j] = q.x; v[s][j + 1] = q.y; v[s][j + 2] = q.z; v[s][j + 3] = q.w;
+      }
 #pragma unroll
     for (int c = 0; c < KX; ++c) {
 #pragma unroll
@@ -545,7 +549,9 @@ BD3MG_D void rz2_plane_pp(const float* tb, const unsigned long long* cp,
         if (b < 0 || b >= KY) continue;
         const unsigned long long kp = cp[b * KX + c];
 #pragma unroll
-        for (int i = 0; i < RX; ++i) acc[r][i] = ffma2_pair(kp, v[Cfg::OFF + i + c], acc[r][i]);
+        for (int s = 0; s < NIN; ++s)
+#pragma unroll
+          for (int i = 0; i < RX; ++i) acc[s][r][i] = ffma2_pair(kp, v[s][Cfg::OFF + i + c], acc[s][r][i]);
       }
     }
   }
@@ -556,12 +562,12 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     conv_rz2_kernel(const __grid_constant__ ConvArgs<T> p) {
   using Cfg = Rz2Cfg<T, KY, KX, MODE>;
   using V = typename Vec16<T>::type;
-  constexpr int RX = Cfg::RX, RY = Cfg::RY, KS = Cfg::KS, VEC = Cfg::VEC;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, KS = Cfg::KS, VEC = Cfg::VEC, NIN = Cfg::NIN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  T* tiles = reinterpret_cast<T*>(sbase);
-  T* slices = reinterpret_cast<T*>(sbase + 2 * Cfg::TILE_BYTES);  // [buf][out][KS]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * Cfg::TILE_BYTES + Cfg::SLICE_BYTES);
+  T* tiles = reinterpret_cast<T*>(sbase);  // [buf][input][TILE]
+  T* slices = reinterpret_cast<T*>(sbase + 2 * NIN * Cfg::TILE_BYTES);  // [buf][out][KS]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::SLICE_BYTES);
   double* red_s = reinterpret_cast<double*>(mbar + 2);
 
   const int zidx = blockIdx.z;
@@ -578,6 +584,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   const int zi_hi = (int)min((long long)(zo0 + (has1 ? 1 : 0) + rz), job.src_z0 + job.src_nz - 1);
 
   constexpr bool kPacked = sizeof(T) == 4 && BD3MG_FFMA2;  // FFMA2 over the plane pair
+  static_assert(NIN == 1 || kPacked, "dual-input two-plane kernel is the fp32 packed path");
   auto stage_slices = [&](int zi, int b) {  // coefficient slices of input plane zi
     T* dst = slices + b * 2 * KS;
     for (int t = threadIdx.x; t < 2 * KS; t += Cfg::NT) {
@@ -589,14 +596,18 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     }
   };
   auto issue = [&](int zi, int b) {
-    T* dst = tiles + b * Cfg::TILE;
+    T* dst = tiles + b * NIN * Cfg::TILE;
     if (tma) {
       if (threadIdx.x == 0) {
-        mbar_expect_tx(&mbar[b], (uint32_t)Cfg::BOX_BYTES);
+        mbar_expect_tx(&mbar[b], (uint32_t)(NIN * Cfg::BOX_BYTES));
         tma_load_3d(dst, &job.tmap0, x0 - Cfg::RXA, y0 - Cfg::RYH, (int)(zi - job.src_z0), &mbar[b]);
+        if constexpr (NIN == 2)
+          tma_load_3d(dst + Cfg::TILE, &job.tmap1, x0 - Cfg::RXA, y0 - Cfg::RYH, (int)(zi - job.src_z0), &mbar[b]);
       }
     } else {
       stage_tile_fallback<Cfg>(dst, job.src0, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
+      if constexpr (NIN == 2)
+        stage_tile_fallback<Cfg>(dst + Cfg::TILE, job.src1, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
       cp_async_commit();
     }
   };
@@ -616,11 +627,14 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     for (int r = 0; r < RY; ++r)
 #pragma unroll
       for (int i = 0; i < RX; ++i) acc[o][r][i] = T(0);
-  unsigned long long accp[RY][RX];  // packed (plane 0, plane 1) accumulators
+  T acc1[2][RY][RX];                     // input 1 (Gram mode), filled from the packed pairs
+  unsigned long long accp[NIN][RY][RX];  // packed (plane 0, plane 1) accumulators per input
 #pragma unroll
-  for (int r = 0; r < RY; ++r)
+  for (int s2 = 0; s2 < NIN; ++s2)
 #pragma unroll
-    for (int i = 0; i < RX; ++i) accp[r][i] = 0ull;
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+      for (int i = 0; i < RX; ++i) accp[s2][r][i] = 0ull;
 
   if (zi_lo <= zi_hi) issue(zi_lo, 0);
   // epilogue operand rows of both output planes pulled into L2 two planes early
@@ -653,7 +667,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     // one code body for both outputs (invalid taps have zero coefficients:
     // exact no-ops for finite inputs); three specialised bodies overflow
     // the instruction cache for the 7x7 / 9x9 instantiations (measured)
-    const T* tb = tiles + buf * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
+    const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
     const T* cs0 = slices + buf * 2 * KS;
     if constexpr (kPacked)
       rz2_plane_pp<Cfg>(reinterpret_cast<const float*>(tb), reinterpret_cast<const unsigned long long*>(cs0), accp);
@@ -667,9 +681,14 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     for (int r = 0; r < RY; ++r)
 #pragma unroll
       for (int i = 0; i < RX; ++i) {
-        const float2 f = unpk2(accp[r][i]);
+        const float2 f = unpk2(accp[0][r][i]);
         acc[0][r][i] = (T)f.x;
         acc[1][r][i] = (T)f.y;
+        if constexpr (NIN == 2) {
+          const float2 h = unpk2(accp[NIN - 1][r][i]);
+          acc1[0][r][i] = (T)h.x;
+          acc1[1][r][i] = (T)h.y;
+        }
       }
   }
 
@@ -735,6 +754,11 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
         } else if constexpr (MODE == M_GRAM1) {
           if (job.dst0) job.dst0[q] = a0;
           part[0] += (double)a0 * (double)a0;
+        } else if constexpr (MODE == M_GRAM2) {
+          const T a1 = acc1[o][r][i];
+          part[0] += (double)a0 * (double)a0;
+          part[1] += (double)a0 * (double)a1;
+          part[2] += (double)a1 * (double)a1;
         } else if constexpr (MODE == M_GRAMC) {
           const double c0 = (double)job.sub[q];
           job.dst0[q] = a0;
