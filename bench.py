@@ -346,7 +346,8 @@ def main():
     if not args.quick:
         extra["e2e"] = e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng)
     if not args.quick and rank == 0 and world == 1:
-        extra["variants"] = {"hd-cache": variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush)}
+        extra["variants"] = {"hd-cache": variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush),
+                             "separable-psf": variant_separable(obj, dtype, torch)}
         extra["cpu_baseline"] = cpu_baseline(cfg)
 
     if rank == 0:
@@ -391,6 +392,42 @@ def variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush):
     fl = blur.flops_jacobi_sweep(cfg.dims, cfg.kdims, eng.blocks, hd_cache=True)
     return {"value": args.steps * eng.nblocks / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
             "correlation_flops_per_step": fl, "achieved_tflops": fl / (ms / args.steps / 1e3) / 1e12}
+
+
+def variant_separable(obj, dtype, torch):
+    """Secondary number: full-volume H / H^T through
+    the separable-PSF fast path (rank-one factors of the BASELINE Gaussians),
+    against HBM: algorithmic bytes = every plane read once + written once."""
+    from paper_2002_02328_b200 import separable
+    try:
+        sep = separable.SeparableStack.from_psf(obj.psf)
+    except ValueError as exc:
+        return {"unavailable": str(exc)}
+    x = torch.rand(obj.dims.shape, dtype=dtype, device="cuda")
+    out = torch.empty_like(x)
+    nz = obj.dims.nz
+    nbytes = separable.bytes_H(obj.dims, x.element_size())
+    try:
+        peak = json.load(open(ROOT / "MEASURED_PEAKS.json"))["hbm_gbs"]
+        src = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"
+    except (OSError, KeyError, ValueError):
+        peak, src = 7700.0, "nominal B200 HBM3e (MEASURED_PEAKS.json absent)"
+    res = {"bound": "hbm", "peak_gbs": peak, "peak_source": src, "algorithmic_bytes_per_launch": nbytes}
+    for adj in (False, True):
+        for _ in range(3):
+            sep.correlate_rows(x, 0, 0, nz - 1, adjoint=adj, out=out)
+        reps = 20
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(reps):
+            sep.correlate_rows(x, 0, 0, nz - 1, adjoint=adj, out=out)
+        e.record()
+        torch.cuda.synchronize()
+        t = s.elapsed_time(e) / reps / 1e3
+        res["Ht" if adj else "H"] = {"ms": t * 1e3, "gvox_s": obj.dims.count / t / 1e9, "gbs": nbytes / t / 1e9,
+                                     "frac": nbytes / t / 1e9 / peak}
+    return res
 
 
 def roofline(obj, cfg, dtype, torch, N, D, blur):

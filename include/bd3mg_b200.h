@@ -248,6 +248,22 @@ int bd3mg_payload_write_device(const char* path, const void* dev_in, int64_t n, 
  * volume.py:87-94).  Synchronous. */
 int bd3mg_field_nonfinite(const void* dev, int64_t n, int32_t dtype, int32_t* bad_out, void* stream);
 
+/* ---- separable-PSF fast path ----
+ * For stacks whose every plane is rank one, K[zo] = u[zo] (x) v[zo] (x) w[zo]
+ * (u: (nzk, kz) depth factors, v: (nzk, ky), w: (nzk, kx); ky == kx in
+ * {3,5,7,9}): H rows (adjoint = 0) or H^T rows (adjoint = 1) with the
+ * contract of bd3mg_depthvar_correlate[_adjoint] (_core.pyx:17-96), in
+ * kz + ky + kx FMAs per voxel.  Results agree with the dense path to
+ * rounding (different summation order); the dense kernels stay the default.
+ * Memory-bound: report against HBM, not the FMA roofline. */
+int bd3mg_sep_correlate_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx, const double* u,
+                            const double* v, const double* w, int64_t nzk, int64_t kz, int64_t ky, int64_t kx,
+                            int64_t frag_z0, int64_t out_lo, int64_t out_hi, double* out, int32_t adjoint,
+                            void* stream);
+int bd3mg_sep_correlate_f32(const float* frag, int64_t nzf, int64_t ny, int64_t nx, const float* u, const float* v,
+                            const float* w, int64_t nzk, int64_t kz, int64_t ky, int64_t kx, int64_t frag_z0,
+                            int64_t out_lo, int64_t out_hi, float* out, int32_t adjoint, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

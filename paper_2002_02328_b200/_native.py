@@ -33,6 +33,7 @@ EXPORTS = (
     "bd3mg_problem_jacobi_sweep_host",
     "bd3mg_fma_probe",
     "bd3mg_payload_read_device", "bd3mg_payload_write_device", "bd3mg_field_nonfinite",
+    "bd3mg_sep_correlate_f64", "bd3mg_sep_correlate_f32",
 )
 
 
@@ -115,6 +116,9 @@ def _load() -> C.CDLL:
     lib.bd3mg_payload_read_device.argtypes = [C.c_char_p, _i64, _i64, _vp, C.c_int32, _vp]
     lib.bd3mg_payload_write_device.argtypes = [C.c_char_p, _vp, _i64, C.c_int32, _vp]
     lib.bd3mg_field_nonfinite.argtypes = [_vp, _i64, C.c_int32, C.POINTER(C.c_int32), _vp]
+    for name in ("bd3mg_sep_correlate_f64", "bd3mg_sep_correlate_f32"):
+        getattr(lib, name).argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                                       _i64, _vp, C.c_int32, _vp]
     return lib
 
 
