@@ -11,18 +11,20 @@
 //   H^T v[zi] = sum_a u_zo[a] S_zo(v[zo]),  zo = zi+rz-a,
 //   S_zo(f)(y, x) = sum_b v_zo[b] sum_c w_zo[c] f(y+ry-b, x+rx-c)  (_core.pyx:56-96)
 //
-// applies each plane's flipped 2-D filter once and combines in depth.  Both
-// are memory-bound (one plane read + one plane written per output plane),
-// so they are measured against HBM, never against the FMA roofline.  The
+// filters each plane once and combines in depth.  Both are memory-bound, so
+// they are measured against HBM, never against the FMA roofline.  The
 // summation order differs from the dense kernels (rounding-level, <= 1e-12
-// relative in fp64); the factors are detected at upload (blur.py side) and
+// relative in fp64); the factors are detected at upload (separable.py) and
 // the dense graded kernel stays the default everywhere.
 //
-// One CTA owns a 32 x 16 tile and marches a chunk of output planes in depth.
-// Forward: a ring of kz+1 halo tiles of x (TMA, mbarrier per slot) feeds the
-// depth combination t (tile + halo, smem), then an x pass and a y pass.
-// Adjoint: each input plane is filtered once into a ring of kz filtered
-// tiles, and every output plane is a kz-term depth combination of the ring.
+// Two streaming passes through one temporary volume (stream-ordered
+// allocation):
+//   sep_z_kernel   depth FIR, one thread per 16-byte pixel vector, the kz
+//                  source planes of consecutive outputs hit L1;
+//   sep_xy_kernel  per-plane separable 2-D filter, 64 x 32 tile + halo in
+//                  shared memory, x pass then y pass.
+// Forward = z then xy; adjoint = flipped xy then z.  HBM traffic per launch:
+// four volume passes (read src, write tmp, read tmp, write out).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -32,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "../../include/bd3mg_b200.h"
@@ -39,263 +42,136 @@
 #include "errors.h"
 
 namespace bd3mg {
-bool encode_tmap(CUtensorMap* map, const void* base, bool f64, long long nx, long long ny, long long nz, int boxw,
-                 int boxh);
-
 namespace {
 
-constexpr int kSx = 32, kSy = 16, kSNT = 128;
-constexpr int kChunk = 16;  // output planes marched per CTA
-
-constexpr int sgcd(int a, int b) { return b == 0 ? a : sgcd(b, a % b); }
-
-template <typename T, int K>
-struct SepGeo {
-  static constexpr int VEC = 16 / (int)sizeof(T);
-  static constexpr int R = (K - 1) / 2;
-  static constexpr int RXA = (R + VEC - 1) / VEC * VEC, OFF = RXA - R;
-  // staged plane tile: x in [x0-RXA, x0+32+R), y in [y0-R, y0+16+R)
-  static constexpr int BW = (kSx + RXA + R + 2 * VEC - 1) / (2 * VEC) * (2 * VEC);
-  static constexpr int ROWQ = 128 / sgcd(BW * (int)sizeof(T), 128);
-  static constexpr int TH = kSy + 2 * R, TW = kSx + 2 * R;
-  static constexpr int BH = (TH + ROWQ - 1) / ROWQ * ROWQ;
-  static constexpr int PL = BW * BH;
-};
-
-struct SepArgs {
-  const void* src;   // fragment, plane 0 = depth src_z0
-  const void* u;     // (nzk, kz) depth factors
-  const void* v;     // (nzk, ky)
-  const void* w;     // (nzk, kx)
-  void* out;         // rows out_lo .. out_hi
-  long long plane;
-  int nx, ny, nzk, kz, src_z0, src_nz, out_lo, out_hi;
-  int use_tma;
-};
+constexpr int kZNT = 256;    // depth-FIR threads
+constexpr int kZChunk = 16;  // output planes per depth-FIR thread
+constexpr int kXx = 64, kXy = 32, kXNT = 256;
 
 template <typename T>
-BD3MG_D void stage_plane_fallback(T* dst, const T* src, long long plane, int zrel, int x0, int y0, int nx, int ny,
-                                  int bw, int bh, int rxa, int r) {
-  const T* base = src + (long long)zrel * plane;
-  for (int i = threadIdx.x; i < bw * bh; i += kSNT) {
-    const int row = i / bw, col = i - row * bw;
-    const int gy = y0 - r + row, gx = x0 - rxa + col;
-    const bool ok = gy >= 0 && gy < ny && gx >= 0 && gx < nx;
-    cp_async<sizeof(T)>(dst + i, ok ? base + (long long)gy * nx + gx : src, ok);
+struct Vec16;
+template <>
+struct Vec16<double> {
+  using type = double2;
+};
+template <>
+struct Vec16<float> {
+  using type = float4;
+};
+
+// Depth FIR.  Forward: dst[zo] = sum_a u[zo][a] src[zo+a-rz] over the source
+// planes present; adjoint: dst[zi] = sum_a u[zo][a] src[zo], zo = zi+rz-a.
+// src plane 0 = depth s_z0 (s_n planes); dst plane 0 = depth d_lo.
+struct SepZArgs {
+  const void* src;
+  void* dst;
+  const void* u;
+  long long plane;
+  int kz, nzk, s_z0, s_n, d_lo, d_hi;
+};
+
+// KZ > 0: taps unrolled at compile time (all kz source loads of an output
+// issue back to back; absent planes are predicated off); KZ == 0: runtime kz.
+template <typename T, bool ADJ, int KZ>
+__global__ void __launch_bounds__(kZNT) sep_z_kernel(const __grid_constant__ SepZArgs p) {
+  using V = typename Vec16<T>::type;
+  constexpr int VEC = 16 / (int)sizeof(T);
+  const long long q = ((long long)blockIdx.x * kZNT + threadIdx.x) * VEC;
+  if (q >= p.plane) return;
+  // 16-byte accesses need every plane to start on a 16-byte boundary
+  const bool full = q + VEC <= p.plane && p.plane % VEC == 0;
+  const int z_a = p.d_lo + blockIdx.y * kZChunk, z_b = min(z_a + kZChunk - 1, p.d_hi);
+  const int kz = KZ > 0 ? KZ : p.kz;
+  const int rz = (kz - 1) / 2;
+  const T* src = static_cast<const T*>(p.src);
+  const T* u = static_cast<const T*>(p.u);
+  T* dst = static_cast<T*>(p.dst);
+  // source planes present (adjoint: and inside the stack)
+  const int s_lo = ADJ ? max(p.s_z0, 0) : p.s_z0;
+  const int s_hi = ADJ ? min(p.s_z0 + p.s_n - 1, p.nzk - 1) : p.s_z0 + p.s_n - 1;
+  for (int z = z_a; z <= z_b; ++z) {
+    T acc[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[i] = T(0);
+    auto tap = [&](int a) {
+      const int zs = ADJ ? z + rz - a : z + a - rz;
+      if (zs < s_lo || zs > s_hi) return;
+      const T c = __ldg(u + (long long)(ADJ ? zs : z) * kz + a);
+      const T* sp = src + (long long)(zs - p.s_z0) * p.plane + q;
+      if (full) {
+        const V v = __ldg(reinterpret_cast<const V*>(sp));
+        const T* vs = reinterpret_cast<const T*>(&v);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] = fma_rn(c, vs[i], acc[i]);
+      } else {
+        for (int i = 0; i < VEC && q + i < p.plane; ++i) acc[i] = fma_rn(c, sp[i], acc[i]);
+      }
+    };
+    if constexpr (KZ > 0) {
+#pragma unroll
+      for (int a = 0; a < KZ; ++a) tap(a);
+    } else {
+      for (int a = 0; a < kz; ++a) tap(a);
+    }
+    T* dp = dst + (long long)(z - p.d_lo) * p.plane + q;
+    if (full) {
+      *reinterpret_cast<V*>(dp) = *reinterpret_cast<const V*>(acc);
+    } else {
+      for (int i = 0; i < VEC && q + i < p.plane; ++i) dp[i] = acc[i];
+    }
   }
 }
 
-// ---------------------------------------------------------------------------
-template <typename T, int K>
-__global__ void __launch_bounds__(kSNT) sep_forward_kernel(const __grid_constant__ SepArgs p,
-                                                           const __grid_constant__ CUtensorMap tm) {
-  using G = SepGeo<T, K>;
-  constexpr int R = G::R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  const int ring = p.kz + 1;
-  T* rs = reinterpret_cast<T*>(base);                       // [ring][PL]
-  T* tb = rs + (size_t)ring * G::PL;                         // [TH][TW]
-  T* rb = tb + G::TH * G::TW;                                // [TH][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rb + G::TH * kSx + 1);
-  bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
+// Per-plane separable 2-D filter of rows [r_lo, r_hi] (global depths; src and
+// dst plane 0 = depth z0 each).  FLIP: the adjoint's flipped taps.
+struct SepXYArgs {
+  const void* src;
+  void* dst;
+  const void* v;
+  const void* w;
+  long long plane;
+  int nx, ny, s_z0, d_z0, r_lo;
+};
 
-  const int x0 = blockIdx.x * kSx, y0 = blockIdx.y * kSy;
-  const int zo_a = p.out_lo + blockIdx.z * kChunk, zo_b = min(zo_a + kChunk - 1, p.out_hi);
-  const int rz = (p.kz - 1) / 2;
-  const T* src = static_cast<const T*>(p.src);
-  // input planes of the chunk inside the fragment
-  const int zi_a = max(zo_a - rz, p.src_z0), zi_b = min(zo_b + rz, p.src_z0 + p.src_nz - 1);
-  const bool tma = p.use_tma != 0;
-  if (tma && threadIdx.x == 0) {
-    for (int s = 0; s < ring; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
+template <typename T, int K, bool FLIP>
+__global__ void __launch_bounds__(kXNT) sep_xy_kernel(const __grid_constant__ SepXYArgs p) {
+  constexpr int R = (K - 1) / 2;
+  constexpr int TW = kXx + 2 * R, TH = kXy + 2 * R;
+  __shared__ T ts[TH][TW + 1];
+  __shared__ T rs[TH][kXx + 1];
+  const int z = p.r_lo + blockIdx.z;
+  const int x0 = blockIdx.x * kXx, y0 = blockIdx.y * kXy;
+  const T* src = static_cast<const T*>(p.src) + (long long)(z - p.s_z0) * p.plane;
+  T* dst = static_cast<T*>(p.dst) + (long long)(z - p.d_z0) * p.plane;
+  for (int i = threadIdx.x; i < TH * TW; i += kXNT) {
+    const int r = i / TW, c = i - r * TW;
+    const int y = y0 - R + r, x = x0 - R + c;
+    ts[r][c] = (y >= 0 && y < p.ny && x >= 0 && x < p.nx) ? src[(long long)y * p.nx + x] : T(0);
+  }
+  T wk[K], vk[K];
+  const T* wz = static_cast<const T*>(p.w) + (long long)z * K;
+  const T* vz = static_cast<const T*>(p.v) + (long long)z * K;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    wk[c] = __ldg(wz + (FLIP ? K - 1 - c : c));
+    vk[c] = __ldg(vz + (FLIP ? K - 1 - c : c));
   }
   __syncthreads();
-  auto slot = [&](int zi) { return (zi - zi_a) % ring; };
-  auto phase = [&](int zi) { return (uint32_t)((zi - zi_a) / ring) & 1u; };
-  auto issue = [&](int zi) {
-    T* dst = rs + (size_t)slot(zi) * G::PL;
-    if (tma) {
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(&bars[slot(zi)], G::PL * sizeof(T));
-        tma_load_3d(dst, &tm, x0 - G::RXA, y0 - R, zi - p.src_z0, &bars[slot(zi)]);
-      }
-    } else {
-      stage_plane_fallback<T>(dst, src, p.plane, zi - p.src_z0, x0, y0, p.nx, p.ny, G::BW, G::BH, G::RXA, R);
-      cp_async_commit();
-    }
-  };
-  // keep kz planes resident plus one in flight
-  int issued = zi_a - 1;
-  auto ensure = [&](int upto) {  // planes <= upto issued (ring permitting)
-    while (issued < min(upto, zi_b)) issue(++issued);
-  };
-  ensure(zo_a + rz + 1);
-  int waited = zi_a - 1;
-  for (int zo = zo_a; zo <= zo_b; ++zo) {
-    // the slot of plane zo+rz+1 last held zo-rz-1, released by the previous
-    // iteration's closing barrier
-    ensure(zo + rz + 1);
-    const int need = min(zo + rz, zi_b);
-    if (tma) {
-      while (waited < need) {
-        ++waited;
-        mbar_wait(&bars[slot(waited)], phase(waited));
-      }
-    } else {
-      cp_async_wait<0>();
-      __syncthreads();
-      waited = need;
-    }
-    const T* uz = static_cast<const T*>(p.u) + (long long)zo * p.kz;
-    const T* vz = static_cast<const T*>(p.v) + (long long)zo * K;
-    const T* wz = static_cast<const T*>(p.w) + (long long)zo * K;
-    // (1) depth combination over the tile + halo
-    const int a_lo = max(0, zi_a - zo + rz), a_hi = min(p.kz - 1, zi_b - zo + rz);
-    for (int i = threadIdx.x; i < G::TH * G::TW; i += kSNT) {
-      const int r = i / G::TW, c = i - r * G::TW;
-      const int si = r * G::BW + c + G::OFF;
-      T t = T(0);
-      for (int a = a_lo; a <= a_hi; ++a) t = fma_rn(__ldg(uz + a), rs[(size_t)slot(zo + a - rz) * G::PL + si], t);
-      tb[i] = t;
-    }
-    __syncthreads();
-    // (2) x pass
-    T wk[K], vk[K];
+  for (int i = threadIdx.x; i < TH * kXx; i += kXNT) {
+    const int r = i / kXx, c = i - r * kXx;
+    T s = T(0);
 #pragma unroll
-    for (int c = 0; c < K; ++c) wk[c] = __ldg(wz + c);
-#pragma unroll
-    for (int b = 0; b < K; ++b) vk[b] = __ldg(vz + b);
-    for (int i = threadIdx.x; i < G::TH * kSx; i += kSNT) {
-      const int r = i / kSx, c = i - r * kSx;
-      T s = T(0);
-#pragma unroll
-      for (int cc = 0; cc < K; ++cc) s = fma_rn(wk[cc], tb[r * G::TW + c + cc], s);
-      rb[i] = s;
-    }
-    __syncthreads();
-    // (3) y pass + store
-    T* out = static_cast<T*>(p.out) + (long long)(zo - p.out_lo) * p.plane;
-    for (int i = threadIdx.x; i < kSy * kSx; i += kSNT) {
-      const int r = i / kSx, c = i - r * kSx;
-      const int y = y0 + r, x = x0 + c;
-      T s = T(0);
-#pragma unroll
-      for (int b = 0; b < K; ++b) s = fma_rn(vk[b], rb[(r + b) * kSx + c], s);
-      if (y < p.ny && x < p.nx) out[(long long)y * p.nx + x] = s;
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-template <typename T, int K>
-__global__ void __launch_bounds__(kSNT) sep_adjoint_kernel(const __grid_constant__ SepArgs p,
-                                                           const __grid_constant__ CUtensorMap tm) {
-  using G = SepGeo<T, K>;
-  constexpr int R = G::R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  T* fs = reinterpret_cast<T*>(base);                        // [2][PL] staged input planes
-  T* ss = fs + 2 * G::PL;                                     // [kz][16*32] filtered planes
-  T* rb = ss + (size_t)p.kz * kSy * kSx;                      // [TH][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rb + G::TH * kSx + 1);
-  bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
-
-  const int x0 = blockIdx.x * kSx, y0 = blockIdx.y * kSy;
-  const int zi_a = p.out_lo + blockIdx.z * kChunk, zi_b = min(zi_a + kChunk - 1, p.out_hi);
-  const int rz = (p.kz - 1) / 2;
-  const T* src = static_cast<const T*>(p.src);
-  // planes zo whose filtered tile is needed: [zi_a-rz, zi_b+rz] within [0, nzk) and the fragment
-  const int zo_a = max(max(zi_a - rz, 0), p.src_z0);
-  const int zo_b = min(min(zi_b + rz, p.nzk - 1), p.src_z0 + p.src_nz - 1);
-  const bool tma = p.use_tma != 0;
-  if (tma && threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
+    for (int cc = 0; cc < K; ++cc) s = fma_rn(wk[cc], ts[r][c + cc], s);
+    rs[r][c] = s;
   }
   __syncthreads();
-  auto issue = [&](int zo) {
-    const int b = (zo - zo_a) & 1;
-    T* dst = fs + b * G::PL;
-    if (tma) {
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(&bars[b], G::PL * sizeof(T));
-        tma_load_3d(dst, &tm, x0 - G::RXA, y0 - R, zo - p.src_z0, &bars[b]);
-      }
-    } else {
-      stage_plane_fallback<T>(dst, src, p.plane, zo - p.src_z0, x0, y0, p.nx, p.ny, G::BW, G::BH, G::RXA, R);
-      cp_async_commit();
-    }
-  };
-  auto sslot = [&](int zo) { return ((zo % p.kz) + p.kz) % p.kz; };
-  if (zo_a <= zo_b) issue(zo_a);
-  int zi = zi_a;  // next output plane
-  for (int zo = zo_a; zo <= zo_b; ++zo) {
-    const int b = (zo - zo_a) & 1;
-    if (zo < zo_b) issue(zo + 1);
-    if (tma) {
-      mbar_wait(&bars[b], (uint32_t)((zo - zo_a) >> 1) & 1u);
-    } else {
-      if (zo < zo_b) cp_async_wait<1>();
-      else cp_async_wait<0>();
-      __syncthreads();
-    }
-    const T* vz = static_cast<const T*>(p.v) + (long long)zo * K;
-    const T* wz = static_cast<const T*>(p.w) + (long long)zo * K;
-    T wk[K], vk[K];
+  for (int i = threadIdx.x; i < kXy * kXx; i += kXNT) {
+    const int r = i / kXx, c = i - r * kXx;
+    const int y = y0 + r, x = x0 + c;
+    T s = T(0);
 #pragma unroll
-    for (int c = 0; c < K; ++c) wk[c] = __ldg(wz + c);
-#pragma unroll
-    for (int q = 0; q < K; ++q) vk[q] = __ldg(vz + q);
-    const T* f = fs + b * G::PL;
-    // x pass (flipped taps) over the rows y0-R .. y0+16+R
-    for (int i = threadIdx.x; i < G::TH * kSx; i += kSNT) {
-      const int r = i / kSx, c = i - r * kSx;
-      T s = T(0);
-#pragma unroll
-      for (int cc = 0; cc < K; ++cc) s = fma_rn(wk[K - 1 - cc], f[r * G::BW + c + cc + G::OFF], s);
-      rb[i] = s;
-    }
-    __syncthreads();
-    // y pass (flipped taps) into the ring slot of zo
-    T* sd = ss + (size_t)sslot(zo) * kSy * kSx;
-    for (int i = threadIdx.x; i < kSy * kSx; i += kSNT) {
-      const int r = i / kSx, c = i - r * kSx;
-      T s = T(0);
-#pragma unroll
-      for (int q = 0; q < K; ++q) s = fma_rn(vk[K - 1 - q], rb[(r + q) * kSx + c], s);
-      sd[i] = s;
-    }
-    __syncthreads();
-    // every output whose last contributing plane is now filtered
-    while (zi <= zi_b && (min(zi + rz, zo_b) <= zo)) {
-      const int a_lo = max(0, zi + rz - zo_b), a_hi = min(p.kz - 1, zi + rz - zo_a);
-      T* out = static_cast<T*>(p.out) + (long long)(zi - p.out_lo) * p.plane;
-      for (int i = threadIdx.x; i < kSy * kSx; i += kSNT) {
-        const int r = i / kSx, c = i - r * kSx;
-        const int y = y0 + r, x = x0 + c;
-        T s = T(0);
-        for (int a = a_lo; a <= a_hi; ++a) {
-          const int z = zi + rz - a;
-          s = fma_rn(__ldg(static_cast<const T*>(p.u) + (long long)z * p.kz + a),
-                     ss[(size_t)sslot(z) * kSy * kSx + i], s);
-        }
-        if (y < p.ny && x < p.nx) out[(long long)y * p.nx + x] = s;
-      }
-      ++zi;
-    }
-    __syncthreads();  // staged slot b is refilled two planes later; ring slots reused after kz planes
-  }
-  // outputs with no contributing plane inside the fragment are zero
-  for (; zi <= zi_b; ++zi) {
-    T* out = static_cast<T*>(p.out) + (long long)(zi - p.out_lo) * p.plane;
-    for (int i = threadIdx.x; i < kSy * kSx; i += kSNT) {
-      const int y = y0 + i / kSx, x = x0 + i % kSx;
-      if (y < p.ny && x < p.nx) out[(long long)y * p.nx + x] = T(0);
-    }
+    for (int b = 0; b < K; ++b) s = fma_rn(vk[b], rs[r + b][c], s);
+    if (y < p.ny && x < p.nx) dst[(long long)y * p.nx + x] = s;
   }
 }
 
@@ -310,27 +186,104 @@ int errf(int code, const char* fmt, ...) {
 }
 
 template <typename T, int K>
-int launch_sep(SepArgs& a, bool adj, cudaStream_t s) {
-  using G = SepGeo<T, K>;
-  static const bool no_tma = getenv("BD3MG_NO_TMA") != nullptr;
-  CUtensorMap tm;
-  memset(&tm, 0, sizeof(tm));
-  a.use_tma = !no_tma && encode_tmap(&tm, a.src, sizeof(T) == 8, a.nx, a.ny, a.src_nz, G::BW, G::BH);
-  size_t smem;
-  if (!adj)
-    smem = 128 + ((size_t)(a.kz + 1) * G::PL + G::TH * G::TW + G::TH * kSx + 2) * sizeof(T) + (a.kz + 2) * 8;
+int launch_xy(SepXYArgs& a, int nrows, bool flip, cudaStream_t s) {
+  if (nrows <= 0) return BD3MG_OK;
+  dim3 grid((a.nx + kXx - 1) / kXx, (a.ny + kXy - 1) / kXy, nrows);
+  if (flip)
+    sep_xy_kernel<T, K, true><<<grid, kXNT, 0, s>>>(a);
   else
-    smem = 128 + ((size_t)2 * G::PL + (size_t)a.kz * kSy * kSx + G::TH * kSx + 2) * sizeof(T) + 4 * 8;
-  if (smem > 227 * 1024) return errf(BD3MG_EINVAL, "separable path: kz=%d does not fit shared memory", a.kz);
-  auto kern = adj ? sep_adjoint_kernel<T, K> : sep_forward_kernel<T, K>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
-  const int nout = a.out_hi - a.out_lo + 1;
-  dim3 grid((a.nx + kSx - 1) / kSx, (a.ny + kSy - 1) / kSy, (nout + kChunk - 1) / kChunk);
-  kern<<<grid, kSNT, smem, s>>>(a, tm);
+    sep_xy_kernel<T, K, false><<<grid, kXNT, 0, s>>>(a);
   count_launches(1);
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+}
+
+template <typename T>
+int launch_z(SepZArgs& a, bool adj, cudaStream_t s) {
+  const int n = a.d_hi - a.d_lo + 1;
+  if (n <= 0) return BD3MG_OK;
+  constexpr int VEC = 16 / (int)sizeof(T);
+  const long long vecs = (a.plane + VEC - 1) / VEC;
+  dim3 grid((unsigned)((vecs + kZNT - 1) / kZNT), (n + kZChunk - 1) / kZChunk);
+  switch (a.kz) {
+#define BD3MG_SEPZ(KZ)                                                  \
+  case KZ:                                                              \
+    if (adj)                                                            \
+      sep_z_kernel<T, true, KZ><<<grid, kZNT, 0, s>>>(a);               \
+    else                                                                \
+      sep_z_kernel<T, false, KZ><<<grid, kZNT, 0, s>>>(a);              \
+    break;
+    BD3MG_SEPZ(3) BD3MG_SEPZ(5) BD3MG_SEPZ(7) BD3MG_SEPZ(9) BD3MG_SEPZ(11) BD3MG_SEPZ(13) BD3MG_SEPZ(15)
+    BD3MG_SEPZ(17) BD3MG_SEPZ(19) BD3MG_SEPZ(21)
+#undef BD3MG_SEPZ
+    default:
+      if (adj)
+        sep_z_kernel<T, true, 0><<<grid, kZNT, 0, s>>>(a);
+      else
+        sep_z_kernel<T, false, 0><<<grid, kZNT, 0, s>>>(a);
+  }
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+}
+
+// Scratch volume per (device, stream), grow-only (a cudaMallocAsync per call
+// re-maps the pool when its release threshold is 0: measured 10x slower).
+int scratch(cudaStream_t s, size_t bytes, void** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& ent = cache[{dev, s}];
+  if (ent.second < bytes) {
+    if (ent.first) {
+      cudaStreamSynchronize(s);
+      cudaFree(ent.first);
+      ent = {nullptr, 0};
+    }
+    e = cudaMalloc(&ent.first, bytes);
+    if (e != cudaSuccess) return errf(BD3MG_ECUDA, "separable scratch (%zu bytes): %s", bytes, cudaGetErrorString(e));
+    ent.second = bytes;
+  }
+  *out = ent.first;
+  return BD3MG_OK;
+}
+
+template <typename T, int K>
+int run_sep(const T* frag, int nzf, int ny, int nx, const T* u, const T* v, const T* w, int nzk, int kz, int frag_z0,
+            int out_lo, int out_hi, T* out, bool adj, cudaStream_t s) {
+  const long long plane = (long long)ny * nx;
+  const int rz = (kz - 1) / 2;
+  if (!adj) {
+    // t rows = output rows
+    const int n = out_hi - out_lo + 1;
+    T* t = nullptr;
+    int rc = scratch(s, (size_t)n * plane * sizeof(T), (void**)&t);
+    if (rc) return rc;
+    SepZArgs za{frag, t, u, plane, kz, nzk, frag_z0, nzf, out_lo, out_hi};
+    rc = launch_z<T>(za, false, s);
+    SepXYArgs xa{t, out, v, w, plane, nx, ny, out_lo, out_lo, out_lo};
+    if (!rc) rc = launch_xy<T, K>(xa, n, false, s);
+    return rc;
+  }
+  // adjoint: filtered planes zo in [out_lo-rz, out_hi+rz] within the stack and the fragment
+  const int s_lo = std::max(std::max(out_lo - rz, 0), frag_z0);
+  const int s_hi = std::min(std::min(out_hi + rz, nzk - 1), frag_z0 + nzf - 1);
+  const int ns = s_hi - s_lo + 1;
+  if (ns <= 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, (size_t)(out_hi - out_lo + 1) * plane * sizeof(T), s);
+    return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+  }
+  T* sb = nullptr;
+  int rc = scratch(s, (size_t)ns * plane * sizeof(T), (void**)&sb);
+  if (rc) return rc;
+  SepXYArgs xa{frag, sb, v, w, plane, nx, ny, frag_z0, s_lo, s_lo};
+  rc = launch_xy<T, K>(xa, ns, true, s);
+  SepZArgs za{sb, out, u, plane, kz, nzk, s_lo, ns, out_lo, out_hi};
+  if (!rc) rc = launch_z<T>(za, true, s);
+  return rc;
 }
 
 template <typename T>
@@ -343,18 +296,15 @@ int sep_correlate(const T* frag, int64_t nzf, int64_t ny, int64_t nx, const T* u
   if (out_lo < 0 || out_hi < out_lo || out_hi >= nzk)
     return errf(BD3MG_EINVAL, "output rows [%lld, %lld] outside the kernel stack of %lld planes", (long long)out_lo,
                 (long long)out_hi, (long long)nzk);
-  SepArgs a;
-  memset(&a, 0, sizeof(a));
-  a.src = frag; a.u = u; a.v = v; a.w = w; a.out = out;
-  a.plane = ny * nx; a.nx = (int)nx; a.ny = (int)ny; a.nzk = (int)nzk; a.kz = (int)kz;
-  a.src_z0 = (int)frag_z0; a.src_nz = (int)nzf; a.out_lo = (int)out_lo; a.out_hi = (int)out_hi;
   cudaStream_t s = (cudaStream_t)stream;
   const bool adj = adjoint != 0;
+  const int a0 = (int)nzf, a1 = (int)ny, a2 = (int)nx, a3 = (int)nzk, a4 = (int)kz, a5 = (int)frag_z0;
+  const int a6 = (int)out_lo, a7 = (int)out_hi;
   switch (ky) {
-    case 3: return launch_sep<T, 3>(a, adj, s);
-    case 5: return launch_sep<T, 5>(a, adj, s);
-    case 7: return launch_sep<T, 7>(a, adj, s);
-    case 9: return launch_sep<T, 9>(a, adj, s);
+    case 3: return run_sep<T, 3>(frag, a0, a1, a2, u, v, w, a3, a4, a5, a6, a7, out, adj, s);
+    case 5: return run_sep<T, 5>(frag, a0, a1, a2, u, v, w, a3, a4, a5, a6, a7, out, adj, s);
+    case 7: return run_sep<T, 7>(frag, a0, a1, a2, u, v, w, a3, a4, a5, a6, a7, out, adj, s);
+    case 9: return run_sep<T, 9>(frag, a0, a1, a2, u, v, w, a3, a4, a5, a6, a7, out, adj, s);
     default: return errf(BD3MG_EINVAL, "separable path: ky = kx = %lld not instantiated (3/5/7/9)", (long long)ky);
   }
 }
