@@ -1137,6 +1137,9 @@ struct DevBuf {
 };
 }  // namespace
 
+constexpr int kPipeMax = 8;     // groups of the pipelined host sweep (upper bound)
+constexpr int kPipeGroups = 4;  // default, measured: e2e 5970 (2), 6260 (3), 6266 (4) block-it/s at C2
+
 struct bd3mg_problem {
   bd3mg_geom_t g;
   bd3mg_reg_t r;
@@ -1145,6 +1148,11 @@ struct bd3mg_problem {
   DevBuf K, y, stage, slab, dmem, inc, info, ws, terms;
   DevBuf dmem_res;          // device-resident memory store (sweep with dmem == NULL)
   int64_t dmem_res_z0 = -1, dmem_res_n = 0;
+  // pipelined host sweep: copy streams, per-group fragments / workspaces, events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_piece[kPipeMax] = {};
+  DevBuf frag[kPipeMax], gws[kPipeMax];
 };
 
 static int download_f64(bd3mg_problem* p, const DevBuf& src, size_t n, double* host) {
@@ -1206,6 +1214,15 @@ int bd3mg_problem_destroy(bd3mg_problem* p) {
   if (!p) return BD3MG_OK;
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->s);
+  for (cudaStream_t t : {p->s_in, p->s_out})
+    if (t) {
+      cudaStreamSynchronize(t);
+      cudaStreamDestroy(t);
+    }
+  for (cudaEvent_t e : p->ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_piece)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(p->s);
   delete p;
   return BD3MG_OK;
@@ -1254,12 +1271,127 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
   return BD3MG_OK;
 }
 
+// Session-mode sweep of the whole volume with the PCIe transfers overlapped.
+// The blocks split into G depth-contiguous groups.  x arrives piece by piece
+// on a copy stream (group g's support first); group g's fragment takes the
+// planes it shares with group g-1 by a D2D copy from g-1's fragment before
+// g-1 updates them.  Group g's sweep runs while later pieces are in flight,
+// and each group's updated rows go back to the host (second copy stream)
+// while the next groups compute.  Every group is a bd3mg_jacobi_sweep over
+// the same anchor, so the iterate is bitwise that of one sweep over all
+// blocks; the recorder terms are the sums of the groups' (every term, f
+// included, is a sum over rows).
+static int pipelined_session_sweep(bd3mg_problem* p, double* x, const int64_t* blocks, int nblocks,
+                                   double* terms_out, double* info_out) {
+  const bd3mg_geom_t* g = &p->g;
+  const int64_t nz = g->nz, plane = g->ny * g->nx, kz = g->kz;
+  static const int env_groups = [] {
+    const char* e = getenv("BD3MG_PIPELINE_GROUPS");
+    return e ? atoi(e) : 0;
+  }();
+  const int G = std::max(2, std::min(env_groups > 0 ? env_groups : kPipeGroups, std::min(nblocks / 2, kPipeMax)));
+  int first[kPipeMax + 1];
+  for (int q = 0; q <= G; ++q) first[q] = (int)((long long)nblocks * q / G);
+  int64_t lo[kPipeMax], hi[kPipeMax], z0[kPipeMax], need[kPipeMax];
+  for (int q = 0; q < G; ++q) {
+    lo[q] = blocks[2 * first[q]];
+    hi[q] = blocks[2 * first[q + 1] - 1];
+    z0[q] = std::max<int64_t>(0, lo[q] - kz);
+    need[q] = std::min(nz - 1, hi[q] + kz);
+  }
+  if (!p->s_in) {
+    CU(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    for (auto& e : p->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : p->ev_piece) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (p->dmem_res_z0 != 0 || p->dmem_res_n != nz) {
+    CU(p->dmem_res.reserve((size_t)nz * plane * 8));
+    CU(cudaMemsetAsync(p->dmem_res.p, 0, (size_t)nz * plane * 8, p->s));
+    p->dmem_res_z0 = 0;
+    p->dmem_res_n = nz;
+  }
+  for (int q = 0; q < G; ++q) {
+    CU(p->frag[q].reserve((size_t)(need[q] - z0[q] + 1) * plane * 8));
+    CU(p->gws[q].reserve(0));
+  }
+  CU(p->info.reserve((size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double)));
+  CU(p->terms.reserve((size_t)G * BD3MG_EVAL_DOUBLES * sizeof(double)));
+  auto fr = [&](int q) { return (double*)p->frag[q].p; };
+  // (1) pieces of x, each into the first group that needs them
+  CU(cudaEventRecord(p->ev[3], p->s));  // the previous call's use of the buffers is ordered on s
+  CU(cudaStreamWaitEvent(p->s_in, p->ev[3], 0));
+  int64_t have = -1;  // last plane shipped
+  for (int q = 0; q < G; ++q) {
+    if (need[q] > have) {
+      CU(cudaMemcpyAsync(fr(q) + (have + 1 - z0[q]) * plane, x + (have + 1) * plane,
+                         (size_t)(need[q] - have) * plane * 8, cudaMemcpyHostToDevice, p->s_in));
+      have = need[q];
+    }
+    CU(cudaEventRecord(p->ev_piece[q], p->s_in));
+  }
+  auto sweep = [&](int q) -> int {
+    bd3mg_sweep_t sw;
+    memset(&sw, 0, sizeof(sw));
+    sw.x = fr(q); sw.dmem = (double*)p->dmem_res.p + z0[q] * plane; sw.frag_z0 = z0[q]; sw.nzf = need[q] - z0[q] + 1;
+    sw.blocks = blocks + 2 * first[q]; sw.nblocks = first[q + 1] - first[q];
+    sw.rec_lo = lo[q]; sw.rec_hi = hi[q]; sw.snap = nullptr;
+    const size_t wsb = bd3mg_jacobi_sweep_ws_bytes(g, &sw);
+    if (wsb == (size_t)-1) return BD3MG_EINVAL;
+    CU(p->gws[q].reserve(wsb));
+    return bd3mg_jacobi_sweep(g, &p->r, p->K.p, p->y.p, &sw, (double*)p->terms.p + q * BD3MG_EVAL_DOUBLES,
+                              (double*)p->info.p + (size_t)first[q] * BD3MG_INFO_DOUBLES, p->gws[q].p, wsb, p->s);
+  };
+  for (int q = 0; q < G; ++q) {
+    CU(cudaStreamWaitEvent(p->s, p->ev_piece[q], 0));
+    // planes group q+1 shares with q, before q's sweep updates them
+    if (q + 1 < G) {
+      const int64_t a = z0[q + 1], b = std::min(need[q], need[q + 1]);
+      if (b >= a)
+        CU(cudaMemcpyAsync(fr(q + 1), fr(q) + (a - z0[q]) * plane, (size_t)(b - a + 1) * plane * 8,
+                           cudaMemcpyDeviceToDevice, p->s));
+    }
+    int rc = sweep(q);
+    if (rc) return rc;
+    // group q's rows back to the host while the later groups compute
+    CU(cudaEventRecord(p->ev[2], p->s));
+    CU(cudaStreamWaitEvent(p->s_out, p->ev[2], 0));
+    CU(cudaMemcpyAsync(x + lo[q] * plane, fr(q) + (lo[q] - z0[q]) * plane, (size_t)(hi[q] - lo[q] + 1) * plane * 8,
+                       cudaMemcpyDeviceToHost, p->s_out));
+  }
+  std::vector<double> info((size_t)nblocks * BD3MG_INFO_DOUBLES), terms((size_t)G * BD3MG_EVAL_DOUBLES);
+  CU(cudaMemcpyAsync(info.data(), p->info.p, info.size() * sizeof(double), cudaMemcpyDeviceToHost, p->s));
+  CU(cudaMemcpyAsync(terms.data(), p->terms.p, terms.size() * sizeof(double), cudaMemcpyDeviceToHost, p->s));
+  CU(cudaStreamSynchronize(p->s));
+  CU(cudaStreamSynchronize(p->s_out));
+  if (terms_out)
+    for (int i = 0; i < BD3MG_EVAL_DOUBLES; ++i) {
+      double t = 0.0;
+      for (int q = 0; q < G; ++q) t += terms[(size_t)q * BD3MG_EVAL_DOUBLES + i];
+      terms_out[i] = t;
+    }
+  if (info_out) memcpy(info_out, info.data(), info.size() * sizeof(double));
+  for (int b = 0; b < nblocks; ++b)
+    if (info[(size_t)b * BD3MG_INFO_DOUBLES + 8] != 0.0) return fail(BD3MG_ENONFINITE, "non-finite gradient");
+  return BD3MG_OK;
+}
+
 int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, int64_t frag_z0, int64_t nzf,
                                     const int64_t* blocks, int nblocks, double* terms_out, double* info_out) {
   if (!p || !x || !blocks || nblocks < 1) return fail(BD3MG_EINVAL, "null argument");
   CU(cudaSetDevice(p->device));
   const bd3mg_geom_t* g = &p->g;
   if (frag_z0 < 0 || nzf < 1 || frag_z0 + nzf > g->nz) return fail(BD3MG_EINVAL, "invalid fragment");
+  {
+    // pipelined path: session mode, fp64, whole volume, >= 4 depth-ordered back-to-back blocks
+    bool ok = !dmem && g->dtype == BD3MG_F64 && frag_z0 == 0 && nzf == g->nz && nblocks >= 4 &&
+              getenv("BD3MG_NO_PIPELINE") == nullptr && blocks[0] >= 0 && blocks[2 * nblocks - 1] < g->nz;
+    for (int b = 0; ok && b < nblocks; ++b) {
+      ok = blocks[2 * b] <= blocks[2 * b + 1];
+      if (b > 0) ok = ok && blocks[2 * b] == blocks[2 * b - 1] + 1;
+    }
+    if (ok) return pipelined_session_sweep(p, x, blocks, nblocks, terms_out, info_out);
+  }
   const size_t n = (size_t)nzf * g->ny * g->nx;
   const size_t esz = g->dtype == BD3MG_F64 ? 8 : 4;
   int64_t rec_lo = blocks[0], rec_hi = blocks[1];

@@ -81,3 +81,32 @@ def test_host_sweep_session_mode(c1obj):
         hp.jacobi_sweep(x, None, eng.blocks)
     assert np.array_equal(x, eng.x.cpu().numpy())
     hp.close()
+
+
+@pytest.mark.parametrize("h", [5, 8, 3])
+def test_pipelined_session_sweep_bitwise(h):
+    """>= 4 back-to-back blocks over the whole volume take the pipelined host
+    path (two halves, transfers overlapped): iterate bitwise that of the
+    device sweep, recorder terms equal to rounding; BD3MG_NO_PIPELINE=1 path
+    agrees."""
+    from paper_2002_02328_b200 import blur, objective, runtime
+    from paper_2002_02328_b200.host import HostProblem
+    from paper_2002_02328_b200.volume import Dims3
+    dims = Dims3(64, 48, 40)
+    psf = blur.depth_variant_stack(dims, (5, 5, 11), (0.8, 2.0), (1.5, 2.5))
+    rng = np.random.Generator(np.random.Philox(11))
+    y = rng.uniform(0, 1, dims.shape)
+    x0 = rng.uniform(0, 1, dims.shape)
+    obj = objective.Objective(psf, y, objective.RegParams(lam=1e-2, eta=1e-1, kappa=0.05, delta=1e-2))
+    eng = runtime.JacobiSweeper(obj, x0, h, torch.float64)
+    assert eng.nblocks >= 4
+    hp = HostProblem(obj)
+    x = x0.copy()
+    terms = np.zeros(7)
+    for _ in range(3):
+        eng.sweep()
+        hp.jacobi_sweep(x, None, eng.blocks, terms=terms)
+        ref = eng.terms.cpu().numpy()
+        np.testing.assert_allclose(terms[:5], ref[:5], rtol=1e-13)
+    assert np.array_equal(x, eng.x.cpu().numpy())
+    hp.close()
