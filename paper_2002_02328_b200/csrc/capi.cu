@@ -1153,6 +1153,11 @@ struct bd3mg_problem {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_piece[kPipeMax] = {};
   DevBuf frag[kPipeMax], gws[kPipeMax];
+  double* info_h = nullptr;   // pinned: per-block records of the last pipelined sweep
+  double* terms_h = nullptr;  // pinned: per-group recorder terms
+  cudaGraphExec_t graph = nullptr;
+  std::vector<int64_t> graph_key;
+  int graph_groups = 0;
 };
 
 static int download_f64(bd3mg_problem* p, const DevBuf& src, size_t n, double* host) {
@@ -1223,6 +1228,9 @@ int bd3mg_problem_destroy(bd3mg_problem* p) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_piece)
     if (e) cudaEventDestroy(e);
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  if (p->info_h) cudaFreeHost(p->info_h);
+  if (p->terms_h) cudaFreeHost(p->terms_h);
   cudaStreamDestroy(p->s);
   delete p;
   return BD3MG_OK;
@@ -1281,8 +1289,7 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
 // the same anchor, so the iterate is bitwise that of one sweep over all
 // blocks; the recorder terms are the sums of the groups' (every term, f
 // included, is a sum over rows).
-static int pipelined_session_sweep(bd3mg_problem* p, double* x, const int64_t* blocks, int nblocks,
-                                   double* terms_out, double* info_out) {
+static int pipeline_enqueue(bd3mg_problem* p, double* x, const int64_t* blocks, int nblocks, int* groups_out) {
   const bd3mg_geom_t* g = &p->g;
   const int64_t nz = g->nz, plane = g->ny * g->nx, kz = g->kz;
   static const int env_groups = [] {
@@ -1359,18 +1366,73 @@ static int pipelined_session_sweep(bd3mg_problem* p, double* x, const int64_t* b
     CU(cudaMemcpyAsync(x + lo[q] * plane, fr(q) + (lo[q] - z0[q]) * plane, (size_t)(hi[q] - lo[q] + 1) * plane * 8,
                        cudaMemcpyDeviceToHost, p->s_out));
   }
-  std::vector<double> info((size_t)nblocks * BD3MG_INFO_DOUBLES), terms((size_t)G * BD3MG_EVAL_DOUBLES);
-  CU(cudaMemcpyAsync(info.data(), p->info.p, info.size() * sizeof(double), cudaMemcpyDeviceToHost, p->s));
-  CU(cudaMemcpyAsync(terms.data(), p->terms.p, terms.size() * sizeof(double), cudaMemcpyDeviceToHost, p->s));
+  // per-group records into pinned host memory; join the copy streams back into s
+  CU(cudaMemcpyAsync(p->info_h, p->info.p, (size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double),
+                     cudaMemcpyDeviceToHost, p->s));
+  CU(cudaMemcpyAsync(p->terms_h, p->terms.p, (size_t)G * BD3MG_EVAL_DOUBLES * sizeof(double), cudaMemcpyDeviceToHost,
+                     p->s));
+  CU(cudaEventRecord(p->ev[0], p->s_in));
+  CU(cudaStreamWaitEvent(p->s, p->ev[0], 0));
+  CU(cudaEventRecord(p->ev[1], p->s_out));
+  CU(cudaStreamWaitEvent(p->s, p->ev[1], 0));
+  *groups_out = G;
+  return BD3MG_OK;
+}
+
+// The enqueued work of one call is captured once per (host x, blocks) key and
+// replayed as one CUDA graph: the ~20 launches per group and the copies cost
+// one cudaGraphLaunch (measured: the host launch cost was exposed between the
+// overlapped copies).  Capture needs page-locked x (pageable copies are not
+// capturable); other calls run the same work eagerly.
+static int pipelined_session_sweep(bd3mg_problem* p, double* x, const int64_t* blocks, int nblocks,
+                                   double* terms_out, double* info_out) {
+  if (!p->info_h) {
+    CU(cudaHostAlloc((void**)&p->info_h, (size_t)kMaxJobs * BD3MG_INFO_DOUBLES * sizeof(double),
+                     cudaHostAllocDefault));
+    CU(cudaHostAlloc((void**)&p->terms_h, (size_t)kPipeMax * BD3MG_EVAL_DOUBLES * sizeof(double),
+                     cudaHostAllocDefault));
+  }
+  if (nblocks > kMaxJobs) return fail(BD3MG_EINVAL, "at most %d blocks per sweep", kMaxJobs);
+  std::vector<int64_t> key(blocks, blocks + 2 * nblocks);
+  key.push_back((int64_t)(uintptr_t)x);
+  int G = 0;
+  if (p->graph && key == p->graph_key) {
+    CU(cudaGraphLaunch(p->graph, p->s));
+    G = p->graph_groups;
+  } else {
+    int rc = pipeline_enqueue(p, x, blocks, nblocks, &G);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(p->s));
+    cudaPointerAttributes attr;
+    const bool pinned = cudaPointerGetAttributes(&attr, x) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    if (pinned && getenv("BD3MG_NO_GRAPH") == nullptr) {  // capture for the next calls with this key
+      if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+      }
+      cudaGraph_t gr = nullptr;
+      CU(cudaStreamBeginCapture(p->s, cudaStreamCaptureModeThreadLocal));
+      int g2 = 0;
+      rc = pipeline_enqueue(p, x, blocks, nblocks, &g2);
+      cudaError_t e = cudaStreamEndCapture(p->s, &gr);
+      if (rc) return rc;
+      CU(e);
+      e = cudaGraphInstantiate(&p->graph, gr, 0);
+      cudaGraphDestroy(gr);
+      CU(e);
+      p->graph_key = key;
+      p->graph_groups = g2;
+    }
+  }
   CU(cudaStreamSynchronize(p->s));
-  CU(cudaStreamSynchronize(p->s_out));
+  const double* info = p->info_h;
   if (terms_out)
     for (int i = 0; i < BD3MG_EVAL_DOUBLES; ++i) {
       double t = 0.0;
-      for (int q = 0; q < G; ++q) t += terms[(size_t)q * BD3MG_EVAL_DOUBLES + i];
+      for (int q = 0; q < G; ++q) t += p->terms_h[(size_t)q * BD3MG_EVAL_DOUBLES + i];
       terms_out[i] = t;
     }
-  if (info_out) memcpy(info_out, info.data(), info.size() * sizeof(double));
+  if (info_out) memcpy(info_out, info, (size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double));
   for (int b = 0; b < nblocks; ++b)
     if (info[(size_t)b * BD3MG_INFO_DOUBLES + 8] != 0.0) return fail(BD3MG_ENONFINITE, "non-finite gradient");
   return BD3MG_OK;
@@ -1391,6 +1453,12 @@ int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, i
       if (b > 0) ok = ok && blocks[2 * b] == blocks[2 * b - 1] + 1;
     }
     if (ok) return pipelined_session_sweep(p, x, blocks, nblocks, terms_out, info_out);
+  }
+  if (p->graph) {  // this path may reallocate buffers the captured pipeline refers to
+    CU(cudaStreamSynchronize(p->s));
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+    p->graph_key.clear();
   }
   const size_t n = (size_t)nzf * g->ny * g->nx;
   const size_t esz = g->dtype == BD3MG_F64 ? 8 : 4;
