@@ -1296,7 +1296,7 @@ static int pipeline_enqueue(bd3mg_problem* p, double* x, const int64_t* blocks, 
     const char* e = getenv("BD3MG_PIPELINE_GROUPS");
     return e ? atoi(e) : 0;
   }();
-  const int G = std::max(2, std::min(env_groups > 0 ? env_groups : kPipeGroups, std::min(nblocks / 2, kPipeMax)));
+  const int G = std::max(2, std::min(env_groups > 0 ? env_groups : kPipeGroups, std::min(nblocks, kPipeMax)));
   int first[kPipeMax + 1];
   for (int q = 0; q <= G; ++q) first[q] = (int)((long long)nblocks * q / G);
   int64_t lo[kPipeMax], hi[kPipeMax], z0[kPipeMax], need[kPipeMax];
