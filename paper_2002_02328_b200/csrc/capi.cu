@@ -1312,6 +1312,8 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
 static int pipeline_enqueue(bd3mg_problem* p, double* x, const int64_t* blocks, int nblocks, int* groups_out) {
   const bd3mg_geom_t* g = &p->g;
   const int64_t nz = g->nz, plane = g->ny * g->nx, kz = g->kz;
+  const bool f32 = g->dtype == BD3MG_F32;
+  const size_t esz = f32 ? 4 : 8;
   static const int env_groups = [] {
     const char* e = getenv("BD3MG_PIPELINE_GROUPS");
     return e ? atoi(e) : 0;
@@ -1333,26 +1335,40 @@ static int pipeline_enqueue(bd3mg_problem* p, double* x, const int64_t* blocks, 
     for (auto& e : p->ev_piece) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   if (p->dmem_res_z0 != 0 || p->dmem_res_n != nz) {
-    CU(p->dmem_res.reserve((size_t)nz * plane * 8));
-    CU(cudaMemsetAsync(p->dmem_res.p, 0, (size_t)nz * plane * 8, p->s));
+    CU(p->dmem_res.reserve((size_t)nz * plane * esz));
+    CU(cudaMemsetAsync(p->dmem_res.p, 0, (size_t)nz * plane * esz, p->s));
     p->dmem_res_z0 = 0;
     p->dmem_res_n = nz;
   }
   for (int q = 0; q < G; ++q) {
-    CU(p->frag[q].reserve((size_t)(need[q] - z0[q] + 1) * plane * 8));
+    CU(p->frag[q].reserve((size_t)(need[q] - z0[q] + 1) * plane * esz));
     CU(p->gws[q].reserve(0));
   }
   CU(p->info.reserve((size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double)));
   CU(p->terms.reserve((size_t)G * BD3MG_EVAL_DOUBLES * sizeof(double)));
-  auto fr = [&](int q) { return (double*)p->frag[q].p; };
+  // fp32 problems: x crosses PCIe as float64 through a staging volume and is
+  // narrowed / widened on the device next to the copies
+  if (f32) CU(p->stage.reserve((size_t)nz * plane * 8));
+  double* stage = (double*)p->stage.p;
+  auto fr = [&](int q) { return (char*)p->frag[q].p; };  // byte pointer; element size esz
+  auto rows = [&](int q, int64_t z) { return fr(q) + (size_t)(z - z0[q]) * plane * esz; };
   // (1) pieces of x, each into the first group that needs them
   CU(cudaEventRecord(p->ev[3], p->s));  // the previous call's use of the buffers is ordered on s
   CU(cudaStreamWaitEvent(p->s_in, p->ev[3], 0));
   int64_t have = -1;  // last plane shipped
   for (int q = 0; q < G; ++q) {
     if (need[q] > have) {
-      CU(cudaMemcpyAsync(fr(q) + (have + 1 - z0[q]) * plane, x + (have + 1) * plane,
-                         (size_t)(need[q] - have) * plane * 8, cudaMemcpyHostToDevice, p->s_in));
+      const size_t n = (size_t)(need[q] - have) * plane;
+      if (!f32) {
+        CU(cudaMemcpyAsync(rows(q, have + 1), x + (have + 1) * plane, n * 8, cudaMemcpyHostToDevice, p->s_in));
+      } else {
+        CU(cudaMemcpyAsync(stage + (have + 1) * plane, x + (have + 1) * plane, n * 8, cudaMemcpyHostToDevice,
+                           p->s_in));
+        cvt_kernel_f64_to_f32<<<592, 256, 0, p->s_in>>>(stage + (have + 1) * plane, (float*)rows(q, have + 1),
+                                                        (long long)n);
+        launched();
+        CU(cudaGetLastError());
+      }
       have = need[q];
     }
     CU(cudaEventRecord(p->ev_piece[q], p->s_in));
@@ -1360,7 +1376,7 @@ static int pipeline_enqueue(bd3mg_problem* p, double* x, const int64_t* blocks, 
   auto sweep = [&](int q) -> int {
     bd3mg_sweep_t sw;
     memset(&sw, 0, sizeof(sw));
-    sw.x = fr(q); sw.dmem = (double*)p->dmem_res.p + z0[q] * plane; sw.frag_z0 = z0[q]; sw.nzf = need[q] - z0[q] + 1;
+    sw.x = fr(q); sw.dmem = (char*)p->dmem_res.p + (size_t)z0[q] * plane * esz; sw.frag_z0 = z0[q]; sw.nzf = need[q] - z0[q] + 1;
     sw.blocks = blocks + 2 * first[q]; sw.nblocks = first[q + 1] - first[q];
     sw.rec_lo = lo[q]; sw.rec_hi = hi[q]; sw.snap = nullptr;
     const size_t wsb = bd3mg_jacobi_sweep_ws_bytes(g, &sw);
@@ -1375,16 +1391,25 @@ static int pipeline_enqueue(bd3mg_problem* p, double* x, const int64_t* blocks, 
     if (q + 1 < G) {
       const int64_t a = z0[q + 1], b = std::min(need[q], need[q + 1]);
       if (b >= a)
-        CU(cudaMemcpyAsync(fr(q + 1), fr(q) + (a - z0[q]) * plane, (size_t)(b - a + 1) * plane * 8,
-                           cudaMemcpyDeviceToDevice, p->s));
+        CU(cudaMemcpyAsync(fr(q + 1), rows(q, a), (size_t)(b - a + 1) * plane * esz, cudaMemcpyDeviceToDevice,
+                           p->s));
     }
     int rc = sweep(q);
     if (rc) return rc;
     // group q's rows back to the host while the later groups compute
-    CU(cudaEventRecord(p->ev[2], p->s));
-    CU(cudaStreamWaitEvent(p->s_out, p->ev[2], 0));
-    CU(cudaMemcpyAsync(x + lo[q] * plane, fr(q) + (lo[q] - z0[q]) * plane, (size_t)(hi[q] - lo[q] + 1) * plane * 8,
-                       cudaMemcpyDeviceToHost, p->s_out));
+    const size_t nq = (size_t)(hi[q] - lo[q] + 1) * plane;
+    if (!f32) {
+      CU(cudaEventRecord(p->ev[2], p->s));
+      CU(cudaStreamWaitEvent(p->s_out, p->ev[2], 0));
+      CU(cudaMemcpyAsync(x + lo[q] * plane, rows(q, lo[q]), nq * 8, cudaMemcpyDeviceToHost, p->s_out));
+    } else {
+      cvt_kernel_f32_to_f64<<<592, 256, 0, p->s>>>((const float*)rows(q, lo[q]), stage + lo[q] * plane, (long long)nq);
+      launched();
+      CU(cudaGetLastError());
+      CU(cudaEventRecord(p->ev[2], p->s));
+      CU(cudaStreamWaitEvent(p->s_out, p->ev[2], 0));
+      CU(cudaMemcpyAsync(x + lo[q] * plane, stage + lo[q] * plane, nq * 8, cudaMemcpyDeviceToHost, p->s_out));
+    }
   }
   // per-group records into pinned host memory; join the copy streams back into s
   CU(cudaMemcpyAsync(p->info_h, p->info.p, (size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double),
@@ -1466,7 +1491,7 @@ int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, i
   if (frag_z0 < 0 || nzf < 1 || frag_z0 + nzf > g->nz) return fail(BD3MG_EINVAL, "invalid fragment");
   {
     // pipelined path: session mode, fp64, whole volume, >= 4 depth-ordered back-to-back blocks
-    bool ok = !dmem && g->dtype == BD3MG_F64 && frag_z0 == 0 && nzf == g->nz && nblocks >= 4 &&
+    bool ok = !dmem && frag_z0 == 0 && nzf == g->nz && nblocks >= 4 &&
               getenv("BD3MG_NO_PIPELINE") == nullptr && blocks[0] >= 0 && blocks[2 * nblocks - 1] < g->nz;
     for (int b = 0; ok && b < nblocks; ++b) {
       ok = blocks[2 * b] <= blocks[2 * b + 1];
