@@ -245,6 +245,25 @@ def _config_dict(cfg, world):
             "regulariser": {"lam": cfg.lam, "eta": cfg.eta, "kappa": cfg.kappa, "delta": cfg.delta}}
 
 
+def _load_until(eng, clocks, target, world, dist, torch, limit_s=5.0):
+    """Untimed sweeps in rounds of 20 until the clock sampler has `target`
+    samples (or `limit_s` passed).  With N ranks the stop decision is an
+    all-reduce, so every rank runs the same number of sweeps (each sweep
+    exchanges halos: unequal counts would leave P2P operations unmatched)."""
+    t_end = time.time() + limit_s
+    while True:
+        for _ in range(20):
+            eng.sweep()
+        torch.cuda.synchronize()
+        done = clocks.count() >= target or time.time() >= t_end
+        if world > 1:
+            f = torch.tensor([1.0 if done else 0.0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(f, op=dist.ReduceOp.MIN)
+            done = float(f.item()) > 0.0
+        if done:
+            return
+
+
 # ---------------------------------------------------------------------------
 def main():
     args = parse()
@@ -296,11 +315,7 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks.start()
-    t_end = time.time() + 5.0
-    while clocks.count() < 2 and time.time() < t_end:  # load the GPU until sampling runs (untimed)
-        for _ in range(20):
-            eng.sweep()
-        torch.cuda.synchronize()
+    _load_until(eng, clocks, 2, world, dist, torch)  # load the GPU until sampling runs (untimed)
     n_before = clocks.count()
     if world > 1:
         dist.barrier()
@@ -313,11 +328,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t_end = time.time() + 5.0
-    while clocks.count() < n_before + 3 and time.time() < t_end:  # keep loading until samples bracket it
-        for _ in range(20):
-            eng.sweep()
-        torch.cuda.synchronize()
+    _load_until(eng, clocks, n_before + 3, world, dist, torch)  # keep loading until samples bracket it
     clk = clocks.stop()
     clk["window"] = "samples from 2 before to 3 after the timed region, GPU kept under the same sweep load"
     eng.check()
