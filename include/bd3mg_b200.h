@@ -157,7 +157,10 @@ int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void
  * the forward-only Gram.  `y` must satisfy: y + z*ny*nx is observation row z
  * for every row the tasks touch (a shard may pass its local rows shifted).  Tasks sharing one anchor fragment compute the
  * residual H x - y once over the union of their rows (block-Jacobi cycle of
- * run_bp3mg_barrier, runtime.py:244-292).  info_out: device, ntasks*16. */
+ * run_bp3mg_barrier, runtime.py:244-292).  info_out: device, ntasks*16.
+ * Tasks run in launches of 32; calls with in-place updates (x_rows) are
+ * limited to 32 tasks (BD3MG_EINVAL otherwise) so that no launch moves the
+ * anchor of the next -- pass inc_out and apply with bd3mg_apply_increment. */
 size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks);
 int bd3mg_mg_steps(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
                    const bd3mg_task_t* tasks, int ntasks, double* info_out, void* ws, size_t ws_bytes,

@@ -16,6 +16,7 @@ LIB_PATH = Path(os.environ.get("BD3MG_LIB") or Path(__file__).resolve().parent /
 BD3MG_OK, BD3MG_EINVAL, BD3MG_ECUDA, BD3MG_EWORKSPACE, BD3MG_ENONFINITE, BD3MG_EFORMAT, BD3MG_EIO = range(7)
 BD3MG_F64, BD3MG_F32 = 0, 1
 INFO_DOUBLES = 16
+MAX_TASKS_IN_PLACE = 32  # bd3mg_mg_steps: in-place calls are one launch of <= 32 tasks
 EVAL_DOUBLES = 7
 
 # every symbol the header declares (checked by tests/test_capi_symbols.py)

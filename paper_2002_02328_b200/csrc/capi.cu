@@ -684,6 +684,12 @@ template <typename T>
 int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
                   int ntasks, double* info_out, Ws& ws, cudaStream_t s) {
   if (ntasks < 0) return fail(BD3MG_EINVAL, "negative task count");
+  // tasks run in launches of kMaxJobs; an in-place update of one launch would
+  // move the anchor of the next, so in-place calls are limited to one launch
+  if (ntasks > kMaxJobs)
+    for (int t = 0; t < ntasks; ++t)
+      if (tasks[t].x_rows)
+        return fail(BD3MG_EINVAL, "in-place updates (x_rows) need at most %d tasks per call", kMaxJobs);
   size_t peak = 0;
   for (int t0 = 0; t0 < ntasks; t0 += kMaxJobs) {
     const int nt = std::min(kMaxJobs, ntasks - t0);

@@ -276,7 +276,9 @@ def run_bp3mg_barrier(obj: Objective, x0, cfg: RunConfig, truth=None, x_star=Non
         # the shared anchor is the full iterate (it covers every slab)
         anchored = [scheduler.TaskMessage(t.worker_id, t.block, scheduler.SliceBlock(0, state.dims.nz - 1),
                                           x_full, t.d_mem, t.issue_k) for t in tasks]
-        fused_in_place = (_fused(cfg.method) and C == nblocks
+        # in place only when the whole cycle is one launch (<= 32 tasks): with
+        # more, an in-place launch would move the anchor of the next one
+        fused_in_place = (_fused(cfg.method) and C == nblocks and C <= N.MAX_TASKS_IN_PLACE
                           and (cfg.max_updates is None or state.k + C <= cfg.max_updates))
         if _fused(cfg.method):
             if fused_in_place:
