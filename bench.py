@@ -10,8 +10,11 @@ receive_update each) and the per-sweep recorder pass (f(x) + stop norms).
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 N>1 is launched by torchrun (one rank per GPU): the z-slabs of the volume are
-split into contiguous block ranges per rank with kz-plane halos exchanged
-over NCCL each sweep (paper_2002_02328_b200/distributed.py).  Rank 0 prints
+split into contiguous block ranges per rank with kz-plane halos: by default
+the update kernel stores each neighbour's halo rows straight into its inbox
+over NVLink (cudaIpc-mapped, double-buffered across the per-sweep recorder
+all-reduce); ``--halo nccl`` exchanges them with grouped ncclSend/Recv
+(paper_2002_02328_b200/distributed.py).  Rank 0 prints
 ONE JSON line.  ``--impl reference`` times the reference's CPU
 implementation of the same sweep on the host cores (oracle port driving the
 reference's own compiled _core, oracle/_ref), rank 0 only.
@@ -61,6 +64,9 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip e2e / cpu baseline / roofline (profiling runs)")
     ap.add_argument("--strong", action="store_true",
                     help="N>1: split the N=1 volume over the ranks (default: weak scaling, the config per GPU)")
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 block-Jacobi halo transport: update-kernel NVLink stores into the neighbours' "
+                         "inboxes (default) or a grouped ncclSend/Recv per sweep")
     ap.add_argument("--mode", default="jacobi", choices=["jacobi", "cyclic", "async"],
                     help="schedule: block-Jacobi sweeps (default), deterministic cyclic (N=1), or the "
                          "asynchronous bounded-delay mode (stale NCCL halos, max delay 2)")
@@ -264,6 +270,28 @@ def _load_until(eng, clocks, target, world, dist, torch, limit_s=5.0):
             return
 
 
+def sharded_engine(distributed, obj, x0, cfg, dtype, halo, dist, torch):
+    """N>1 block-Jacobi shard.  halo="p2p" maps the neighbours' inboxes with
+    cudaIpc (all ranks agree on it through an all-reduce; if any rank cannot
+    map a peer, every rank uses the NCCL-halo path and the line says why)."""
+    why = ""
+    if halo == "p2p":
+        eng = None
+        try:
+            eng = distributed.ShardedJacobi(obj, x0, cfg.block_height, dtype, halo="p2p")
+        except (RuntimeError, ValueError, OSError) as e:
+            why = str(e).splitlines()[0][:160] if str(e) else type(e).__name__
+        ok = torch.tensor([0.0 if eng is None else 1.0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if float(ok.item()) > 0:
+            return eng, "p2p: update-kernel NVLink stores into the neighbours' double-buffered inboxes (cudaIpc)"
+        if eng is not None:
+            eng.close()
+        why = f" (p2p unavailable: {why or 'on another rank'})"
+    return (distributed.ShardedJacobi(obj, x0, cfg.block_height, dtype),
+            "nccl: one grouped ncclSend/Recv of the kz halo planes per sweep" + why)
+
+
 # ---------------------------------------------------------------------------
 def main():
     args = parse()
@@ -285,6 +313,7 @@ def main():
     psf, truth, y, x0, params = configs.make_problem(cfg)
     obj = objective.Objective(psf, y, params)
     B = -(-cfg.dims.nz // cfg.block_height)
+    halo_note = None
 
     if args.mode == "async":
         from paper_2002_02328_b200 import distributed
@@ -295,7 +324,7 @@ def main():
         eng = runtime.CyclicSweeper(obj, x0, cfg.block_height, dtype)
     elif world > 1:
         from paper_2002_02328_b200 import distributed
-        eng = distributed.ShardedJacobi(obj, x0, cfg.block_height, dtype)
+        eng, halo_note = sharded_engine(distributed, obj, x0, cfg, dtype, args.halo, dist, torch)
     else:
         eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, dtype)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -373,6 +402,8 @@ def main():
                           "correlation_flops_per_step": sweep_flops,
                           "achieved_tflops": sweep_flops / (t_max / args.steps / 1e3) / 1e12},
                 "f_anchor_last_step": f_last}
+        if halo_note:
+            line["halo"] = halo_note
         line.update(extra)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -503,7 +534,7 @@ def e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng=None):
     bd3mg_problem_jacobi_sweep_host (x and the memory store in from pinned
     host memory, updated x / increments and the recorder terms back).  N>1:
     each rank ships its slab (owned planes + halos) and memory store from
-    pinned host memory to its GPU, runs the NCCL-halo sweep, and copies the
+    pinned host memory to its GPU, runs the sharded sweep, and copies the
     owned planes and the terms back."""
     from paper_2002_02328_b200.host import HostProblem, pinned_empty
 
@@ -572,7 +603,8 @@ def e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng=None):
         nb = eng.nblocks
         h2d = 2 * xl_h.nbytes
         d2h = 2 * (o1 - o0) * plane * 8 + 8
-        path = "per rank: pinned host slab + memory store -> GPU, NCCL-halo sweep, owned planes + f back"
+        path = (f"per rank: pinned host slab + memory store -> GPU, sharded sweep ({eng.halo} halos), "
+                "owned planes + f back")
     return {"value": steps * nb / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": steps, "path": path}
 

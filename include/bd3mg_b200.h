@@ -196,6 +196,31 @@ int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* 
                        const bd3mg_sweep_t* sw, double* terms_out, double* info_out, void* ws, size_t ws_bytes,
                        void* stream);
 
+/* Sharded sweep with the halo exchange fused into the in-place update: the
+ * updated iterate rows [z_lo, z_hi] (global depths, each inside one of the
+ * sweep's blocks) are ALSO stored to dst (plane z_lo first), typically a
+ * peer GPU's halo inbox opened with bd3mg_peer_open -- the NVLink stores
+ * replace the per-sweep ncclSend/Recv of the kz halo planes (
+ * the reference's slab copy of make_task, scheduler.py:186-194).  Same
+ * workspace as bd3mg_jacobi_sweep.  Ordering is the caller's: a peer may read
+ * its inbox only after this call's stream work completed (the sharded driver
+ * double-buffers the inboxes across the per-sweep all-reduce). */
+typedef struct {
+  int64_t z_lo, z_hi;
+  void* dst;
+} bd3mg_mirror_t;
+int bd3mg_jacobi_sweep_mirrored(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                                const bd3mg_sweep_t* sw, const bd3mg_mirror_t* mirrors, int nmirrors,
+                                double* terms_out, double* info_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Peer memory for the halo inboxes: a zeroed device allocation plus its
+ * 64-byte cudaIpc handle; bd3mg_peer_open maps another process's allocation
+ * (NVLink peer access enabled lazily); close unmaps, free releases own. */
+int bd3mg_peer_alloc(size_t bytes, void** dev_out, void* ipc_handle_out);
+int bd3mg_peer_open(const void* ipc_handle, void** dev_out);
+int bd3mg_peer_close(void* dev);
+int bd3mg_peer_free(void* dev);
+
 /* ---- host-buffer problem handle (worker-task boundary of the reference:
  * TaskMessage -> UpdateMessage, scheduler.py:36-57, runtime.py:92-105) ---- */
 typedef struct bd3mg_problem bd3mg_problem;

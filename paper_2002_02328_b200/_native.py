@@ -30,6 +30,7 @@ EXPORTS = (
     "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
     "bd3mg_jacobi_sweep_ws_bytes", "bd3mg_jacobi_cache_elems", "bd3mg_jacobi_sweep",
+    "bd3mg_jacobi_sweep_mirrored", "bd3mg_peer_alloc", "bd3mg_peer_open", "bd3mg_peer_close", "bd3mg_peer_free",
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
     "bd3mg_problem_jacobi_sweep_host",
     "bd3mg_fma_probe",
@@ -58,6 +59,13 @@ class Sweep(C.Structure):
     _fields_ = [("x", C.c_void_p), ("dmem", C.c_void_p), ("frag_z0", C.c_int64), ("nzf", C.c_int64),
                 ("blocks", C.POINTER(C.c_int64)), ("nblocks", C.c_int), ("rec_lo", C.c_int64),
                 ("rec_hi", C.c_int64), ("snap", C.c_void_p), ("hd_cache", C.c_void_p)]
+
+
+class Mirror(C.Structure):
+    _fields_ = [("z_lo", C.c_int64), ("z_hi", C.c_int64), ("dst", C.c_void_p)]
+
+
+IPC_HANDLE_BYTES = 64
 
 
 class NativeError(RuntimeError):
@@ -107,6 +115,12 @@ def _load() -> C.CDLL:
     lib.bd3mg_jacobi_cache_elems.argtypes = [G, S]
     lib.bd3mg_jacobi_cache_elems.restype = C.c_int64
     lib.bd3mg_jacobi_sweep.argtypes = [G, R, _vp, _vp, S, _vp, _vp, _vp, _sz, _vp]
+    lib.bd3mg_jacobi_sweep_mirrored.argtypes = [G, R, _vp, _vp, S, C.POINTER(Mirror), C.c_int, _vp, _vp, _vp, _sz,
+                                                _vp]
+    lib.bd3mg_peer_alloc.argtypes = [_sz, C.POINTER(C.c_void_p), _vp]
+    lib.bd3mg_peer_open.argtypes = [_vp, C.POINTER(C.c_void_p)]
+    lib.bd3mg_peer_close.argtypes = [_vp]
+    lib.bd3mg_peer_free.argtypes = [_vp]
     lib.bd3mg_apply_increment.argtypes = [C.c_int32, _vp, _vp, _vp, _i64, _vp]
     lib.bd3mg_problem_create.argtypes = [G, R, _vp, _vp, C.c_int, C.POINTER(C.c_void_p)]
     lib.bd3mg_problem_destroy.argtypes = [_vp]

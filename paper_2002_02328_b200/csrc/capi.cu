@@ -426,6 +426,8 @@ struct StepOpts {
   T* const* greg = nullptr;    // per task: precomputed regulariser gradient rows (skip the greg launch)
   T* const* omega = nullptr;   // per task: precomputed omega rows
   SideStream* ss = nullptr;    // run reg_gram next to the Gram correlation
+  const bd3mg_mirror_t* mirrors = nullptr;  // rows of the updated iterate also stored to (peer) buffers
+  int nmirrors = 0;
 };
 
 template <typename T>
@@ -658,7 +660,33 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       mc = std::max(mc, B.ctas);
     }
 #ifndef BD3MG_EXP_SKIP_UPDATE
-    update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, info_out); launched();
+    if (opt.nmirrors == 0) {
+      update_kernel<T, 0><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, MirArgs<T, 0>{0, {}}, info_out); launched();
+    } else {
+      // split each mirror into per-block element ranges of the in-place update
+      MirArgs<T, kMaxMirSegs> ma;
+      memset(&ma, 0, sizeof(ma));
+      for (int j = 0; j < opt.nmirrors; ++j) {
+        const bd3mg_mirror_t& M = opt.mirrors[j];
+        int64_t covered = 0;
+        for (int t = 0; t < nt; ++t) {
+          const int64_t lo = std::max<int64_t>(M.z_lo, tasks[t].z_lo), hi = std::min<int64_t>(M.z_hi, tasks[t].z_hi);
+          if (lo > hi) continue;
+          if (!tasks[t].x_rows) return fail(BD3MG_EINVAL, "mirrored rows need an in-place update");
+          if (ma.n == kMaxMirSegs) return fail(BD3MG_EINVAL, "more than %d mirror segments", kMaxMirSegs);
+          MirSeg<T>& S = ma.s[ma.n++];
+          S.blk = t;
+          S.a = (lo - tasks[t].z_lo) * plane;
+          S.b = (hi - tasks[t].z_lo + 1) * plane;
+          S.dst = (T*)M.dst + (lo - M.z_lo) * plane;
+          covered += hi - lo + 1;
+        }
+        if (covered != M.z_hi - M.z_lo + 1)
+          return fail(BD3MG_EINVAL, "mirror rows [%lld, %lld] are not all updated by this call", (long long)M.z_lo,
+                      (long long)M.z_hi);
+      }
+      update_kernel<T, kMaxMirSegs><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, ma, info_out); launched();
+    }
 #endif
     CU(cudaGetLastError());
   }
@@ -712,7 +740,8 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
 // [eval partials][sums][greg, omega per block][step scratch].
 template <typename T>
 int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_sweep_t* sw,
-                      double* terms, double* info, Ws& ws, cudaStream_t s) {
+                      double* terms, double* info, Ws& ws, cudaStream_t s, const bd3mg_mirror_t* mirrors = nullptr,
+                      int nmirrors = 0) {
   if (!sw || sw->nblocks < 1 || sw->nblocks > kMaxJobs)
     return fail(BD3MG_EINVAL, "jacobi sweep needs 1..%d blocks", kMaxJobs);
   const int64_t plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
@@ -759,6 +788,11 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   opt.rec_lo = sw->rec_lo;
   opt.rec_hi = sw->rec_hi;
   opt.hd = sw->hd_cache ? hd.data() : nullptr;
+  if (nmirrors < 0 || (nmirrors > 0 && !mirrors)) return fail(BD3MG_EINVAL, "invalid mirror list");
+  for (int j = 0; j < nmirrors; ++j)
+    if (!mirrors[j].dst || mirrors[j].z_hi < mirrors[j].z_lo) return fail(BD3MG_EINVAL, "invalid mirror %d", j);
+  opt.mirrors = mirrors;
+  opt.nmirrors = nmirrors;
   if (fused) { opt.greg = grb.data(); opt.omega = wb.data(); }
   SideStream* ss = nullptr;
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
@@ -1109,6 +1143,56 @@ int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* 
                                               ws, s),
                     jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
                                              s));
+}
+
+int bd3mg_jacobi_sweep_mirrored(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                                const bd3mg_sweep_t* sw, const bd3mg_mirror_t* mirrors, int nmirrors,
+                                double* terms_out, double* info_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !sw || !info_out || !terms_out) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  return DISPATCH_T(g,
+                    jacobi_sweep_impl<double>(g, r, (const double*)kernels, (const double*)y, sw, terms_out, info_out,
+                                              ws, s, mirrors, nmirrors),
+                    jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
+                                             s, mirrors, nmirrors));
+}
+
+/* ---- peer (NVLink) memory: halo inboxes written by other ranks' kernels ---- */
+int bd3mg_peer_alloc(size_t bytes, void** dev_out, void* ipc_handle_out) {
+  if (!dev_out || !ipc_handle_out || bytes == 0) return fail(BD3MG_EINVAL, "invalid peer allocation");
+  void* p = nullptr;
+  CU(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(BD3MG_ECUDA, "peer allocation: %s", cudaGetErrorString(e));
+  }
+  memcpy(ipc_handle_out, &h, sizeof(h));
+  *dev_out = p;
+  return BD3MG_OK;
+}
+
+int bd3mg_peer_open(const void* ipc_handle, void** dev_out) {
+  if (!ipc_handle || !dev_out) return fail(BD3MG_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  CU(cudaIpcOpenMemHandle(dev_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return BD3MG_OK;
+}
+
+int bd3mg_peer_close(void* dev) {
+  if (dev) CU(cudaIpcCloseMemHandle(dev));
+  return BD3MG_OK;
+}
+
+int bd3mg_peer_free(void* dev) {
+  if (dev) CU(cudaFree(dev));
+  return BD3MG_OK;
 }
 
 size_t bd3mg_mg_steps_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks) {

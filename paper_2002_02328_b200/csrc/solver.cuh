@@ -171,22 +171,61 @@ struct UpdArgs {
   UpdBlock<T> blk[kMaxJobs];
 };
 
+// Mirrored rows of the updated iterate: elements [a, b) of block `blk` are
+// also stored to dst[i - a] -- a peer GPU's halo inbox mapped over NVLink
+// (cudaIpc), so the halo exchange of the sharded sweep rides on the update's
+// own stores instead of a separate collective.
 template <typename T>
+struct MirSeg {
+  T* dst;
+  long long a, b;
+  int blk;
+};
+constexpr int kMaxMirSegs = 64;
+template <typename T, int NSEG>
+struct MirArgs {
+  int n;
+  MirSeg<T> s[NSEG > 0 ? NSEG : 1];
+};
+
+template <typename T, int NSEG>
+__device__ __forceinline__ void mirror_store(const MirArgs<T, NSEG>& m, long long i, T v) {
+  if constexpr (NSEG > 0) {
+    for (int j = 0; j < m.n; ++j) {
+      const MirSeg<T>& s = m.s[j];
+      if (s.blk == (int)blockIdx.y && i >= s.a && i < s.b) s.dst[i - s.a] = v;
+    }
+  }
+}
+
+template <typename T, int NSEG>
 __global__ void __launch_bounds__(kEwNT) update_kernel(const __grid_constant__ UpdArgs<T> p,
+                                                        const __grid_constant__ MirArgs<T, NSEG> m,
                                                         const double* __restrict__ info) {
   const UpdBlock<T>& B = p.blk[blockIdx.y];
   if ((int)blockIdx.x >= B.ctas) return;
   const double* o = info + blockIdx.y * kInfoNV;
-  if (o[8] != 0.0) return;  // non-finite gradient: host raises, nothing applied
+  const long long i0 = (long long)blockIdx.x * kEwNT + threadIdx.x, di = (long long)B.ctas * kEwNT;
+  if (o[8] != 0.0) {  // non-finite gradient: host raises, nothing applied (mirrors keep x current)
+    if constexpr (NSEG > 0)
+      if (B.x)
+        for (long long i = i0; i < B.n; i += di) mirror_store(m, i, B.x[i]);
+    return;
+  }
   const T cg = (T)o[10], cd = (T)o[11];
   const bool has_d = B.d != nullptr;
-  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < B.n; i += (long long)B.ctas * kEwNT) {
+  for (long long i = i0; i < B.n; i += di) {
     T inc = mul_rn(-B.g[i], cg);
     if (has_d) inc = add_rn(inc, mul_rn(B.d[i], cd));
     if (B.inc_out) B.inc_out[i] = inc;
-    if (B.x) B.x[i] = add_rn(B.x[i], inc);
+    if (B.x) {
+      const T xn = add_rn(B.x[i], inc);
+      B.x[i] = xn;
+      mirror_store(m, i, xn);
+    }
     if (B.dmem) B.dmem[i] = inc;
   }
+  if constexpr (NSEG > 0) __threadfence_system();  // peer stores ordered before the stream's next work
 }
 
 // terms: [data, box, tv, axial, f, |x-snap|^2, |snap|^2]

@@ -99,13 +99,137 @@ def exchange_halos(buf: torch.Tensor, z0: int, plan, group=None) -> None:
             req.wait()
 
 
+class _RawDevice:
+    """A raw device allocation seen by torch (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, n: int, dtype: torch.dtype):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8" if dtype == torch.float64 else "<f4",
+                                         "data": (ptr, False), "strides": None, "version": 3}
+
+
+class PeerHalo:
+    """Halo exchange by NVLink peer stores, fused into the sweep's update.
+
+    Every rank owns a halo INBOX: its received halo planes (the "recv" plan
+    of SlabLayout.transfers, in plan order), twice -- one copy per sweep
+    parity.  Sweep t of a rank (1) copies inbox[t % 2] into the halo planes
+    of its local slab (a device-local copy), (2) runs the fused sweep
+    (``bd3mg_jacobi_sweep_mirrored``) whose in-place update stores the
+    updated rows each neighbour keeps as halo straight into that neighbour's
+    inbox[(t + 1) % 2] -- mapped into this process with cudaIpc, so the
+    stores go over NVLink while the update streams through HBM, and no
+    ncclSend/Recv is left on the sweep's critical path.  (3) The recorder
+    all-reduce that ends every sweep is the only synchronisation: a rank
+    enters sweep t + 1 (reading inbox[(t + 1) % 2]) only after every rank's
+    sweep t work -- its peer stores included -- completed, and no rank can
+    write inbox[t % 2] again (sweep t + 1) before every rank finished
+    reading it (sweep t).  The iterate is bitwise that of the NCCL-halo
+    path.  Peer pointers come from ``connect_ipc`` (one process per GPU) or
+    ``connect`` (virtual ranks of one process)."""
+
+    def __init__(self, shard: "ShardedJacobi"):
+        import ctypes as C
+
+        from . import _native as N
+        self.N, self.C = N, C
+        self.shard = shard
+        lay, me = shard.layout, shard.rank
+        self.recv = [(q, lo, hi) for q, lo, hi, k in lay.transfers(me) if k == "recv"]
+        self.send = [(q, lo, hi) for q, lo, hi, k in lay.transfers(me) if k == "send"]
+        self.nplanes = sum(hi - lo + 1 for _, lo, hi in self.recv)
+        self.plane = shard.plane
+        self.esz = shard.x.element_size()
+        n = max(1, 2 * self.nplanes * self.plane)
+        ptr, self.handle = C.c_void_p(), (C.c_ubyte * N.IPC_HANDLE_BYTES)()
+        N.check(N.lib.bd3mg_peer_alloc(n * self.esz, C.byref(ptr), self.handle))
+        self.ptr = ptr.value
+        self.opened: list[int] = []
+        dims = shard.x.shape[1:]
+        self.inbox = torch.as_tensor(_RawDevice(self.ptr, n, shard.x.dtype), device=shard.x.device)
+        self.inbox = self.inbox[:2 * self.nplanes * self.plane].view(2, self.nplanes, *dims)
+        self.slots = []  # (inbox plane offset, x plane offset, count) per received range
+        off = 0
+        for _, lo, hi in self.recv:
+            self.slots.append((off, lo - shard.l_lo, hi - lo + 1))
+            off += hi - lo + 1
+        for o, xo, c in self.slots:  # parity 0 = the initial iterate's halos
+            self.inbox[0, o:o + c].copy_(shard.x[xo:xo + c])
+        self.mirrors = None
+
+    @staticmethod
+    def inbox_offset(layout: SlabLayout, rank: int, src: int, lo: int, hi: int) -> tuple[int, int]:
+        """(plane offset of src's range [lo, hi] in rank's inbox, planes per parity)."""
+        off, total, at = 0, 0, None
+        for q, a, b, k in layout.transfers(rank):
+            if k != "recv":
+                continue
+            if (q, a, b) == (src, lo, hi):
+                at = total
+            total += b - a + 1
+        if at is None:
+            raise ValueError(f"rank {rank} receives no planes [{lo}, {hi}] from rank {src}")
+        return at, total
+
+    def connect(self, bases: dict) -> None:
+        """bases[q] = device address of rank q's inbox (mapped here) for every
+        rank this one sends to; builds the mirror lists of both parities."""
+        N, C = self.N, self.C
+        lay, me = self.shard.layout, self.shard.rank
+        self.mirrors = []
+        for parity in (0, 1):
+            arr = (N.Mirror * max(1, len(self.send)))()
+            for i, (q, lo, hi) in enumerate(self.send):
+                off, total = self.inbox_offset(lay, q, me, lo, hi)
+                arr[i] = N.Mirror(lo, hi, bases[q] + (parity * total + off) * self.plane * self.esz)
+            self.mirrors.append(arr)
+
+    def connect_ipc(self, group=None) -> None:
+        """One process per GPU: exchange the inbox cudaIpc handles, map the
+        inboxes of the ranks this one sends to (NVLink peer access)."""
+        N, C = self.N, self.C
+        world = dist.get_world_size(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(self.handle), group=group)
+        bases = {}
+        for q in sorted({q for q, _, _ in self.send}):
+            ptr = C.c_void_p()
+            buf = (C.c_ubyte * N.IPC_HANDLE_BYTES).from_buffer_copy(handles[q])
+            N.check(N.lib.bd3mg_peer_open(buf, C.byref(ptr)))
+            bases[q] = ptr.value
+            self.opened.append(ptr.value)
+        self.connect(bases)
+
+    def unpack(self, parity: int) -> None:
+        """Halo planes of the local slab <- inbox[parity] (device-local copies)."""
+        for o, xo, c in self.slots:
+            self.shard.x[xo:xo + c].copy_(self.inbox[parity, o:o + c])
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.N.lib.bd3mg_peer_close(p)
+        self.opened = []
+        if self.ptr:
+            self.inbox = None
+            self.N.lib.bd3mg_peer_free(self.ptr)
+            self.ptr = 0
+
+
 class ShardedJacobi:
-    """GPU block-Jacobi shard of this rank: NCCL halos + one fused
+    """GPU block-Jacobi shard of this rank: halos + one fused
     ``bd3mg_jacobi_sweep`` over the owned blocks (recorder on owned rows,
-    whose 7 terms are all-reduced)."""
+    whose 7 terms are all-reduced).
+
+    halo="nccl": one grouped ncclSend/Recv of the halo planes per sweep.
+    halo="p2p": the update kernel stores the neighbour-facing rows straight
+    into the neighbours' halo inboxes over NVLink (PeerHalo); with
+    ``rank``/``world`` given (virtual ranks of one process) the caller
+    connects the inboxes itself."""
 
     def __init__(self, obj, x0, block_height: int, dtype: torch.dtype = torch.float64, group=None,
-                 rank: int | None = None, world: int | None = None, hd_cache: bool = False):
+                 rank: int | None = None, world: int | None = None, hd_cache: bool = False,
+                 halo: str = "nccl"):
+        if halo not in ("nccl", "p2p"):
+            raise ValueError(f"unknown halo transport {halo!r}")
         import ctypes as C
 
         from . import _native as N
@@ -148,29 +272,67 @@ class ShardedJacobi:
         self.terms = torch.zeros(N.EVAL_DOUBLES, dtype=torch.float64, device=dev)
         self.K = obj.psf.device_kernels(dtype, dev)
         self.k = 0
+        self.sweeps = 0
+        self.halo = halo
+        self.graphs = None
+        self.peer = PeerHalo(self) if halo == "p2p" else None
+        if self.peer is not None and rank is None:
+            self.peer.connect_ipc(group)
 
     @property
     def nblocks(self) -> int:
         return len(self.layout.blocks)
+
+    def _sync_terms(self) -> None:
+        """Sum the recorder terms over the ranks.  On the p2p path this is
+        also the sweep's synchronisation point (stream-ordered on NCCL; a
+        host barrier after a device synchronise on gloo)."""
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self.terms, group=self.group)
+        else:
+            torch.cuda.synchronize()
+            t = self.terms.cpu()
+            dist.all_reduce(t, group=self.group)
+            self.terms.copy_(t)
 
     # -- phases (sweep() runs them; a single-process emulation of several
     #    ranks drives them itself) -----------------------------------------
     def exchange(self) -> None:
         exchange_halos(self.x, self.l_lo, self.plan, self.group)
 
+    def _launch(self, parity: int) -> None:
+        N, D = self.N, self.D
+        if self.peer is None:
+            N.check(N.lib.bd3mg_jacobi_sweep(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.y_shift,
+                                             D.byref(self.sw), self.terms.data_ptr(), self.info.data_ptr(),
+                                             self.ws.data_ptr(), self.ws_bytes, D.stream_handle()))
+            return
+        if self.peer.mirrors is None:
+            raise RuntimeError("p2p halos: inboxes not connected")
+        self.peer.unpack(parity)
+        mir = self.peer.mirrors[(parity + 1) % 2]
+        N.check(N.lib.bd3mg_jacobi_sweep_mirrored(
+            D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.y_shift, D.byref(self.sw), mir,
+            len(self.peer.send), self.terms.data_ptr(), self.info.data_ptr(), self.ws.data_ptr(), self.ws_bytes,
+            D.stream_handle()))
+
     def local_sweep(self) -> None:
         """Recorder terms of the anchor on owned rows (local sums) + the fused
-        steps of the owned blocks."""
-        N, D = self.N, self.D
-        N.check(N.lib.bd3mg_jacobi_sweep(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.y_shift,
-                                         D.byref(self.sw), self.terms.data_ptr(), self.info.data_ptr(),
-                                         self.ws.data_ptr(), self.ws_bytes, D.stream_handle()))
+        steps of the owned blocks (p2p: after unpacking this sweep's inbox,
+        with the neighbour-facing rows mirrored into the peers' next one)."""
+        parity = self.sweeps % 2
+        if self.graphs is not None:
+            self.graphs[parity].replay()
+        else:
+            self._launch(parity)
+        self.sweeps += 1
         self.k += self.nblocks
 
     def sweep(self) -> None:
-        self.exchange()
+        if self.peer is None:
+            self.exchange()
         self.local_sweep()
-        dist.all_reduce(self.terms, group=self.group)
+        self._sync_terms()
 
     def record_local(self) -> None:
         """Recorder terms of the current iterate on owned rows (halos must be current)."""
@@ -183,13 +345,32 @@ class ShardedJacobi:
 
     def finish(self) -> float:
         """Recorder pass of the last sweep's result; returns f(x)."""
-        self.exchange()
+        if self.peer is None:
+            self.exchange()
+        else:
+            self.peer.unpack(self.sweeps % 2)
         self.record_local()
-        dist.all_reduce(self.terms, group=self.group)
+        self._sync_terms()
         return float(self.terms[4].item())
 
     def capture(self) -> None:
-        """Sweeps with NCCL P2P stay eager (no graph capture)."""
+        """p2p halos: the inbox unpack + fused sweep of each parity become a
+        CUDA graph (the recorder all-reduce stays outside).  NCCL halos stay
+        eager."""
+        if self.peer is None:
+            return
+        graphs = []
+        for parity in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch(parity)
+            graphs.append(g)
+        self.graphs = graphs
+
+    def close(self) -> None:
+        self.graphs = None
+        if self.peer is not None:
+            self.peer.close()
 
     def check(self) -> None:
         if bool((self.info[:, 8] != 0).any().item()):
@@ -201,6 +382,8 @@ class ShardedJacobi:
     def gather(self) -> np.ndarray | None:
         """Full iterate on rank 0 (owned planes from every rank)."""
         own = self.x[self.o_lo - self.l_lo:self.o_hi - self.l_lo + 1].contiguous()
+        if dist.get_backend(self.group) != "nccl":
+            own = own.cpu()  # gloo moves host tensors
         if self.rank == 0:
             parts = [own]
             for q in range(1, self.world):

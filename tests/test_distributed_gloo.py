@@ -149,3 +149,28 @@ def test_async_bounded_delay_gloo(world, tmp_path, oracle_mod):
     B = -(-x0.shape[0] // h)
     sync, _, _ = oracle_mod.run_bp3mg(crit, x0, B, h, max_updates=sweeps * B)
     assert abs(crit.value(got) - crit.value(sync)) <= 0.05 * crit.value(sync)
+
+
+def test_p2p_inbox_plan():
+    """Every send of the halo plan lands at a distinct, in-range slot of the
+    receiver's inbox, and the inbox slots tile the receiver's halo planes."""
+    from paper_2002_02328_b200.distributed import PeerHalo
+    for nz, kz, h, world in [(64, 11, 8, 8), (64, 11, 8, 2), (24, 5, 2, 4), (30, 7, 4, 3), (512, 21, 64, 8)]:
+        lay = SlabLayout.build(nz, kz, h, world)
+        slots = {q: [] for q in range(world)}
+        for r in range(world):
+            for q, lo, hi, k in lay.transfers(r):
+                if k != "send":
+                    continue
+                off, total = PeerHalo.inbox_offset(lay, q, r, lo, hi)
+                assert 0 <= off and off + (hi - lo + 1) <= total
+                slots[q].append((off, off + hi - lo + 1))
+        for q in range(world):
+            l_lo, l_hi = lay.local(q)
+            o_lo, o_hi = lay.owned(q)
+            halo = (l_hi - l_lo + 1) - (o_hi - o_lo + 1)
+            covered = sorted(slots[q])
+            assert sum(b - a for a, b in covered) == halo
+            assert all(covered[i][1] == covered[i + 1][0] for i in range(len(covered) - 1))
+        with pytest.raises(ValueError):
+            PeerHalo.inbox_offset(lay, 0, 0, 0, 0)
