@@ -65,11 +65,11 @@ def parse():
     ap.add_argument("--strong", action="store_true",
                     help="N>1: split the N=1 volume over the ranks (default: weak scaling, the config per GPU)")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
-                    help="N>1 block-Jacobi halo transport: update-kernel NVLink stores into the neighbours' "
-                         "inboxes (default) or a grouped ncclSend/Recv per sweep")
+                    help="N>1 halo transport: update-kernel NVLink stores into the neighbours' inboxes "
+                         "(block-Jacobi) / halo rings (async) -- the default -- or NCCL messages")
     ap.add_argument("--mode", default="jacobi", choices=["jacobi", "cyclic", "async"],
                     help="schedule: block-Jacobi sweeps (default), deterministic cyclic (N=1), or the "
-                         "asynchronous bounded-delay mode (stale NCCL halos, max delay 2)")
+                         "asynchronous bounded-delay mode (stale peer halos, max delay 2)")
     return ap.parse_args()
 
 
@@ -317,7 +317,10 @@ def main():
 
     if args.mode == "async":
         from paper_2002_02328_b200 import distributed
-        eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2)
+        eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2, halo=args.halo)
+        if world > 1:
+            halo_note = ("p2p: update-kernel NVLink stores into the readers' halo rings, fenced version flags "
+                         "in a shared host page" if args.halo == "p2p" else "nccl: isend/irecv halo messages")
     elif args.mode == "cyclic":
         if world > 1:
             raise SystemExit("--mode cyclic is the single-worker schedule (N=1)")

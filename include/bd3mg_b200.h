@@ -213,6 +213,26 @@ int bd3mg_jacobi_sweep_mirrored(const bd3mg_geom_t* g, const bd3mg_reg_t* r, con
                                 const bd3mg_sweep_t* sw, const bd3mg_mirror_t* mirrors, int nmirrors,
                                 double* terms_out, double* info_out, void* ws, size_t ws_bytes, void* stream);
 
+/* bd3mg_mg_steps with the in-place update's rows also stored to mirrors (the
+ * asynchronous mode's halo rings); one launch (<= 32 tasks). */
+int bd3mg_mg_steps_mirrored(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                            const bd3mg_task_t* tasks, int ntasks, const bd3mg_mirror_t* mirrors, int nmirrors,
+                            double* info_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Version flags of the asynchronous halo rings: host memory (e.g. a shared
+ * mapping every rank's process maps) registered for device access, and a
+ * stream-ordered publish that stores each value after a system-scope fence
+ * (a reader that sees flag i sees the stream's earlier stores, ring data
+ * included). */
+#define BD3MG_MAX_FLAGS 16
+typedef struct {
+  int64_t* word;  /* device-visible address (bd3mg_host_register) */
+  int64_t value;
+} bd3mg_flag_t;
+int bd3mg_host_register(void* host, size_t bytes, void** dev_out);
+int bd3mg_host_unregister(void* host);
+int bd3mg_publish(const bd3mg_flag_t* flags, int nflags, void* stream);
+
 /* Peer memory for the halo inboxes: a zeroed device allocation plus its
  * 64-byte cudaIpc handle; bd3mg_peer_open maps another process's allocation
  * (NVLink peer access enabled lazily); close unmaps, free releases own. */

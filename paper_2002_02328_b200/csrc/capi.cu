@@ -64,6 +64,23 @@ struct Ws {
   bool ok() const { return measure || off <= cap; }
 };
 
+// Ordered flag stores for the asynchronous halo rings: each store is
+// preceded by a system-scope fence, so a host (or peer) that sees flag i
+// also sees every earlier store of this stream -- the ring data the update
+// kernel wrote over NVLink and the flags before i.
+struct PubArgs {
+  int n;
+  volatile long long* word[BD3MG_MAX_FLAGS];
+  long long value[BD3MG_MAX_FLAGS];
+};
+__global__ void publish_kernel(const __grid_constant__ PubArgs a) {
+  for (int i = 0; i < a.n; ++i) {
+    __threadfence_system();
+    *a.word[i] = a.value[i];
+  }
+  __threadfence_system();
+}
+
 bool odd_pos(int64_t k) { return k >= 1 && (k % 2) == 1; }
 
 int check_geom(const bd3mg_geom_t* g) {
@@ -710,8 +727,16 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
 
 template <typename T>
 int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
-                  int ntasks, double* info_out, Ws& ws, cudaStream_t s) {
+                  int ntasks, double* info_out, Ws& ws, cudaStream_t s, const bd3mg_mirror_t* mirrors = nullptr,
+                  int nmirrors = 0) {
   if (ntasks < 0) return fail(BD3MG_EINVAL, "negative task count");
+  if (nmirrors < 0 || (nmirrors > 0 && (!mirrors || ntasks > kMaxJobs)))
+    return fail(BD3MG_EINVAL, "invalid mirror list (mirrored calls are one launch of <= %d tasks)", kMaxJobs);
+  for (int j = 0; j < nmirrors; ++j)
+    if (!mirrors[j].dst || mirrors[j].z_hi < mirrors[j].z_lo) return fail(BD3MG_EINVAL, "invalid mirror %d", j);
+  StepOpts<T> opt;
+  opt.mirrors = mirrors;
+  opt.nmirrors = nmirrors;
   // tasks run in launches of kMaxJobs; an in-place update of one launch would
   // move the anchor of the next, so in-place calls are limited to one launch
   if (ntasks > kMaxJobs)
@@ -725,7 +750,7 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
     sub.off = 0;
     if (!ws.measure) { sub.base = ws.base; sub.cap = ws.cap; }
     int rc = mg_steps_chunk<T>(g, r, K, y, tasks + t0, nt, info_out ? info_out + (size_t)t0 * kInfoNV : nullptr,
-                               sub, s);
+                               sub, s, opt);
     if (rc != BD3MG_OK) return rc;
     peak = std::max(peak, sub.off);
   }
@@ -1182,6 +1207,53 @@ int bd3mg_peer_open(const void* ipc_handle, void** dev_out) {
   cudaIpcMemHandle_t h;
   memcpy(&h, ipc_handle, sizeof(h));
   CU(cudaIpcOpenMemHandle(dev_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return BD3MG_OK;
+}
+
+int bd3mg_mg_steps_mirrored(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                            const bd3mg_task_t* tasks, int ntasks, const bd3mg_mirror_t* mirrors, int nmirrors,
+                            double* info_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r) return fail(BD3MG_EINVAL, "null regulariser");
+  if (!info_out) return fail(BD3MG_EINVAL, "info_out is required");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    mg_steps_impl<double>(g, r, (const double*)kernels, (const double*)y, tasks, ntasks, info_out,
+                                          ws, (cudaStream_t)stream, mirrors, nmirrors),
+                    mg_steps_impl<float>(g, r, (const float*)kernels, (const float*)y, tasks, ntasks, info_out, ws,
+                                         (cudaStream_t)stream, mirrors, nmirrors));
+}
+
+int bd3mg_host_register(void* host, size_t bytes, void** dev_out) {
+  if (!host || !dev_out || bytes == 0) return fail(BD3MG_EINVAL, "invalid host range");
+  CU(cudaHostRegister(host, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+  cudaError_t e = cudaHostGetDevicePointer(dev_out, host, 0);
+  if (e != cudaSuccess) {
+    cudaHostUnregister(host);
+    return fail(BD3MG_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+  }
+  return BD3MG_OK;
+}
+
+int bd3mg_host_unregister(void* host) {
+  if (host) CU(cudaHostUnregister(host));
+  return BD3MG_OK;
+}
+
+int bd3mg_publish(const bd3mg_flag_t* flags, int nflags, void* stream) {
+  if (nflags < 0 || nflags > BD3MG_MAX_FLAGS || (nflags > 0 && !flags))
+    return fail(BD3MG_EINVAL, "1..%d flags per publish", BD3MG_MAX_FLAGS);
+  if (nflags == 0) return BD3MG_OK;
+  PubArgs a;
+  a.n = nflags;
+  for (int i = 0; i < nflags; ++i) {
+    if (!flags[i].word) return fail(BD3MG_EINVAL, "null flag word %d", i);
+    a.word[i] = (volatile long long*)flags[i].word;
+    a.value[i] = flags[i].value;
+  }
+  publish_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(a); launched();
+  CU(cudaGetLastError());
   return BD3MG_OK;
 }
 

@@ -114,9 +114,11 @@ def info_to_step(info: np.ndarray, increment) -> StepInfo:
 
 
 def mg_steps_device(obj: Objective, tasks: list[N.Task], dtype: torch.dtype,
-                    info: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                    info: torch.Tensor | None = None, stream=None, mirrors=None) -> torch.Tensor:
     """Launch the fused block steps for `tasks` (device pointers) on the
-    current stream; returns the device info tensor (ntasks x 16)."""
+    current stream; returns the device info tensor (ntasks x 16).
+    ``mirrors`` (a list of N.Mirror): updated rows also stored there
+    (bd3mg_mg_steps_mirrored; the asynchronous mode's peer halo rings)."""
     n = len(tasks)
     arr = (N.Task * max(n, 1))(*tasks)
     g = obj.geom(dtype)
@@ -126,6 +128,12 @@ def mg_steps_device(obj: Objective, tasks: list[N.Task], dtype: torch.dtype,
     if info is None:
         info = torch.empty((n, N.INFO_DOUBLES), dtype=torch.float64, device=dev)
     k = obj.psf.device_kernels(dtype, dev)
+    if mirrors:
+        marr = (N.Mirror * len(mirrors))(*mirrors)
+        N.check(N.lib.bd3mg_mg_steps_mirrored(D.byref(g), D.byref(D.reg(obj.params)), k.data_ptr(),
+                                              obj.device_y(dtype, dev).data_ptr(), arr, n, marr, len(mirrors),
+                                              info.data_ptr(), ws.data_ptr(), nbytes, D.stream_handle(stream)))
+        return info
     N.check(N.lib.bd3mg_mg_steps(D.byref(g), D.byref(D.reg(obj.params)), k.data_ptr(),
                                  obj.device_y(dtype, dev).data_ptr(), arr, n, info.data_ptr(),
                                  ws.data_ptr(), nbytes, D.stream_handle(stream)))

@@ -575,14 +575,19 @@ class AsyncShard:
         return [q for q, rs in self.recv_ranges.items() if any(lo <= s_hi and hi >= s_lo for lo, hi in rs)]
 
     def update(self) -> None:
-        block = self.blocks[self.t % len(self.blocks)]
+        bi = self.t % len(self.blocks)
+        block = self.blocks[bi]
         stale = 0
-        for q in self.recv_ranges:
-            v = self.net.poll(q)
-            if v is not None:
-                self.version[q] = v
+        lazy = getattr(self.net, "lazy", False)  # peer rings: read only the peers this block needs
+        if not lazy:
+            for q in self.recv_ranges:
+                v = self.net.poll(q)
+                if v is not None:
+                    self.version[q] = v
         for q in self._needs(block):
             need = self.t - self.max_delay
+            if lazy:
+                self.version[q] = self.net.poll(q)
             if self.version[q] < need:
                 self.waits += 1
                 v = self.net.poll(q, need)
@@ -590,6 +595,14 @@ class AsyncShard:
                     self.version[q] = v
             stale = max(stale, max(0, self.t - self.version[q]))
         self.staleness.append(stale)
+        if lazy:
+            # the update kernel stores the neighbour-facing rows into the
+            # peers' rings; the publish that follows it on the stream makes
+            # them (and the update count t+1) visible
+            self.step_fn(self, block, self.net.mirrors_for(bi, self.t))
+            self.t += 1
+            self.net.publish(bi, self.t)
+            return
         self.step_fn(self, block)
         self.t += 1
         # every update publishes the neighbour-facing planes with version t,
@@ -637,18 +650,272 @@ class LocalP2P:
         pass
 
 
+class RingPlan:
+    """Units of the asynchronous peer halo rings.
+
+    A unit is the rows one writer block contributes to one reader's halo:
+    (writer, reader, writer-block index, z_lo, z_hi).  A block update
+    changes exactly its own rows, so each unit carries its own data version
+    (the writer's update count when the rows were last written) and its own
+    ring of `slots` copies in the READER's memory; slot v % slots holds data
+    version v (slot 0 = the initial iterate).  Flag words (int64, host
+    memory every rank maps): dv[u] per unit, then count[p] per writer (p's
+    completed updates -- the version the bounded-delay rule reads)."""
+
+    def __init__(self, layout: SlabLayout, slots: int):
+        self.layout, self.slots = layout, slots
+        self.units = []
+        for p in range(layout.world):
+            blocks = layout.owned_blocks(p)
+            for q, lo, hi, kind in layout.transfers(p):
+                if kind != "send":
+                    continue
+                for bi, b in enumerate(blocks):
+                    a, c = max(lo, b.z_lo), min(hi, b.z_hi)
+                    if a <= c:
+                        self.units.append((p, q, bi, a, c))
+        self.offset = []                       # unit -> plane offset in the reader's ring
+        self.ring_planes = [0] * layout.world  # ring size (planes) per reader
+        for p, q, bi, a, c in self.units:
+            self.offset.append(self.ring_planes[q])
+            self.ring_planes[q] += slots * (c - a + 1)
+        self.nflags = len(self.units) + layout.world
+
+    def count_index(self, p: int) -> int:
+        return len(self.units) + p
+
+    def writes(self, p: int, bi: int) -> list[int]:
+        return [u for u, (w, _, b, _, _) in enumerate(self.units) if w == p and b == bi]
+
+    def reads(self, q: int, p: int) -> list[int]:
+        return [u for u, (w, r, _, _, _) in enumerate(self.units) if r == q and w == p]
+
+    def slot_plane(self, u: int, version: int) -> int:
+        """Plane offset of data version `version` of unit u in its reader's ring."""
+        p, q, bi, a, c = self.units[u]
+        return self.offset[u] + (version % self.slots) * (c - a + 1)
+
+
+def _map_flags(path: str | None, nbytes: int):
+    """Host flag page(s): a shared file mapping (one per job, every rank maps
+    it) or an anonymous one (virtual ranks of one process), registered for
+    device access.  Returns (mmap, int64 view, device address)."""
+    import ctypes as C
+    import mmap
+
+    from . import _native as N
+    nbytes = max(mmap.PAGESIZE, -(-nbytes // mmap.PAGESIZE) * mmap.PAGESIZE)
+    if path is None:
+        mm = mmap.mmap(-1, nbytes)
+    else:
+        import os
+        fd = os.open(path, os.O_RDWR)
+        try:
+            mm = mmap.mmap(fd, nbytes)
+        finally:
+            os.close(fd)
+    words = np.frombuffer(mm, dtype=np.int64)
+    host = C.addressof(C.c_char.from_buffer(mm))
+    dev = C.c_void_p()
+    N.check(N.lib.bd3mg_host_register(host, nbytes, C.byref(dev)))
+    return mm, words, host, dev.value
+
+
+class PeerRing:
+    """Asynchronous-mode halo transport over peer memory (SURVEY.md 8(e):
+    "P2P stores into peer halo rings with version counters").
+
+    Writer side: the block's update kernel stores the rows of every unit it
+    feeds into slot (t+1) % slots of the reader's ring (NVLink stores into
+    cudaIpc-mapped memory; ``mirrors_for``), then a one-thread publish kernel
+    on the same stream stores dv[u] = t+1 and count[me] = t+1, each after a
+    system-scope fence (``publish``).  Reader side (``poll``): reads count
+    and dv from the host-mapped flags, spins while count < need (the
+    bounded-delay rule), and copies the newest slot of each unit into its
+    slab with a stream-ordered device copy.  Only the peers the current
+    block needs are read (``lazy``), so a reader copies only after the
+    writer satisfied the delay bound; with that, a writer can move at most
+    2*max_delay + 2 updates ahead of a copy still queued on the reader's
+    stream, which `slots` covers (the writer blocks on the reader in turn).
+    No kernel waits on another rank: all waiting is host-side."""
+
+    lazy = True
+
+    def __init__(self, plan: RingPlan, rank: int, x: torch.Tensor, z0: int, ring_ptr: int, ring_bases: dict,
+                 flags: np.ndarray, flags_dev: int, timeout_s: float = 120.0):
+        from . import _native as N
+        self.N = N
+        self.plan, self.me, self.x, self.z0 = plan, rank, x, z0
+        self.plane = int(np.prod(x.shape[1:]))
+        self.esz = x.element_size()
+        self.bases = ring_bases
+        self.flags, self.flags_dev = flags, flags_dev
+        self.timeout_s = timeout_s
+        nring = max(1, plan.ring_planes[rank] * self.plane)
+        self.ring = torch.as_tensor(_RawDevice(ring_ptr, nring, x.dtype), device=x.device)
+        self.applied = {}
+        for u, (p, q, bi, a, c) in enumerate(plan.units):
+            if q == rank:  # slot 0 of my rings = the initial iterate's rows
+                off = plan.slot_plane(u, 0) * self.plane
+                self.ring[off:off + (c - a + 1) * self.plane].copy_(x[a - z0:c - z0 + 1].reshape(-1))
+                self.applied[u] = 0
+        self.reads = {p: plan.reads(rank, p) for p in range(plan.layout.world)}
+        self.writes = [plan.writes(rank, bi) for bi in range(len(plan.layout.owned_blocks(rank)))]
+
+    def mirrors_for(self, bi: int, t: int):
+        N, plan = self.N, self.plan
+        out = []
+        for u in self.writes[bi]:
+            p, q, _, a, c = plan.units[u]
+            out.append(N.Mirror(a, c, self.bases[q] + plan.slot_plane(u, t + 1) * self.plane * self.esz))
+        return out
+
+    def publish(self, bi: int, t: int) -> None:
+        from . import device as D
+        N, plan = self.N, self.plan
+        words = [u for u in self.writes[bi]] + [plan.count_index(self.me)]
+        arr = (N.Flag * len(words))(*[N.Flag(self.flags_dev + 8 * w, t) for w in words])
+        N.check(N.lib.bd3mg_publish(arr, len(words), D.stream_handle()))
+
+    def count(self, p: int) -> int:
+        return int(self.flags[self.plan.count_index(p)])
+
+    def poll(self, p: int, need: int | None = None) -> int:
+        """Newest update count of writer p (waiting while it is below
+        `need`); its newest unit data is copied into the slab."""
+        import time
+        v = self.count(p)
+        if need is not None and v < need:
+            t_end = time.monotonic() + self.timeout_s
+            while v < need:
+                if time.monotonic() > t_end:
+                    raise TimeoutError(f"rank {self.me}: writer {p} stuck at update {v} < {need}")
+                time.sleep(0)
+                v = self.count(p)
+        for u in self.reads[p]:
+            d = int(self.flags[u])
+            if d > self.applied[u]:
+                _, _, _, a, c = self.plan.units[u]
+                off = self.plan.slot_plane(u, d) * self.plane
+                self.x[a - self.z0:c - self.z0 + 1].copy_(
+                    self.ring[off:off + (c - a + 1) * self.plane].view((c - a + 1,) + tuple(self.x.shape[1:])))
+                self.applied[u] = d
+        return v
+
+    def finish(self) -> None:
+        """Nothing is in flight between ranks once the stream drained."""
+        torch.cuda.synchronize()
+
+
+def ring_slots(max_delay: int) -> int:
+    """Ring depth covering a writer's lead over a queued reader copy."""
+    return 2 * max_delay + 6
+
+
+class RingHub:
+    """Rings + flags of every rank of one asynchronous job.
+
+    ``RingHub.local(...)``: virtual ranks of one process (rings allocated
+    here, flags in an anonymous mapping).  ``RingHub.ipc(...)``: one rank per
+    process: a shared flag file under /dev/shm (rank 0 creates it), each
+    rank's ring exported as a cudaIpc handle and mapped by its writers."""
+
+    def __init__(self):
+        self.mm = None
+        self.path = None
+        self.host = 0
+        self.own = []
+        self.opened = []
+
+    @classmethod
+    def local(cls, plan: RingPlan, xs: list, z0s: list) -> tuple["RingHub", list]:
+        import ctypes as C
+
+        from . import _native as N
+        hub = cls()
+        hub.mm, flags, hub.host, fdev = _map_flags(None, plan.nflags * 8)
+        ptrs = []
+        for q, x in enumerate(xs):
+            ptr, h = C.c_void_p(), (C.c_ubyte * N.IPC_HANDLE_BYTES)()
+            N.check(N.lib.bd3mg_peer_alloc(max(1, plan.ring_planes[q] * int(np.prod(x.shape[1:])))
+                                           * x.element_size(), C.byref(ptr), h))
+            ptrs.append(ptr.value)
+            hub.own.append(ptr.value)
+        bases = dict(enumerate(ptrs))
+        rings = [PeerRing(plan, q, x, z0, ptrs[q], bases, flags, fdev) for q, (x, z0) in enumerate(zip(xs, z0s))]
+        return hub, rings
+
+    @classmethod
+    def ipc(cls, plan: RingPlan, rank: int, x: torch.Tensor, z0: int, group=None) -> tuple["RingHub", PeerRing]:
+        import ctypes as C
+        import os
+        import uuid
+
+        from . import _native as N
+        hub = cls()
+        world = plan.layout.world
+        name = [f"/dev/shm/bd3mg_async_{uuid.uuid4().hex}" if rank == 0 else None]
+        dist.broadcast_object_list(name, src=0, group=group)
+        hub.path = name[0]
+        nbytes = plan.nflags * 8
+        if rank == 0:
+            fd = os.open(hub.path, os.O_RDWR | os.O_CREAT | os.O_EXCL, 0o600)
+            os.ftruncate(fd, max(4096, -(-nbytes // 4096) * 4096))
+            os.close(fd)
+        dist.barrier(group=group)
+        hub.mm, flags, hub.host, fdev = _map_flags(hub.path, nbytes)
+        ptr, h = C.c_void_p(), (C.c_ubyte * N.IPC_HANDLE_BYTES)()
+        N.check(N.lib.bd3mg_peer_alloc(max(1, plan.ring_planes[rank] * int(np.prod(x.shape[1:]))) * x.element_size(),
+                                       C.byref(ptr), h))
+        hub.own.append(ptr.value)
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        bases = {rank: ptr.value}
+        for q in sorted({q for p, q, _, _, _ in plan.units if p == rank}):
+            dp = C.c_void_p()
+            N.check(N.lib.bd3mg_peer_open((C.c_ubyte * N.IPC_HANDLE_BYTES).from_buffer_copy(handles[q]),
+                                          C.byref(dp)))
+            bases[q] = dp.value
+            hub.opened.append(dp.value)
+        ring = PeerRing(plan, rank, x, z0, ptr.value, bases, flags, fdev)
+        torch.cuda.synchronize()  # slot 0 of every ring written before anyone reads it
+        dist.barrier(group=group)
+        return hub, ring
+
+    def close(self, group=None) -> None:
+        from . import _native as N
+        torch.cuda.synchronize()
+        if self.path is not None and dist.is_initialized():
+            dist.barrier(group=group)  # no rank still writes into a ring or a flag
+        for p in self.opened:
+            N.lib.bd3mg_peer_close(p)
+        for p in self.own:
+            N.lib.bd3mg_peer_free(p)
+        self.opened, self.own = [], []
+        if self.host:
+            N.lib.bd3mg_host_unregister(self.host)
+            self.host = 0
+        if self.path is not None:
+            try:
+                import os
+                os.unlink(self.path)
+            except FileNotFoundError:
+                pass
+            self.path = None
+
+
 def cuda_block_step(obj, dtype: torch.dtype = torch.float64):
     """Fused in-place block step on the shard's local slab (bd3mg_mg_steps;
     the observation is the device copy of the full y)."""
     from . import _native as N
     from .directions import mg_steps_device
 
-    def step(shard: AsyncShard, block: SliceBlock) -> None:
+    def step(shard: AsyncShard, block: SliceBlock, mirrors=None) -> None:
         z0 = shard.l_lo
         rows = slice(block.z_lo - z0, block.z_hi - z0 + 1)
         task = N.Task(shard.x.data_ptr(), z0, shard.x.shape[0], block.z_lo, block.z_hi,
                       shard.prev[rows].data_ptr(), None, shard.x[rows].data_ptr(), shard.prev[rows].data_ptr())
-        info = mg_steps_device(obj, [task], dtype)
+        info = mg_steps_device(obj, [task], dtype, mirrors=mirrors)
         shard.infos.append(info)
 
     return step
@@ -669,10 +936,11 @@ class _NoPeers:
 
 class AsyncEngine:
     """bench/runtime driver of the asynchronous mode on this rank: one
-    ``sweep()`` = one pass over the rank's own blocks, no global barrier."""
+    ``sweep()`` = one pass over the rank's own blocks, no global barrier.
+    halo="p2p": peer halo rings (PeerRing); "nccl": TorchP2P messages."""
 
     def __init__(self, obj, x0, block_height: int, dtype: torch.dtype = torch.float64, max_delay: int = 2,
-                 group=None):
+                 group=None, halo: str = "p2p"):
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.layout = SlabLayout.build(obj.dims.nz, obj.psf.kdims.kz, block_height, world)
@@ -680,7 +948,14 @@ class AsyncEngine:
         dev = torch.device("cuda", torch.cuda.current_device())
         x = torch.from_numpy(np.ascontiguousarray(x0[lo:hi + 1], dtype=np.float64)).to(dev).to(dtype).contiguous()
         prev = torch.zeros_like(x)
-        net = TorchP2P(x, lo, self.layout.transfers(rank), group) if world > 1 else _NoPeers()
+        self.hub = None
+        if world == 1:
+            net = _NoPeers()
+        elif halo == "p2p":
+            self.hub, net = RingHub.ipc(RingPlan(self.layout, ring_slots(max_delay)), rank, x, lo, group)
+        else:
+            net = TorchP2P(x, lo, self.layout.transfers(rank), group)
+        self.group = group
         self.shard = AsyncShard(self.layout, rank, x, prev, net, cuda_block_step(obj, dtype), max_delay)
         self.x = x
         self.nblocks_local = len(self.shard.blocks)
@@ -708,3 +983,6 @@ class AsyncEngine:
 
     def finish(self) -> None:
         self.shard.net.finish()
+        if self.hub is not None:
+            self.hub.close(self.group)
+            self.hub = None

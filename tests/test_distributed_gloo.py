@@ -174,3 +174,25 @@ def test_p2p_inbox_plan():
             assert all(covered[i][1] == covered[i + 1][0] for i in range(len(covered) - 1))
         with pytest.raises(ValueError):
             PeerHalo.inbox_offset(lay, 0, 0, 0, 0)
+
+
+def test_ring_plan_units_tile_the_halos():
+    """Async peer rings: the units of every reader tile its halo planes, each
+    writer block publishes within the flag limit, ring slots do not overlap."""
+    from paper_2002_02328_b200._native import MAX_FLAGS
+    from paper_2002_02328_b200.distributed import RingPlan, ring_slots
+    for nz, kz, h, world in [(64, 11, 8, 8), (64, 11, 8, 2), (24, 5, 2, 4), (30, 7, 4, 3), (256, 15, 8, 8)]:
+        lay = SlabLayout.build(nz, kz, h, world)
+        plan = RingPlan(lay, ring_slots(2))
+        for q in range(world):
+            l_lo, l_hi = lay.local(q)
+            o_lo, o_hi = lay.owned(q)
+            got = sorted(z for p, r, bi, a, c in plan.units if r == q for z in range(a, c + 1))
+            assert got == [z for z in range(l_lo, l_hi + 1) if not o_lo <= z <= o_hi]
+            spans = sorted((plan.slot_plane(u, v), plan.slot_plane(u, v) + plan.units[u][4] - plan.units[u][3] + 1)
+                           for u in range(len(plan.units)) if plan.units[u][1] == q for v in range(plan.slots))
+            assert all(spans[i][1] <= spans[i + 1][0] for i in range(len(spans) - 1))
+            assert not spans or spans[-1][1] <= plan.ring_planes[q]
+        for p in range(world):
+            for bi in range(len(lay.owned_blocks(p))):
+                assert len(plan.writes(p, bi)) + 1 <= MAX_FLAGS
