@@ -57,7 +57,10 @@ struct Ws {
   template <typename U>
   U* take(size_t n) {
     off = (off + 255) & ~size_t(255);
-    U* p = measure ? nullptr : reinterpret_cast<U*>(base + off);
+    // measure mode hands out non-null placeholders: callers branch on
+    // pointers (e.g. the recorder's residual sum), so sizing must see the
+    // same pointers as the real call; they are never dereferenced
+    U* p = measure ? reinterpret_cast<U*>(uintptr_t(4096) + off) : reinterpret_cast<U*>(base + off);
     off += n * sizeof(U);
     return p;
   }
@@ -79,6 +82,10 @@ __global__ void publish_kernel(const __grid_constant__ PubArgs a) {
     *a.word[i] = a.value[i];
   }
   __threadfence_system();
+}
+
+int ws_fail(const Ws& ws) {
+  return fail(BD3MG_EWORKSPACE, "workspace too small: %zu bytes needed, %zu given", ws.off, ws.cap);
 }
 
 bool odd_pos(int64_t k) { return k >= 1 && (k % 2) == 1; }
@@ -285,7 +292,7 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   T* greg = ws.take<T>(h * plane);
   double* parts = ws.take<double>(conv_rows<T>(g, M_RESID, nr));
   if (ws.measure) return BD3MG_OK;
-  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  if (!ws.ok()) return ws_fail(ws);
   {
     StArgs<T> sa = st_args<T>(g, r);
     sa.njobs = 1;
@@ -331,7 +338,7 @@ int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   double* eparts = ws.take<double>((size_t)erows * kEvalNV);
   double* sums = ws.take<double>(8);
   if (ws.measure) return BD3MG_OK;
-  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  if (!ws.ok()) return ws_fail(ws);
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
   a.partials = parts;
@@ -367,7 +374,7 @@ int majorant_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   const int64_t nr = o_hi - o_lo + 1, h = hi - lo + 1;
   T* hv = ws.take<T>(nr * plane);
   if (ws.measure) return BD3MG_OK;
-  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  if (!ws.ok()) return ws_fail(ws);
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
   a.jobs[0].src0 = v; a.jobs[0].src_z0 = lo; a.jobs[0].src_nz = (int)h;
@@ -530,7 +537,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   const long long reg_rows = (long long)nt * z_tiles<T>(g);  // one partial row per (block, tile)
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
   if (ws.measure) return BD3MG_OK;
-  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  if (!ws.ok()) return ws_fail(ws);
 
   // (1) r = H x - y
   {
@@ -822,7 +829,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   SideStream* ss = nullptr;
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
   if (!ws.measure) {
-    if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+    if (!ws.ok()) return ws_fail(ws);
     if (fused && !getenv("BD3MG_NO_SIDE_STREAM")) {
       CU(side_stream(s, &ss));
       opt.ss = ss;
@@ -864,7 +871,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   int rc = mg_steps_chunk<T>(g, r, K, y, tasks.data(), nb, info, sub, s, opt);
   ws.off = sub.off;
   if (rc != BD3MG_OK || ws.measure) return rc;
-  if (!ws.ok()) return fail(BD3MG_EWORKSPACE, "workspace too small");
+  if (!ws.ok()) return ws_fail(ws);
   eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;

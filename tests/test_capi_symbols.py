@@ -60,3 +60,24 @@ def test_sm100a_code_present():
     out = subprocess.run(["cuobjdump", "-sass", str(LIB)], capture_output=True, text=True).stdout
     assert "sm_100a" in out or "SM100" in out.upper()
     assert "UTMALDG" in out and "DFMA" in out
+
+
+def test_sharded_fp32_workspace_sizing():
+    """Regression: an fp32 rank whose residual rows split around its recorder
+    rows into odd-length jobs (two-plane kernel) needs more partial rows than
+    one job; the size query must see the same split as the call (it once
+    measured with a null recorder pointer and came out 3 KB short)."""
+    import ctypes as C
+
+    from paper_2002_02328_b200 import _native as N
+    from paper_2002_02328_b200.distributed import SlabLayout
+    g = N.Geom(512, 512, 128, 7, 7, 15, N.BD3MG_F32)
+    lay = SlabLayout.build(128, 15, 16, 8)
+    bl = lay.owned_blocks(1)
+    (o_lo, o_hi), (l_lo, l_hi) = lay.owned(1), lay.local(1)
+    barr = (C.c_int64 * 2)(bl[0].z_lo, bl[0].z_hi)
+    with_rec = N.Sweep(1 << 30, 1 << 31, l_lo, l_hi - l_lo + 1, barr, 1, o_lo, o_hi, 1 << 32, None)
+    no_rec = N.Sweep(1 << 30, 1 << 31, l_lo, l_hi - l_lo + 1, barr, 1, 0, -1, None, None)
+    a = N.lib.bd3mg_jacobi_sweep_ws_bytes(C.byref(g), C.byref(with_rec))
+    b = N.lib.bd3mg_jacobi_sweep_ws_bytes(C.byref(g), C.byref(no_rec))
+    assert a >= 82051328 and a > b
