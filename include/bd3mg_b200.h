@@ -82,6 +82,11 @@ const char* bd3mg_version(void);
 /* Number of kernels this library has launched in the process (eager calls;
  * a captured CUDA graph's replays are not counted). */
 long long bd3mg_launch_count(void);
+/* The library's own CUDA runtime is bound to the device of the caller's
+ * streams with bd3mg_set_device (cudaSetDevice); the Python layer does it
+ * whenever the device of the stream it passes changes. */
+int bd3mg_set_device(int device);
+int bd3mg_get_device(int* device);
 
 /* ---- drop-in native core: replaces bd3mg._core (src/_core.pyx:17-96) ---- */
 /* H rows: out[i] = sum_{a,b,c} K[zo,a,b,c] frag[zo+a-rz-frag_z0, y+b-ry, x+c-rx],

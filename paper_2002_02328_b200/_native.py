@@ -21,7 +21,7 @@ EVAL_DOUBLES = 7
 
 # every symbol the header declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
-    "bd3mg_last_error", "bd3mg_version", "bd3mg_launch_count",
+    "bd3mg_last_error", "bd3mg_version", "bd3mg_launch_count", "bd3mg_set_device", "bd3mg_get_device",
     "bd3mg_depthvar_correlate_f64", "bd3mg_depthvar_correlate_adjoint_f64",
     "bd3mg_depthvar_correlate_f32", "bd3mg_depthvar_correlate_adjoint_f32",
     "bd3mg_depthvar_correlate_host_f64", "bd3mg_depthvar_correlate_adjoint_host_f64",
@@ -99,6 +99,8 @@ def _load() -> C.CDLL:
     lib.bd3mg_last_error.restype = C.c_char_p
     lib.bd3mg_version.restype = C.c_char_p
     lib.bd3mg_launch_count.restype = C.c_longlong
+    lib.bd3mg_set_device.argtypes = [C.c_int]
+    lib.bd3mg_get_device.argtypes = [C.POINTER(C.c_int)]
     lib.bd3mg_grad_rows_ws_bytes.argtypes = [G, _i64, _i64]
     lib.bd3mg_grad_rows_ws_bytes.restype = _sz
     lib.bd3mg_grad_rows.argtypes = [G, R, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]

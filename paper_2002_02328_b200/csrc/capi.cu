@@ -930,6 +930,19 @@ extern "C" {
 
 const char* bd3mg_last_error(void) { return g_err.c_str(); }
 const char* bd3mg_version(void) { return "bd3mg_b200 0.1 sm_100a"; }
+
+// This library links its own (static) CUDA runtime: its notion of the
+// calling thread's current device is bound explicitly to the device of the
+// caller's stream (one process per GPU: rank r on device r).
+int bd3mg_set_device(int device) {
+  CU(cudaSetDevice(device));
+  return BD3MG_OK;
+}
+int bd3mg_get_device(int* device) {
+  if (!device) return fail(BD3MG_EINVAL, "null argument");
+  CU(cudaGetDevice(device));
+  return BD3MG_OK;
+}
 long long bd3mg_launch_count(void) { return g_launches.load(); }
 
 int bd3mg_depthvar_correlate_f64(const double* frag, int64_t nzf, int64_t ny, int64_t nx, const double* kernels,

@@ -50,8 +50,21 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+_bound = threading.local()
+
+
+def bind(device: int) -> None:
+    """Point the library's own CUDA runtime at `device` for this thread
+    (it links cudart statically, so torch.cuda.set_device alone is not its
+    state)."""
+    if getattr(_bound, "dev", None) != device:
+        N.check(N.lib.bd3mg_set_device(device))
+        _bound.dev = device
+
+
 def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
     s = stream or torch.cuda.current_stream()
+    bind(s.device.index if s.device.index is not None else torch.cuda.current_device())
     return s.cuda_stream
 
 

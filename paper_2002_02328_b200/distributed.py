@@ -141,6 +141,8 @@ class PeerHalo:
         self.esz = shard.x.element_size()
         n = max(1, 2 * self.nplanes * self.plane)
         ptr, self.handle = C.c_void_p(), (C.c_ubyte * N.IPC_HANDLE_BYTES)()
+        from . import device as D
+        D.bind(shard.x.device.index)
         N.check(N.lib.bd3mg_peer_alloc(n * self.esz, C.byref(ptr), self.handle))
         self.ptr = ptr.value
         self.opened: list[int] = []
@@ -714,6 +716,8 @@ def _map_flags(path: str | None, nbytes: int):
             mm = mmap.mmap(fd, nbytes)
         finally:
             os.close(fd)
+    from . import device as D
+    D.bind(torch.cuda.current_device())
     words = np.frombuffer(mm, dtype=np.int64)
     host = C.addressof(C.c_char.from_buffer(mm))
     dev = C.c_void_p()
