@@ -539,6 +539,21 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return ws_fail(ws);
 
+  // (0) block steps with a side stream (mg_steps): the regulariser gradient
+  // needs x only, so it runs next to the residual correlation
+  const bool greg_side = opt.ss && !pre;
+  if (greg_side) {
+    CU(hop(s, opt.ss->side, opt.ss->ev[0]));
+    StArgs<T> sa = st_args<T>(g, r);
+    sa.njobs = nt;
+    for (int t = 0; t < nt; ++t) {
+      StJob<T>& J = sa.jobs[t];
+      J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
+      J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi; J.out0 = grb[t]; J.out1 = wb[t];
+    }
+    int rc = launch_greg<T>(sa, false, opt.ss->side);
+    if (rc) return rc;
+  }
   // (1) r = H x - y
   {
     ConvArgs<T> a = base_args<T>(g, r, K);
@@ -567,7 +582,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   // join the recorder / regulariser-gradient stencil of the side stream
   if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
   // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
-  if (!pre) {
+  if (!pre && !greg_side) {
     StArgs<T> sa = st_args<T>(g, r);
     sa.njobs = nt;
     for (int t = 0; t < nt; ++t) {
@@ -744,6 +759,17 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   StepOpts<T> opt;
   opt.mirrors = mirrors;
   opt.nmirrors = nmirrors;
+  // eager block steps overlap the stencils on a side stream (measured: async
+  // mode at C2 8040 -> 8880 block-it/s); inside a graph capture the extra
+  // branch costs more than it hides for one-block steps (cyclic sweep 7985 ->
+  // 7597), so captured calls stay on one stream
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!ws.measure) CU(cudaStreamIsCapturing(s, &cap));
+  if (!ws.measure && cap == cudaStreamCaptureStatusNone && !getenv("BD3MG_NO_SIDE_STREAM")) {
+    SideStream* ss = nullptr;
+    CU(side_stream(s, &ss));
+    opt.ss = ss;
+  }
   // tasks run in launches of kMaxJobs; an in-place update of one launch would
   // move the anchor of the next, so in-place calls are limited to one launch
   if (ntasks > kMaxJobs)

@@ -14,7 +14,7 @@ constexpr int kInfoNV = 16;          // doubles of StepInfo per block
 // ---------------------------------------------------------------------------
 // Deterministic final reduction: out[j*nv + k] = sum_{r in [begin_j, end_j)}
 // rows[r*nv + k], each thread summing a fixed stride class in order, then a
-// fixed tree.  One CTA per job.
+// fixed tree (cta_sum_rows).  One CTA per job.
 struct RowRanges {
   int njobs;
   long long begin[kMaxJobs];
@@ -22,10 +22,14 @@ struct RowRanges {
 };
 
 constexpr int kRedMaxNV = 12;
-// Deterministic CTA sum of rows[begin:end, 0:nv] (fixed stride classes, then
-// a fixed tree).  Result in res[0:nv] for every thread (after the barrier).
+// Deterministic CTA sum of rows[begin:end, 0:nv]: fixed stride classes per
+// thread, a butterfly over the warp (a + b == b + a bitwise, so every lane
+// holds the same sum), then the 8 warp sums in warp order.  Result in
+// res[0:nv] for every thread (after the barrier).  Latency: 5 shuffles and
+// one barrier instead of an 8-level shared-memory tree.
 __device__ __forceinline__ void cta_sum_rows(const double* __restrict__ rows, int nv, long long begin,
-                                             long long end, double (*s)[kEwNT], double* res) {
+                                             long long end, double (*s)[kEwNT / 32], double* res) {
+  constexpr int NW = kEwNT / 32;
   double acc[kRedMaxNV];
 #pragma unroll
   for (int k = 0; k < kRedMaxNV; ++k) acc[k] = 0.0;
@@ -35,22 +39,35 @@ __device__ __forceinline__ void cta_sum_rows(const double* __restrict__ rows, in
       if (k < nv) acc[k] += rows[r * nv + k];
   }
 #pragma unroll
-  for (int k = 0; k < kRedMaxNV; ++k)
-    if (k < nv) s[k][threadIdx.x] = acc[k];
-  __syncthreads();
-  for (int w = kEwNT / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w)
-      for (int k = 0; k < nv; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + w];
-    __syncthreads();
+  for (int k = 0; k < kRedMaxNV; ++k) {
+    if (k < nv) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+    }
   }
-  for (int k = 0; k < nv; ++k) res[k] = s[k][0];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kRedMaxNV; ++k)
+      if (k < nv) s[k][warp] = acc[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kRedMaxNV; ++k) {
+    if (k < nv) {
+      double t = s[k][0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) t += s[k][w];
+      res[k] = t;
+    }
+  }
   __syncthreads();
 }
 
 __global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
                                                             const __grid_constant__ RowRanges rr,
                                                             double* __restrict__ out, int out_stride) {
-  __shared__ double s[kRedMaxNV][kEwNT];
+  __shared__ double s[kRedMaxNV][kEwNT / 32];
   double res[kRedMaxNV];
   const int j = blockIdx.x;
   cta_sum_rows(rows, nv, rr.begin[j], rr.end[j], s, res);
@@ -143,7 +160,7 @@ __global__ void __launch_bounds__(kEwNT) reduce_solve_kernel(const __grid_consta
                                                              const double* __restrict__ gram_rows,
                                                              const double* __restrict__ reg_rows,
                                                              double* __restrict__ info) {
-  __shared__ double s[kRedMaxNV][kEwNT];
+  __shared__ double s[kRedMaxNV][kEwNT / 32];
   const int j = blockIdx.x;
   double D[kRedMaxNV], R[kRedMaxNV];
   cta_sum_rows(gram_rows, p.nv_gram, p.g_begin[j], p.g_end[j], s, D);
