@@ -46,10 +46,14 @@ struct GregGeo {
   static constexpr int BH = (kTmY + 2 + ROWQ - 1) / ROWQ * ROWQ;
   static constexpr int PL = BW * BH;
   static constexpr int RING = 4;  // z-1, z, z+1 resident, z+2 in flight
-  static constexpr int PP = kTmX + 1;  // px/py region cols x0-1 .. x0+31
+  // w*dx / w*dy exchange: the left neighbour's px comes from lane-1 (shuffle),
+  // the upper neighbour's py from the thread's previous row; shared memory
+  // only holds the halo row (py, y0-1), the halo column (px, x0-1) and each
+  // warp's last row (py), so 7 CTAs fit an SM (one wave at 256 x 256 x 64)
+  static constexpr int NW = kTmNT / 32;
+  static constexpr int HALO = kTmX + kTmY + NW * kTmX;
   static constexpr size_t smem() {
-    return 128 + (size_t)RING * PL * sizeof(T) + 2 * (size_t)(kTmY + 1) * PP * sizeof(T) +
-           (kTmNT / 32) * kEvalNV * 8 + RING * 8;
+    return 128 + (size_t)RING * PL * sizeof(T) + (size_t)HALO * sizeof(T) + (kTmNT / 32) * kEvalNV * 8 + RING * 8;
   }
 };
 
@@ -77,13 +81,14 @@ template <typename T, bool EVAL>
 __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ StArgs<T> p,
                                                        const __grid_constant__ StTma<T> tm) {
   using G = GregGeo<T>;
-  constexpr int VEC = G::VEC, PP = G::PP;
+  constexpr int VEC = G::VEC;
   extern __shared__ __align__(128) unsigned char st_smem[];
   unsigned char* base = st_smem + ((128 - (smem_u32(st_smem) & 127)) & 127);
   T (*xs)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base);
-  T* pxs = reinterpret_cast<T*>(base + G::RING * G::PL * sizeof(T));
-  T* pys = pxs + (kTmY + 1) * PP;
-  double* red = reinterpret_cast<double*>(pys + (kTmY + 1) * PP);
+  T* hpy = reinterpret_cast<T*>(base + G::RING * G::PL * sizeof(T));  // py of row y0-1, cols x0..x0+31
+  T* hpx = hpy + kTmX;                                                // px of col x0-1, rows y0..y0+15
+  T* lastpy = hpx + kTmY;                                             // [warp][lane]: py of the warp's last row
+  double* red = reinterpret_cast<double*>(lastpy + G::NW * kTmX);
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kEvalNV);
 
   const int job = blockIdx.z;
@@ -115,10 +120,11 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
   const T xmin = (T)p.x_min, xmax = (T)p.x_max;
   const int x = x0 + lane;
   double ev[kEvalNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  // extra px/py item of this thread: region row 0 (c = 0..32) or column 0 (r = 1..16)
-  constexpr int NEXTRA = PP + kTmY;
-  const int er = threadIdx.x < PP ? 0 : threadIdx.x - PP + 1;
-  const int ec = threadIdx.x < PP ? threadIdx.x : 0;
+  // halo item of this thread: threads 0..31 the py of (y0-1, x0+t), threads
+  // 32..47 the px of (y0+t-32, x0-1)
+  constexpr int NEXTRA = kTmX + kTmY;
+  const int er = threadIdx.x < kTmX ? 0 : threadIdx.x - kTmX + 1;   // region row (0 = y0-1)
+  const int ec = threadIdx.x < kTmX ? threadIdx.x + 1 : 0;          // region col (0 = x0-1)
   const int ey = y0 - 1 + er, ex = x0 - 1 + ec;
 
   for (int z = J.lo; z <= J.hi; ++z) {
@@ -148,13 +154,12 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
       const T w = rsqrt(sq);
       px[j] = mul_rn(w, dx);
       py[j] = mul_rn(w, dy);
-      pxs[(ly + 1) * PP + lane + 1] = px[j];
-      pys[(ly + 1) * PP + lane + 1] = py[j];
       if (y < ny && x < nx) {
         J.out1[orow + (long long)y * nx + x] = w;
         if constexpr (EVAL) ev[1] += (double)sq * (double)w;
       }
     }
+    lastpy[warp * kTmX + lane] = py[kTmR - 1];
     if (threadIdx.x < NEXTRA) {
       T ex_px = T(0), ex_py = T(0);
       if (ey >= 0 && ex >= 0 && ey < ny && ex < nx) {
@@ -166,9 +171,13 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
         ex_px = mul_rn(w, dx);
         ex_py = mul_rn(w, dy);
       }
-      pxs[er * PP + ec] = ex_px;
-      pys[er * PP + ec] = ex_py;
+      if (threadIdx.x < kTmX) hpy[threadIdx.x] = ex_py;
+      else hpx[er - 1] = ex_px;
     }
+    // left neighbours' px: lane - 1 (all lanes shuffle before any predication)
+    T pxl[kTmR];
+#pragma unroll
+    for (int j = 0; j < kTmR; ++j) pxl[j] = __shfl_up_sync(0xffffffffu, px[j], 1);
     __syncthreads();
     // pass 2: box + TV divergence + axial terms
     const T* xm_t = xs[slot(max(z - 1, zfirst))];
@@ -181,7 +190,8 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
       const int si = (ly + 1) * G::BW + lane + VEC;
       const T clipped = xc[j] < xmin ? xmin : (xc[j] > xmax ? xmax : xc[j]);
       const T box = mul_rn(two_eta, sub_rn(xc[j], clipped));
-      const T pxm = pxs[(ly + 1) * PP + lane], pym = pys[ly * PP + lane + 1];
+      const T pxm = lane > 0 ? pxl[j] : hpx[ly];
+      const T pym = j > 0 ? py[j - 1] : (warp > 0 ? lastpy[(warp - 1) * kTmX + lane] : hpy[lane]);
       const T tvx = (nx == 1) ? T(0) : sub_rn(pxm, px[j]);
       const T tvy = (ny == 1) ? T(0) : sub_rn(pym, py[j]);
       const T xzp = has_p ? xp_t[si] : T(0);
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
         }
       }
     }
-    __syncthreads();  // px/py rewritten and the slot of z-1 refilled next iteration
+    __syncthreads();  // halo px/py rewritten and the slot of z-1 refilled next iteration
   }
   if constexpr (EVAL) {
     cta_reduce<kEvalNV, kTmNT>(ev, red);
