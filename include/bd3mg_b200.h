@@ -201,6 +201,18 @@ int bd3mg_jacobi_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* 
                        const bd3mg_sweep_t* sw, double* terms_out, double* info_out, void* ws, size_t ws_bytes,
                        void* stream);
 
+/* Variant "hd-incremental" of the sweep (cached H d_mem +
+ * incremental residual).  `resid` (device, nz*ny*nx elements of the dtype)
+ * holds r = H x - y of the current anchor; the call keeps it current by
+ * linearity, r += sum_b H E_b inc_b, from the hd-cache rows it updates, so no
+ * residual correlation runs.  refresh != 0 recomputes r exactly (required on
+ * the first call; periodic refreshes bound the rounding drift).  Needs
+ * sw->hd_cache and blocks tiling the whole volume on this device; same
+ * workspace as bd3mg_jacobi_sweep. */
+int bd3mg_jacobi_sweep_incremental(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                                   const bd3mg_sweep_t* sw, void* resid, int refresh, double* terms_out,
+                                   double* info_out, void* ws, size_t ws_bytes, void* stream);
+
 /* Sharded sweep with the halo exchange fused into the in-place update: the
  * updated iterate rows [z_lo, z_hi] (global depths, each inside one of the
  * sweep's blocks) are ALSO stored to dst (plane z_lo first), typically a

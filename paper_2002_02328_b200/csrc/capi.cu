@@ -452,7 +452,11 @@ struct StepOpts {
   SideStream* ss = nullptr;    // run reg_gram next to the Gram correlation
   const bd3mg_mirror_t* mirrors = nullptr;  // rows of the updated iterate also stored to (peer) buffers
   int nmirrors = 0;
+  T* r_full = nullptr;         // variant "hd-incremental": r = Hx - y kept across calls (plane 0 = r_full_z0)
+  int64_t r_full_z0 = 0;
+  bool r_refresh = false;      // recompute r_full exactly in this call
 };
+constexpr int kSumsqCtas = 4 * 148;  // fixed grid of the recorder's sum of squares (deterministic)
 
 template <typename T>
 int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
@@ -483,7 +487,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   if (shared) {
     u_lo = *std::min_element(olo.begin(), olo.end());
     u_hi = *std::max_element(ohi.begin(), ohi.end());
-    T* ru = ws.take<T>((u_hi - u_lo + 1) * plane);
+    T* ru = opt.r_full ? opt.r_full + (u_lo - opt.r_full_z0) * plane : ws.take<T>((u_hi - u_lo + 1) * plane);
     for (int t = 0; t < nt; ++t) { rb[t] = ru; r_z0[t] = u_lo; r_n[t] = u_hi - u_lo + 1; }
     resid_work = u_hi - u_lo + 1;
   } else {
@@ -530,7 +534,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   for (int t = 0; t < nt; ++t) gram_rows += conv_rows<T>(g, gmode, ohi[t] - olo[t] + 1);
   (void)resid_work;
   (void)gram_work;
-  const long long conv_part_rows = std::max(resid_rows, gram_rows);
+  const long long conv_part_rows = std::max<long long>(std::max(resid_rows, gram_rows), kSumsqCtas);
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   long long hsum = 0;
   for (int t = 0; t < nt; ++t) hsum += h[t];
@@ -554,8 +558,21 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     int rc = launch_greg<T>(sa, false, opt.ss->side);
     if (rc) return rc;
   }
-  // (1) r = H x - y
-  {
+  // (1) r = H x - y (variant "hd-incremental": kept from the previous call
+  // unless refreshed; the recorder's data term is then a sum of squares)
+  if (opt.r_full && !opt.r_refresh) {
+    if (opt.resid_sq) {
+      if (opt.rec_hi >= opt.rec_lo) {
+        sumsq_kernel<T><<<kSumsqCtas, kEwNT, 0, s>>>(rb[0] + (opt.rec_lo - u_lo) * plane,
+                                                     (opt.rec_hi - opt.rec_lo + 1) * plane, cparts);
+        launched();
+        CU(cudaGetLastError());
+        CU(reduce(cparts, 1, {{0, kSumsqCtas}}, opt.resid_sq, 1, s));
+      } else {
+        CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
+      }
+    }
+  } else {
     ConvArgs<T> a = base_args<T>(g, r, K);
     a.partials = cparts;
     a.njobs = (int)rjobs.size();
@@ -729,7 +746,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
 #endif
     CU(cudaGetLastError());
   }
-  // (8) cached H E_S d_mem for the next visit (variant "hd-cache")
+  // (8) cached H E_S d_mem for the next visit (variant "hd-cache"), and the
+  // maintained residual (variant "hd-incremental")
   if (cached) {
     HdArgs<T> ha;
     memset(&ha, 0, sizeof(ha));
@@ -743,6 +761,17 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     }
     hd_update_kernel<T><<<dim3(mc, nt), kEwNT, 0, s>>>(ha, info_out); launched();
     CU(cudaGetLastError());
+    if (opt.r_full) {
+      RIncArgs<T> ra;
+      memset(&ra, 0, sizeof(ra));
+      ra.r = opt.r_full; ra.plane = plane; ra.r_z0 = (int)opt.r_full_z0;
+      ra.u_lo = (int)u_lo; ra.u_hi = (int)u_hi; ra.nblocks = nt;
+      for (int t = 0; t < nt; ++t) { ra.hd[t] = opt.hd[t]; ra.olo[t] = (int)olo[t]; ra.ohi[t] = (int)ohi[t]; }
+      const long long n = (u_hi - u_lo + 1) * plane;
+      const int ctas = (int)std::max<long long>(1, std::min<long long>((n + 4 * kEwNT - 1) / (4 * kEwNT), 8 * 148));
+      resid_inc_kernel<T><<<ctas, kEwNT, 0, s>>>(ra, info_out); launched();
+      CU(cudaGetLastError());
+    }
   }
   return BD3MG_OK;
 }
@@ -799,7 +828,7 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
 template <typename T>
 int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_sweep_t* sw,
                       double* terms, double* info, Ws& ws, cudaStream_t s, const bd3mg_mirror_t* mirrors = nullptr,
-                      int nmirrors = 0) {
+                      int nmirrors = 0, T* r_full = nullptr, bool r_refresh = false) {
   if (!sw || sw->nblocks < 1 || sw->nblocks > kMaxJobs)
     return fail(BD3MG_EINVAL, "jacobi sweep needs 1..%d blocks", kMaxJobs);
   const int64_t plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
@@ -851,6 +880,15 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     if (!mirrors[j].dst || mirrors[j].z_hi < mirrors[j].z_lo) return fail(BD3MG_EINVAL, "invalid mirror %d", j);
   opt.mirrors = mirrors;
   opt.nmirrors = nmirrors;
+  if (r_full) {
+    // every residual row must be one this device's blocks update
+    if (!sw->hd_cache) return fail(BD3MG_EINVAL, "the incremental residual needs the hd cache");
+    if (sw->frag_z0 != 0 || sw->nzf != g->nz || !contiguous || bmin != 0 || bmax != g->nz - 1)
+      return fail(BD3MG_EINVAL, "the incremental residual needs blocks tiling the whole volume on one device");
+    opt.r_full = r_full;
+    opt.r_full_z0 = 0;
+    opt.r_refresh = r_refresh;
+  }
   if (fused) { opt.greg = grb.data(); opt.omega = wb.data(); }
   SideStream* ss = nullptr;
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
@@ -1229,6 +1267,21 @@ int bd3mg_jacobi_sweep_mirrored(const bd3mg_geom_t* g, const bd3mg_reg_t* r, con
                                               ws, s, mirrors, nmirrors),
                     jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
                                              s, mirrors, nmirrors));
+}
+
+int bd3mg_jacobi_sweep_incremental(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                                   const bd3mg_sweep_t* sw, void* resid, int refresh, double* terms_out,
+                                   double* info_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !sw || !info_out || !terms_out || !resid) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  return DISPATCH_T(g,
+                    jacobi_sweep_impl<double>(g, r, (const double*)kernels, (const double*)y, sw, terms_out, info_out,
+                                              ws, s, nullptr, 0, (double*)resid, refresh != 0),
+                    jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
+                                             s, nullptr, 0, (float*)resid, refresh != 0));
 }
 
 /* ---- peer (NVLink) memory: halo inboxes written by other ranks' kernels ---- */

@@ -336,6 +336,57 @@ __global__ void __launch_bounds__(kEwNT) hd_update_kernel(const __grid_constant_
     B.hd[i] = add_rn(mul_rn(-B.hg[i], cg), mul_rn(B.hd[i], cd));
 }
 
+// Variant "hd-incremental": the residual r = H x - y of the anchor is kept
+// across sweeps by linearity, r += sum_b H E_b inc_b, from the hd-cache rows
+// the step has just updated (hd_b = H E_b inc_b over rows [olo_b, ohi_b]);
+// contributions of overlapping blocks are added in block order.  A block
+// whose gradient was non-finite applied nothing and adds nothing.
+template <typename T>
+struct RIncArgs {
+  T* r;  // plane 0 = depth r_z0
+  long long plane;
+  int r_z0, u_lo, u_hi, nblocks;
+  const T* hd[kMaxJobs];
+  int olo[kMaxJobs], ohi[kMaxJobs];
+};
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) resid_inc_kernel(const __grid_constant__ RIncArgs<T> p,
+                                                           const double* __restrict__ info) {
+  const long long n = (long long)(p.u_hi - p.u_lo + 1) * p.plane;
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < n; i += (long long)gridDim.x * kEwNT) {
+    const int z = p.u_lo + (int)(i / p.plane);
+    const long long q = i - (long long)(z - p.u_lo) * p.plane;
+    T* rp = p.r + (long long)(z - p.r_z0) * p.plane + q;
+    T v = *rp;
+    for (int b = 0; b < p.nblocks; ++b)
+      if (z >= p.olo[b] && z <= p.ohi[b] && info[b * kInfoNV + 8] == 0.0)
+        v = add_rn(v, p.hd[b][(long long)(z - p.olo[b]) * p.plane + q]);
+    *rp = v;
+  }
+}
+
+// Sum of squares of n elements, one partial per CTA (fixed grid, fixed
+// per-thread order, warp butterfly: deterministic).
+template <typename T>
+__global__ void __launch_bounds__(kEwNT) sumsq_kernel(const T* __restrict__ a, long long n,
+                                                       double* __restrict__ partials) {
+  __shared__ double s[kEwNT / 32];
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * kEwNT + threadIdx.x; i < n; i += (long long)gridDim.x * kEwNT) {
+    const double v = (double)a[i];
+    acc += v * v;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = s[0];
+    for (int w = 1; w < kEwNT / 32; ++w) t += s[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
 // receive_update's block write (scheduler.py:151-153): x += inc; d_mem = inc.
 template <typename T>
 __global__ void __launch_bounds__(kEwNT) apply_increment_kernel(T* __restrict__ x, T* __restrict__ dmem,

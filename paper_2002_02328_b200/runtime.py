@@ -463,11 +463,17 @@ class JacobiSweeper:
 
     ``hd_cache=True`` selects the "hd-cache" variant: H E_S d_mem is kept
     from each block's previous visit (linearity of H) so the Gram needs one
-    forward correlation instead of two.
+    forward correlation instead of two.  ``incremental=True`` (implies
+    hd_cache) selects "hd-incremental": the residual r = H x - y is kept on
+    the device as well, r += sum_b H E_b inc_b, so the sweep runs no residual
+    correlation; it is recomputed exactly on the first sweep and every
+    ``refresh_every`` sweeps (0: never again).
     """
 
     def __init__(self, obj: Objective, x0, block_height: int, dtype: torch.dtype = torch.float64,
-                 blocks: list | None = None, hd_cache: bool = False):
+                 blocks: list | None = None, hd_cache: bool = False, incremental: bool = False,
+                 refresh_every: int = 0):
+        hd_cache = hd_cache or incremental
         self.obj = obj
         self.dtype = dtype
         self.x = D.to_device(x0, dtype).clone()
@@ -495,30 +501,48 @@ class JacobiSweeper:
         self.K = obj.psf.device_kernels(dtype, dev)
         self.Y = obj.device_y(dtype, dev)
         self.k = 0
+        self.sweeps = 0
         self.graph = None
+        self.graphs = {}
+        self.refresh_every = refresh_every
+        self.resid = torch.zeros_like(self.x) if incremental else None
 
     @property
     def nblocks(self) -> int:
         return len(self.blocks)
 
-    def _launch(self) -> None:
+    def _refresh_due(self) -> bool:
+        return self.sweeps == 0 or (self.refresh_every > 0 and self.sweeps % self.refresh_every == 0)
+
+    def _launch(self, refresh: bool = False) -> None:
+        if self.resid is not None:
+            N.check(N.lib.bd3mg_jacobi_sweep_incremental(
+                D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(), D.byref(self.sw),
+                self.resid.data_ptr(), int(refresh), self.terms.data_ptr(), self.info.data_ptr(),
+                self.ws.data_ptr(), self.ws_bytes, D.stream_handle()))
+            return
         N.check(N.lib.bd3mg_jacobi_sweep(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(),
                                          self.Y.data_ptr(), D.byref(self.sw), self.terms.data_ptr(),
                                          self.info.data_ptr(), self.ws.data_ptr(), self.ws_bytes,
                                          D.stream_handle()))
 
     def capture(self) -> None:
-        """Record one sweep as a CUDA graph (after one eager warm-up sweep)."""
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._launch()
-        self.graph = g
+        """Record the sweep as a CUDA graph (after one eager warm-up sweep);
+        the incremental variant records its refresh sweep too."""
+        for refresh in ((False, True) if self.resid is not None else (False,)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch(refresh)
+            self.graphs[refresh] = g
+        self.graph = self.graphs[False]
 
     def sweep(self) -> None:
-        if self.graph is not None:
-            self.graph.replay()
+        refresh = self.resid is not None and self._refresh_due()
+        if self.graphs:
+            self.graphs[refresh].replay()
         else:
-            self._launch()
+            self._launch(refresh)
+        self.sweeps += 1
         self.k += len(self.blocks)
 
     def finish(self) -> float:

@@ -219,3 +219,44 @@ def test_ipc_p2p_halos_two_processes(tmp_path):
     fs.append(single.finish())
     assert np.array_equal(np.load(tmp_path / "x.npy"), single.x.cpu().numpy())
     np.testing.assert_allclose(np.load(tmp_path / "f.npy"), fs, rtol=1e-12)
+
+
+@pytest.mark.parametrize("dtype,refresh", [(torch.float64, 0), (torch.float64, 4), (torch.float32, 0)])
+def test_incremental_residual_variant_tracks_exact(dtype, refresh):
+    """Variant "hd-incremental" (residual kept by linearity, no residual
+    correlation per sweep): iterates and recorded f track the exact sweep to
+    rounding, eagerly and through the captured graphs."""
+    from paper_2002_02328_b200 import configs, objective, runtime
+    cfg = configs.CONFIGS["C1"]
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    obj = objective.Objective(psf, y, params)
+    a = runtime.JacobiSweeper(obj, x0, cfg.block_height, dtype)
+    b = runtime.JacobiSweeper(obj, x0, cfg.block_height, dtype, incremental=True, refresh_every=refresh)
+    tol_x, tol_f = (1e-10, 1e-11) if dtype == torch.float64 else (2e-5, 1e-5)
+    for it in range(30):
+        if it == 3:
+            a.capture()
+            b.capture()
+        a.sweep()
+        b.sweep()
+        if it > 0:
+            assert abs(a.f() - b.f()) <= tol_f * abs(a.f()), (it, a.f(), b.f())
+    xa, xb = a.x.double().cpu().numpy(), b.x.double().cpu().numpy()
+    assert np.linalg.norm(xa - xb) <= tol_x * np.linalg.norm(xa)
+    # the kept residual is H x - y of the current iterate
+    from paper_2002_02328_b200 import blur
+    r = blur.apply_H(psf, b.x) - obj.device_y(dtype)
+    assert float(torch.linalg.vector_norm(r - b.resid)) <= (1e-11 if dtype == torch.float64 else 1e-4) * float(
+        torch.linalg.vector_norm(r))
+
+
+def test_incremental_residual_needs_whole_volume():
+    from paper_2002_02328_b200 import configs, objective, runtime
+    from paper_2002_02328_b200.volume import SliceBlock
+    cfg = configs.CONFIGS["C1"]
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    obj = objective.Objective(psf, y, params)
+    with pytest.raises(ValueError):  # blocks that do not tile the volume
+        eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, torch.float64,
+                                    blocks=[SliceBlock(0, 7), SliceBlock(8, 15)], incremental=True)
+        eng.sweep()
