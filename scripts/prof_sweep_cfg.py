@@ -1,4 +1,5 @@
-"""Sweeps of a named config (for ncu launch lists):  python scripts/prof_sweep_cfg.py C3 [reps]"""
+"""Sweeps of a named config (for ncu launch lists):
+    python scripts/prof_sweep_cfg.py C3 [reps] [jacobi|cyclic|incremental]"""
 import sys
 from pathlib import Path
 
@@ -11,7 +12,12 @@ cfg = configs.CONFIGS[sys.argv[1]]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 dt = torch.float64 if cfg.dtype == "f64" else torch.float32
 psf, truth, y, x0, params = configs.make_problem(cfg)
-eng = runtime.JacobiSweeper(objective.Objective(psf, y, params), x0, cfg.block_height, dt)
+mode = sys.argv[3] if len(sys.argv) > 3 else "jacobi"
+obj = objective.Objective(psf, y, params)
+if mode == "cyclic":
+    eng = runtime.CyclicSweeper(obj, x0, cfg.block_height, dt)
+else:
+    eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, dt, incremental=mode == "incremental", refresh_every=0)
 for _ in range(reps):
     eng.sweep()
 torch.cuda.synchronize()

@@ -45,7 +45,11 @@ def timed(fn, steps=5, warmup=3):
     return tot / steps
 
 
-def ranks_ms(obj, x0, h, dtype, P):
+def ranks_ms(obj, x0, h, dtype, P, exposed=False):
+    """Per-rank sweep time (p2p graph: inbox unpack + mirrored sweep).  With
+    `exposed`, also the same rank's plain sweep (no unpack, no mirror stores):
+    the difference is the halo exchange work left on the rank's stream (here
+    the mirror stores hit local HBM instead of NVLink)."""
     shards = [ShardedJacobi(obj, x0, h, dtype, rank=r, world=P, halo="p2p") for r in range(P)]
     bases = {r: s.peer.ptr for r, s in enumerate(shards)}
     for s in shards:
@@ -55,16 +59,27 @@ def ranks_ms(obj, x0, h, dtype, P):
     for s in shards:
         s.capture()
     out = [timed(s.local_sweep) for s in shards]
+    plain = None
+    if exposed:
+        plain = []
+        for s in shards:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                s.peer, peer = None, s.peer
+                s._launch(0)
+                s.peer = peer
+            plain.append(timed(g.replay))
     for s in shards:
         s.close()
     del shards
     torch.cuda.empty_cache()
-    return out
+    return (out, plain) if exposed else out
 
 
 def main():
     names = sys.argv[1:] or ["C2", "C3", "C5"]
     res = {"method": __doc__.strip().splitlines()[0], "excluded": "recorder all-reduce of 7 doubles per sweep",
+           "exposed_halo": "p2p rank sweep minus the same sweep without inbox unpack and mirror stores",
            "configs": {}}
     for name in names:
         cfg = configs.CONFIGS[name]
@@ -82,8 +97,10 @@ def main():
         for P in (2, 4, 8):
             if P > B:
                 continue
-            ms = ranks_ms(obj, x0, cfg.block_height, dtype, P)
-            entry["strong"][P] = {"rank_ms": ms, "max_ms": max(ms), "efficiency": t1 / (P * max(ms))}
+            ms, plain = ranks_ms(obj, x0, cfg.block_height, dtype, P, exposed=True)
+            entry["strong"][P] = {"rank_ms": ms, "max_ms": max(ms), "efficiency": t1 / (P * max(ms)),
+                                  "plain_rank_ms": plain,
+                                  "exposed_halo_us": [1e3 * (a - b) for a, b in zip(ms, plain)]}
         if name == "C2":  # bench.py's default N>1 mode: the config per GPU
             for P in (2, 4, 8):
                 wc = dataclasses.replace(cfg, name=f"C2x{P}", dims=Dims3(cfg.dims.nx, cfg.dims.ny, cfg.dims.nz * P))
