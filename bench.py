@@ -263,11 +263,18 @@ def _load_until(eng, clocks, target, world, dist, torch, limit_s=5.0):
         torch.cuda.synchronize()
         done = clocks.count() >= target or time.time() >= t_end
         if world > 1:
-            f = torch.tensor([1.0 if done else 0.0], dtype=torch.float64, device="cuda")
-            dist.all_reduce(f, op=dist.ReduceOp.MIN)
-            done = float(f.item()) > 0.0
+            done = allreduce_scalar(1.0 if done else 0.0, dist.ReduceOp.MIN, dist, torch) > 0.0
         if done:
             return
+
+
+def allreduce_scalar(v: float, op, dist, torch) -> float:
+    """All-reduce of one float: a device tensor over NCCL, a host tensor over
+    gloo (the one-GPU multi-process check of this path, tests/test_gpu_bench.py)."""
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return float(t.item())
 
 
 def sharded_engine(distributed, obj, x0, cfg, dtype, halo, dist, torch):
@@ -281,9 +288,7 @@ def sharded_engine(distributed, obj, x0, cfg, dtype, halo, dist, torch):
             eng = distributed.ShardedJacobi(obj, x0, cfg.block_height, dtype, halo="p2p")
         except (RuntimeError, ValueError, OSError) as e:
             why = str(e).splitlines()[0][:160] if str(e) else type(e).__name__
-        ok = torch.tensor([0.0 if eng is None else 1.0], dtype=torch.float64, device="cuda")
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if float(ok.item()) > 0:
+        if allreduce_scalar(0.0 if eng is None else 1.0, dist.ReduceOp.MIN, dist, torch) > 0:
             return eng, "p2p: update-kernel NVLink stores into the neighbours' double-buffered inboxes (cudaIpc)"
         if eng is not None:
             eng.close()
@@ -305,9 +310,16 @@ def main():
     from paper_2002_02328_b200 import blur, configs, device as D, objective, runtime
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # BD3MG_BENCH_ONE_GPU=1 (test hook): every rank on device 0 over gloo, so the
+    # N>1 code path runs on a one-GPU box with host-side synchronisation
+    one_gpu = os.environ.get("BD3MG_BENCH_ONE_GPU") == "1"
+    device = 0 if one_gpu else local
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
     cfg = bench_config(args, world)
     dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
     psf, truth, y, x0, params = configs.make_problem(cfg)
@@ -343,7 +355,7 @@ def main():
     torch.cuda.synchronize()
     eng.check()
 
-    clocks = Clocks(local)
+    clocks = Clocks(device)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks.start()
@@ -367,9 +379,7 @@ def main():
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     t_max = ms
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
+        t_max = allreduce_scalar(ms, dist.ReduceOp.MAX, dist, torch)
     value = args.steps * B / (t_max / 1e3)
     f_last = eng.f()
     blocks_all = [runtime.scheduler.SliceBlock(lo, min(lo + cfg.block_height - 1, cfg.dims.nz - 1))
@@ -610,9 +620,7 @@ def e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng=None):
             step()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
+        dt = allreduce_scalar(dt, dist.ReduceOp.MAX, dist, torch)
         nb = eng.nblocks
         h2d = 2 * xl_h.nbytes
         d2h = 2 * (o1 - o0) * plane * 8 + 8
