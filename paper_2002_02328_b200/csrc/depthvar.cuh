@@ -60,6 +60,8 @@ struct alignas(64) ConvJob {
   int out_lo, nout;     // global output rows [out_lo, out_lo+nout)
   int work_begin;       // prefix of nout over jobs (grid.z index of first plane)
   int use_tma;          // 1: stage tiles with TMA; 0: cp.async fallback
+  int epi_tma;          // 1: tmap1 maps `sub` (RESID / GRAD, one input): the epilogue operand tile is
+                        //    staged by TMA into the free tile buffer during the last tap plane
 };
 
 template <typename T>
@@ -290,10 +292,20 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   const long long orow = (long long)(zo - job.out_lo) * p.plane;
   const bool vec_io = (p.nx % VEC) == 0;  // rows are whole 16-byte chunks
   const int a_pf = max(a_lo, a_hi - 1);
+  // RESID / GRAD: the epilogue operand tile (y rows or the regulariser
+  // gradient) is loaded by TMA into the tile buffer the last tap plane frees,
+  // while that plane computes; the epilogue then reads it from shared memory
+  constexpr bool kEpiTma = (MODE == M_RESID || MODE == M_GRAD) && NIN == 1 && sizeof(T) == 8;
+  const bool epi_tma = kEpiTma && tma && job.epi_tma && a_lo <= a_hi;
   uint32_t phase = 0;  // bit b = parity of buffer b
   int buf = 0;
   for (int a = a_lo; a <= a_hi; ++a) {
-    if (a < a_hi) issue(a + 1, buf ^ 1);
+    if (a < a_hi) {
+      issue(a + 1, buf ^ 1);
+    } else if (epi_tma && threadIdx.x == 0) {
+      mbar_expect_tx(&mbar[buf ^ 1], (uint32_t)(Cfg::TX * Cfg::TY * sizeof(T)));
+      tma_load_3d(tiles + (buf ^ 1) * NIN * Cfg::TILE, &job.tmap1, x0, y0, zo - job.out_lo, &mbar[buf ^ 1]);
+    }
     if constexpr (kEpiLoad) {
       if (a == a_pf && vec_io && job.sub && threadIdx.x < Cfg::TY) {
         const int y = y0 + threadIdx.x, w = min(Cfg::TX, p.nx - x0);
@@ -345,6 +357,8 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   }
 
   // ---- epilogue -----------------------------------------------------------
+  const T* etile = tiles + buf * NIN * Cfg::TILE;  // the buffer the last plane left free
+  if (epi_tma) mbar_wait(&mbar[buf], (phase >> buf) & 1u);
   constexpr int NV = Cfg::NV;
   double part[NV > 0 ? NV : 1];
 #pragma unroll
@@ -365,7 +379,8 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
 #pragma unroll
           for (int i = 0; i < RX; ++i) res[i] = acc[0][r][i];
         } else {
-          const V q = *reinterpret_cast<const V*>(job.sub + o);
+          const V q = epi_tma ? *reinterpret_cast<const V*>(etile + (ty * RY + r) * Cfg::TX + tx * RX)
+                              : *reinterpret_cast<const V*>(job.sub + o);
           const T* qs = reinterpret_cast<const T*>(&q);
 #pragma unroll
           for (int i = 0; i < RX; ++i) {
