@@ -93,7 +93,7 @@ cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
     if (ok && Cfg::NIN == 2) ok = encode_tmap(&jb.tmap1, jb.src1, f64, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH);
     jb.use_tma = (ok && !no_tma) ? 1 : 0;
     jb.epi_tma = 0;
-    if constexpr ((MODE == M_RESID || MODE == M_GRAD) && Cfg::NIN == 1 && sizeof(T) == 8) {
+    if constexpr ((MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC) && Cfg::NIN == 1 && sizeof(T) == 8) {
       static const bool no_epi = getenv("BD3MG_NO_EPI_TMA") != nullptr;
       if (jb.use_tma && jb.sub && !no_epi)
         jb.epi_tma = encode_tmap(&jb.tmap1, jb.sub, f64, p.nx, p.ny, jb.nout, Cfg::TX, Cfg::TY) ? 1 : 0;

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   // RESID / GRAD: the epilogue operand tile (y rows or the regulariser
   // gradient) is loaded by TMA into the tile buffer the last tap plane frees,
   // while that plane computes; the epilogue then reads it from shared memory
-  constexpr bool kEpiTma = (MODE == M_RESID || MODE == M_GRAD) && NIN == 1 && sizeof(T) == 8;
+  constexpr bool kEpiTma = (MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC) && NIN == 1 && sizeof(T) == 8;
   const bool epi_tma = kEpiTma && tma && job.epi_tma && a_lo <= a_hi;
   uint32_t phase = 0;  // bit b = parity of buffer b
   int buf = 0;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
   const int xt = x0 + tx * RX;
   // 16-byte loads / stores of the thread's RX outputs where the row allows
-  constexpr bool kVecEpi = RX == VEC && (MODE == M_STORE || MODE == M_RESID || MODE == M_GRAD);
+  constexpr bool kVecEpi = RX == VEC && (MODE == M_STORE || MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC);
   const bool vec_here = kVecEpi && vec_io && xt + RX <= p.nx;
   if constexpr (kVecEpi) {
     if (vec_here) {
@@ -387,6 +387,12 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
             if constexpr (MODE == M_RESID) {
               res[i] = sub_rn(acc[0][r][i], qs[i]);
               part[0] += (double)res[i] * (double)res[i];
+            } else if constexpr (MODE == M_GRAMC) {  // H E_S g out; Gram with the cached H E_S d
+              const double a0 = (double)acc[0][r][i], c0 = (double)qs[i];
+              res[i] = acc[0][r][i];
+              part[0] += a0 * a0;
+              part[1] += a0 * c0;
+              part[2] += c0 * c0;
             } else {
               res[i] = add_rn(acc[0][r][i], qs[i]);
             }
