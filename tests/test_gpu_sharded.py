@@ -260,3 +260,37 @@ def test_incremental_residual_needs_whole_volume():
         eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, torch.float64,
                                     blocks=[SliceBlock(0, 7), SliceBlock(8, 15)], incremental=True)
         eng.sweep()
+
+
+def test_p2p_mirrors_keep_inboxes_current_on_nonfinite_gradient():
+    """A block whose gradient is non-finite applies no update; its mirror
+    rows still land in the neighbour's inbox (unchanged x), so the next
+    sweep's halos equal the owner's rows."""
+    from paper_2002_02328_b200 import configs, objective
+    from paper_2002_02328_b200.distributed import ShardedJacobi
+    cfg = configs.CONFIGS["C1"]
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    x0 = x0.copy()
+    x0[20, 5, 5] = np.nan  # rank 1 owns planes 8..23: both of its blocks see the NaN in their residual
+    obj = objective.Objective(psf, y, params)
+    shards = [ShardedJacobi(obj, x0, cfg.block_height, torch.float64, rank=r, world=2, halo="p2p") for r in range(2)]
+    bases = {r: s.peer.ptr for r, s in enumerate(shards)}
+    for s in shards:
+        s.peer.connect(bases)
+    before = shards[1].x.clone()
+    for s in shards:
+        s.local_sweep()
+    torch.cuda.synchronize()
+    assert bool((shards[1].info[:, 8] != 0).any())
+    with pytest.raises(ValueError, match="non-finite"):
+        shards[1].check()
+    o1 = shards[1].o_lo - shards[1].l_lo
+    assert torch.equal(torch.nan_to_num(shards[1].x[o1:]), torch.nan_to_num(before[o1:]))
+    s0 = shards[0]
+    s0.peer.unpack(s0.sweeps % 2)
+    lo = s0.o_hi + 1
+    got = s0.x[lo - s0.l_lo:s0.l_hi - s0.l_lo + 1]
+    want = shards[1].x[lo - shards[1].l_lo:s0.l_hi - shards[1].l_lo + 1]
+    assert torch.equal(got, want)
+    for s in shards:
+        s.close()
