@@ -198,7 +198,7 @@ int launch_reg_gram(StArgs<T>& a, cudaStream_t s) {
   std::lock_guard<std::mutex> lock(mu);
   for (int j = 0; j < a.njobs; ++j) {
     const StJob<T>& J = a.jobs[j];
-    const long long h = J.hi - J.lo + 1;
+    const long long h = (J.chunk && J.hi < J.bhi ? J.hi + 1 : J.hi) - J.lo + 1;  // chunks stage one plane more
     if (!encode_tmap(&tm.a[j], J.a, sizeof(T) == 8, a.nx, a.ny, h, G::BW, G::BH) ||
         (J.b && !encode_tmap(&tm.b[j], J.b, sizeof(T) == 8, a.nx, a.ny, h, G::BW, G::BH)))
       return fail(BD3MG_EINVAL, "reg_gram: TMA descriptor rejected (job %d)", j);
@@ -458,6 +458,45 @@ struct StepOpts {
 };
 constexpr int kSumsqCtas = 4 * 148;  // fixed grid of the recorder's sum of squares (deterministic)
 
+// Small stencil grids (one block of a cyclic / asynchronous step): each
+// block's z-march is cut into chunks of c planes so a block alone fills ~2
+// CTAs per SM (the march is a serial chain of TMA round trips per CTA).  c
+// depends on the block and the plane only -- never on how many blocks share
+// a launch -- so a block's regulariser-Gram partial sums are grouped the same
+// way in every batching (sharded, pipelined and single-launch sweeps stay
+// bitwise equal).  TMA path only; returns h for an unchunked block.
+template <typename T>
+int64_t stencil_chunk(const bd3mg_geom_t* g, int64_t h) {
+  static const int sms = [] {
+    int d = 0, n = 148;
+    if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess)
+      n = 148;
+    return n;
+  }();
+  static const bool off = getenv("BD3MG_NO_ST_CHUNK") != nullptr;
+  if (off || !st_use_tma<T>(g->nx) || h < 2) return h;
+  const long long tiles = tm_tiles(g->ny, g->nx), want = 2LL * sms;
+  if (tiles >= want) return h;
+  const long long k = std::min<long long>((want + tiles - 1) / tiles, h);
+  return (h + k - 1) / k;
+}
+
+// Launch a stencil over `jobs` in groups of at most kMaxJobs (partials
+// job-major, continuing across the groups).
+template <typename T, typename F>
+int launch_jobs(const StArgs<T>& proto, const std::vector<StJob<T>>& jobs, size_t partial_doubles_per_job,
+                F&& launch) {
+  for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxJobs) {
+    StArgs<T> a = proto;
+    a.njobs = (int)std::min<size_t>(kMaxJobs, jobs.size() - j0);
+    for (int j = 0; j < a.njobs; ++j) a.jobs[j] = jobs[j0 + j];
+    if (proto.partials) a.partials = proto.partials + j0 * partial_doubles_per_job;
+    int rc = launch(a);
+    if (rc) return rc;
+  }
+  return BD3MG_OK;
+}
+
 template <typename T>
 int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
                    int nt, double* info_out, Ws& ws, cudaStream_t s, const StepOpts<T>& opt = StepOpts<T>()) {
@@ -538,24 +577,39 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   long long hsum = 0;
   for (int t = 0; t < nt; ++t) hsum += h[t];
-  const long long reg_rows = (long long)nt * z_tiles<T>(g);  // one partial row per (block, tile)
+  // one partial row per (job, tile); a z-chunked block is several jobs
+  long long rg_total = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t c = stencil_chunk<T>(g, h[t]);
+    rg_total += (h[t] + c - 1) / c;
+  }
+  const long long reg_rows = rg_total * z_tiles<T>(g);
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return ws_fail(ws);
 
+  // regulariser gradient of every block (whole blocks, or z-chunks of them)
+  auto greg_launch = [&](cudaStream_t st) -> int {
+    std::vector<StJob<T>> jobs;
+    for (int t = 0; t < nt; ++t) {
+      const int64_t c = stencil_chunk<T>(g, h[t]);
+      for (int64_t lo = tasks[t].z_lo; lo <= tasks[t].z_hi; lo += c) {
+        StJob<T> J;
+        memset(&J, 0, sizeof(J));
+        J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
+        J.lo = (int)lo; J.hi = (int)std::min<int64_t>(lo + c - 1, tasks[t].z_hi);
+        J.out0 = grb[t] + (lo - tasks[t].z_lo) * plane; J.out1 = wb[t] + (lo - tasks[t].z_lo) * plane;
+        jobs.push_back(J);
+      }
+    }
+    return launch_jobs<T>(st_args<T>(g, r), jobs, 0, [&](StArgs<T>& a) { return launch_greg<T>(a, false, st); });
+  };
   // (0) block steps with a side stream (mg_steps): the regulariser gradient
   // needs x only, so it runs next to the residual correlation
   const bool greg_side = opt.ss && !pre;
   if (greg_side) {
     CU(hop(s, opt.ss->side, opt.ss->ev[0]));
-    StArgs<T> sa = st_args<T>(g, r);
-    sa.njobs = nt;
-    for (int t = 0; t < nt; ++t) {
-      StJob<T>& J = sa.jobs[t];
-      J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
-      J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi; J.out0 = grb[t]; J.out1 = wb[t];
-    }
-    int rc = launch_greg<T>(sa, false, opt.ss->side);
+    int rc = greg_launch(opt.ss->side);
     if (rc) return rc;
   }
   // (1) r = H x - y (variant "hd-incremental": kept from the previous call
@@ -600,14 +654,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
   // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
   if (!pre && !greg_side) {
-    StArgs<T> sa = st_args<T>(g, r);
-    sa.njobs = nt;
-    for (int t = 0; t < nt; ++t) {
-      StJob<T>& J = sa.jobs[t];
-      J.a = (const T*)tasks[t].frag; J.a_z0 = tasks[t].frag_z0;
-      J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi; J.out0 = grb[t]; J.out1 = wb[t];
-    }
-    int rc = launch_greg<T>(sa, false, s);
+    int rc = greg_launch(s);
     if (rc) return rc;
   }
   // (2b)-(4) per half of the blocks: g = H^T r + greg, then the regulariser
@@ -619,6 +666,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   std::vector<std::pair<long long, long long>> granges(nt);
   long long gram_row0 = 0;  // first partial row of the current part's Gram launch
   const long long tl_reg = z_tiles<T>(g);
+  std::vector<int> rg_begin(nt), rg_end(nt);  // regulariser-Gram jobs of each block
+  int rg_jobs = 0;
   if (parts == 2) CU(hop(s, opt.ss->side2, opt.ss->ev[4]));  // fork after RESID / greg
   for (int part = 0; part < parts; ++part) {
     const int t0 = part == 0 ? 0 : nt / 2, t1 = (parts == 1 || part == 1) ? nt : nt / 2;
@@ -644,15 +693,27 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     }
     {
       StArgs<T> sa = st_args<T>(g, r);
-      sa.njobs = np;
-      sa.partials = rparts + (size_t)t0 * tl_reg * kRegNV;  // rows t*tl .. of block t
+      sa.partials = rparts + (size_t)rg_jobs * tl_reg * kRegNV;  // job-major rows after the earlier parts
+      std::vector<StJob<T>> jobs;
       for (int t = t0; t < t1; ++t) {
-        StJob<T>& J = sa.jobs[t - t0];
-        J.a = gb[t]; J.a_z0 = tasks[t].z_lo; J.b = (const T*)tasks[t].d_mem; J.w = wb[t];
-        J.lo = (int)tasks[t].z_lo; J.hi = (int)tasks[t].z_hi;
+        const int64_t c = stencil_chunk<T>(g, h[t]);
+        rg_begin[t] = rg_jobs + (int)jobs.size();
+        for (int64_t lo = tasks[t].z_lo; lo <= tasks[t].z_hi; lo += c) {
+          const int64_t o = (lo - tasks[t].z_lo) * plane;
+          StJob<T> J;
+          memset(&J, 0, sizeof(J));
+          J.a = gb[t] + o; J.a_z0 = lo; J.b = tasks[t].d_mem ? (const T*)tasks[t].d_mem + o : nullptr;
+          J.w = wb[t] + o;
+          J.lo = (int)lo; J.hi = (int)std::min<int64_t>(lo + c - 1, tasks[t].z_hi);
+          if (c < h[t]) { J.chunk = 1; J.blo = (int)tasks[t].z_lo; J.bhi = (int)tasks[t].z_hi; }
+          jobs.push_back(J);
+        }
+        rg_end[t] = rg_jobs + (int)jobs.size();
       }
+      rg_jobs += (int)jobs.size();
 #ifndef BD3MG_EXP_SKIP_REGGRAM
-      int rc = launch_reg_gram<T>(sa, s3);
+      int rc = launch_jobs<T>(sa, jobs, (size_t)tl_reg * kRegNV,
+                              [&](StArgs<T>& a) { return launch_reg_gram<T>(a, s3); });
       if (rc) return rc;
 #endif
     }
@@ -696,7 +757,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     for (int t = 0; t < nt; ++t) {
       sa.has_d[t] = tasks[t].d_mem != nullptr;
       sa.g_begin[t] = granges[t].first; sa.g_end[t] = granges[t].second;
-      sa.r_begin[t] = t * tl; sa.r_end[t] = (t + 1) * tl;
+      sa.r_begin[t] = rg_begin[t] * tl; sa.r_end[t] = rg_end[t] * tl;
     }
     reduce_solve_kernel<<<nt, kEwNT, 0, s>>>(sa, cparts, rparts, info_out); launched();
     CU(cudaGetLastError());

@@ -34,7 +34,8 @@ struct StJob {
   long long a_z0;
   int lo, hi;      // rows of the job
   int work_begin;  // first grid.z index of the job
-  int pad_;
+  int chunk;       // reg_gram (TMA path): [lo, hi] is a z-chunk of the block [blo, bhi]
+  int blo, bhi;
 };
 
 template <typename T>

@@ -239,6 +239,11 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool has_d = J.b != nullptr;
   const int nx = p.nx, ny = p.ny;
+  // z-chunk of a block (small grids): the block's own rows decide the
+  // embedding rules; the chunk also stages the plane after its last row
+  const bool chunk = J.chunk != 0;
+  const int blo = chunk ? J.blo : J.lo, bhi = chunk ? J.bhi : J.hi;
+  const int zend = J.hi < bhi ? J.hi + 1 : J.hi;  // last plane staged
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::RING; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
     tma_prefetch_desc(&tm.a[job]);
     if (has_d) tma_prefetch_desc(&tm.b[job]);
     issue(J.lo);
-    if (J.lo + 1 <= J.hi) issue(J.lo + 1);
+    if (J.lo + 1 <= zend) issue(J.lo + 1);
   }
   mbar_wait(&bars[slot(J.lo)], phase(J.lo));
 
@@ -272,12 +277,12 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
       const int y = y0 + warp * kTmR + j;
       wv[j] = (y < ny && x < nx) ? J.w[orow + (long long)y * nx + x] : T(0);
     }
-    if (threadIdx.x == 0 && z + 2 <= J.hi) issue(z + 2);
-    if (z + 1 <= J.hi) mbar_wait(&bars[slot(z + 1)], phase(z + 1));
+    if (threadIdx.x == 0 && z + 2 <= zend) issue(z + 2);
+    if (z + 1 <= zend) mbar_wait(&bars[slot(z + 1)], phase(z + 1));
     const T* g0 = gs[slot(z)];
     const T* d0 = dss[slot(z)];
-    const T* g1 = gs[slot(min(z + 1, J.hi))];
-    const T* d1 = dss[slot(min(z + 1, J.hi))];
+    const T* g1 = gs[slot(min(z + 1, zend))];
+    const T* d1 = dss[slot(min(z + 1, zend))];
 #pragma unroll
     for (int j = 0; j < kTmR; ++j) {
       const int ly = warp * kTmR + j, y = y0 + ly;
@@ -298,10 +303,10 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
       v[4] += w * (dx0 * dx1 + dy0 * dy1);
       v[5] += w * (dx1 * dx1 + dy1 * dy1);
       double z0v, z1v;  // axial row z of the block-embedded vectors
-      if (z < J.hi) {
+      if (z < bhi) {
         z0v = -((double)g1[q] - (double)g);
         z1v = has_d ? (double)d1[q] - (double)d : 0.0;
-      } else if (J.hi < p.nz - 1) {
+      } else if (bhi < p.nz - 1) {
         z0v = -b0;
         z1v = -b1;
       } else {
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
       v[6] += z0v * z0v;
       v[7] += z0v * z1v;
       v[8] += z1v * z1v;
-      if (z == J.lo && J.lo >= 1) {
+      if (z == blo && blo >= 1) {
         v[6] += b0 * b0;
         v[7] += b0 * b1;
         v[8] += b1 * b1;
