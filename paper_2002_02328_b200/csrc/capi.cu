@@ -1026,7 +1026,7 @@ int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
 void count_launches(int n) { launched(n); }
 
 bool encode_tmap(CUtensorMap* map, const void* base, bool f64, long long nx, long long ny, long long nz, int boxw,
-                 int boxh) {
+                 int boxh, int boxd) {
   static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1037,11 +1037,11 @@ bool encode_tmap(CUtensorMap* map, const void* base, bool f64, long long nx, lon
   }();  // thread-safe one-time lookup
   const size_t es = f64 ? 8 : 4;
   if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15) || ((size_t)nx * es) % 16 || boxw > 256 ||
-      boxh > 256 || ((size_t)boxw * es) % 16)
+      boxh > 256 || boxd < 1 || boxd > 256 || ((size_t)boxw * es) % 16)
     return false;
   const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
   const cuuint64_t strides[2] = {(cuuint64_t)(nx * es), (cuuint64_t)(nx * ny * es)};
-  const cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)boxh, (cuuint32_t)boxd};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -80,7 +80,7 @@ inline cudaError_t ensure_smem_attr(Kern kern, size_t bytes) {
 // out-of-bounds elements are zero-filled by the copy engine.  Returns false
 // when the layout is not TMA-legal (row pitch / base not 16-byte aligned).
 bool encode_tmap(CUtensorMap* map, const void* base, bool f64, long long nx, long long ny, long long nz, int boxw,
-                 int boxh);
+                 int boxh, int boxd = 1);
 
 template <typename T, int K, int MODE, bool ADJ>
 cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
@@ -116,6 +116,15 @@ cudaError_t launch_rz2(ConvArgs<T>& p, int total_work, cudaStream_t s) {
     ConvJob<T>& jb = p.jobs[j];
     jb.use_tma = encode_tmap(&jb.tmap0, jb.src0, sizeof(T) == 8, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH) &&
                  getenv("BD3MG_NO_TMA") == nullptr;
+  }
+  for (int j = 0; j < p.njobs; ++j) {  // epilogue operand tiles of both output planes (RESID / GRAD / GRAMC)
+    ConvJob<T>& jb = p.jobs[j];
+    jb.epi_tma = 0;
+    if constexpr (Cfg::EPI_T) {
+      static const bool no_epi = getenv("BD3MG_NO_EPI_TMA") != nullptr;
+      if (jb.use_tma && jb.sub && !no_epi)
+        jb.epi_tma = encode_tmap(&jb.tmap1, jb.sub, sizeof(T) == 8, p.nx, p.ny, jb.nout, Cfg::TX, Cfg::TY, 2) ? 1 : 0;
+    }
   }
   const size_t sm = Cfg::smem_bytes(p.kz);
   if constexpr (Cfg::NIN == 2) {

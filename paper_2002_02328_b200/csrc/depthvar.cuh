@@ -482,8 +482,15 @@ struct Rz2Cfg {
   static constexpr int NV = ModeNV<MODE>::value;
   static constexpr int KS = KY * KX;                       // one tap slice
   static constexpr size_t SLICE_BYTES = ((size_t)2 * 2 * KS * sizeof(T) + 127) & ~size_t(127);
+  // RESID / GRAD / GRAMC: the epilogue operand tiles of both output planes
+  // (2 x TX x TY) are TMA-staged into the ring buffer the last input plane
+  // frees, so each buffer holds at least that much
+  static constexpr bool EPI_T = (MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC) && NIN == 1;
+  static constexpr int EPI = 2 * TX * TY;
+  static constexpr int BUF = (EPI_T && EPI > NIN * TILE) ? EPI : NIN * TILE;  // elements per ring buffer
+  static constexpr size_t BUF_BYTES = (size_t)BUF * sizeof(T);
   static size_t smem_bytes(int) {
-    return 2 * NIN * TILE_BYTES + SLICE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
+    return 2 * BUF_BYTES + SLICE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
   }
 };
 
@@ -587,8 +594,8 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* tiles = reinterpret_cast<T*>(sbase);  // [buf][input][TILE]
-  T* slices = reinterpret_cast<T*>(sbase + 2 * NIN * Cfg::TILE_BYTES);  // [buf][out][KS]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::SLICE_BYTES);
+  T* slices = reinterpret_cast<T*>(sbase + 2 * Cfg::BUF_BYTES);  // [buf][out][KS]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * Cfg::BUF_BYTES + Cfg::SLICE_BYTES);
   double* red_s = reinterpret_cast<double*>(mbar + 2);
 
   const int zidx = blockIdx.z;
@@ -617,7 +624,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     }
   };
   auto issue = [&](int zi, int b) {
-    T* dst = tiles + b * NIN * Cfg::TILE;
+    T* dst = tiles + b * Cfg::BUF;
     if (tma) {
       if (threadIdx.x == 0) {
         mbar_expect_tx(&mbar[b], (uint32_t)(NIN * Cfg::BOX_BYTES));
@@ -664,10 +671,15 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   const int zi_pf = max(zi_lo, zi_hi - 1);
   uint32_t phase = 0;
   int buf = 0;
+  constexpr bool kEpiTma = Cfg::EPI_T;
+  const bool epi_tma = kEpiTma && tma && job.epi_tma && zi_lo <= zi_hi;
   for (int zi = zi_lo; zi <= zi_hi; ++zi) {
     if (zi < zi_hi) {
       issue(zi + 1, buf ^ 1);
       stage_slices(zi + 1, buf ^ 1);  // visible after this iteration's closing barrier
+    } else if (epi_tma && threadIdx.x == 0) {  // both planes' operand tiles into the freed buffer
+      mbar_expect_tx(&mbar[buf ^ 1], (uint32_t)(Cfg::EPI * sizeof(T)));
+      tma_load_3d(tiles + (buf ^ 1) * Cfg::BUF, &job.tmap1, x0, y0, zo0 - job.out_lo, &mbar[buf ^ 1]);
     }
     if constexpr (kEpiLoad) {
       if (zi == zi_pf && vec_io && job.sub && threadIdx.x < 2 * Cfg::TY) {
@@ -688,7 +700,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
     // one code body for both outputs (invalid taps have zero coefficients:
     // exact no-ops for finite inputs); three specialised bodies overflow
     // the instruction cache for the 7x7 / 9x9 instantiations (measured)
-    const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
+    const T* tb = tiles + buf * Cfg::BUF + (ty * RY) * Cfg::PITCH + tx * RX;
     const T* cs0 = slices + buf * 2 * KS;
     if constexpr (kPacked)
       rz2_plane_pp<Cfg>(reinterpret_cast<const float*>(tb), reinterpret_cast<const unsigned long long*>(cs0), accp);
@@ -714,12 +726,14 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   }
 
   // ---- epilogue (both output planes) --------------------------------------
+  const T* etile = tiles + buf * Cfg::BUF;  // the buffer the last plane left free
+  if (epi_tma) mbar_wait(&mbar[buf], (phase >> buf) & 1u);
   constexpr int NV = Cfg::NV;
   double part[NV > 0 ? NV : 1];
 #pragma unroll
   for (int k = 0; k < (NV > 0 ? NV : 1); ++k) part[k] = 0.0;
   const int xt = x0 + tx * RX;
-  constexpr bool kVecEpi = MODE == M_STORE || MODE == M_RESID || MODE == M_GRAD;
+  constexpr bool kVecEpi = MODE == M_STORE || MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC;
   const bool vec_here = kVecEpi && vec_io && xt + RX <= p.nx;  // RX == VEC: one 16-byte access per row
 #pragma unroll
   for (int o = 0; o < 2; ++o) {
@@ -737,13 +751,20 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
 #pragma unroll
             for (int i = 0; i < RX; ++i) res[i] = acc[o][r][i];
           } else {
-            const V v = *reinterpret_cast<const V*>(job.sub + q);
+            const V v = epi_tma ? *reinterpret_cast<const V*>(etile + (o * Cfg::TY + ty * RY + r) * Cfg::TX + tx * RX)
+                                : *reinterpret_cast<const V*>(job.sub + q);
             const T* vs = reinterpret_cast<const T*>(&v);
 #pragma unroll
             for (int i = 0; i < RX; ++i) {
               if constexpr (MODE == M_RESID) {
                 res[i] = sub_rn(acc[o][r][i], vs[i]);
                 part[0] += (double)res[i] * (double)res[i];
+              } else if constexpr (MODE == M_GRAMC) {  // H E_S g out; Gram with the cached H E_S d
+                const double a0 = (double)acc[o][r][i], c0 = (double)vs[i];
+                res[i] = acc[o][r][i];
+                part[0] += a0 * a0;
+                part[1] += a0 * c0;
+                part[2] += c0 * c0;
               } else {
                 res[i] = add_rn(acc[o][r][i], vs[i]);
               }
