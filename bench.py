@@ -392,6 +392,9 @@ def main():
         st = eng.shard.staleness
         extra["async"] = {"max_delay_bound": 2, "staleness_max": max(st) if st else 0,
                           "staleness_mean": float(np.mean(st)) if st else 0.0, "waits": eng.shard.waits}
+    if args.mode == "cyclic" and world == 1:
+        extra["variants"] = {"hd-incremental": variant_cyclic_incremental(obj, cfg, x0, dtype, args, torch, runtime,
+                                                                          flush)}
     if args.mode != "jacobi":
         args.quick = True  # e2e / roofline / baselines are defined on the default schedule
     if not args.quick and rank == 0:
@@ -457,6 +460,31 @@ def variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush, inc
         out["note"] = ("flops exclude the residual correlation of the refresh sweeps (1 in 16 in the timed "
                        "region at most); iterates track the exact variant to 1e-10 (tests/test_gpu_sharded.py)")
     return out
+
+
+def variant_cyclic_incremental(obj, cfg, x0, dtype, args, torch, runtime, flush):
+    """Secondary number of the cyclic schedule: the "hd-incremental" variant
+    (cached H E_S d_mem, residual kept by linearity, recorder from it; exact
+    refresh every 16 sweeps)."""
+    eng = runtime.CyclicSweeper(obj, x0, cfg.block_height, dtype, incremental=True, refresh_every=16)
+    eng.sweep()
+    eng.capture()
+    for _ in range(max(args.warmup - 1, 0)):
+        eng.sweep()
+    torch.cuda.synchronize()
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        st[i].record()
+        eng.sweep()
+        en[i].record()
+    torch.cuda.synchronize()
+    eng.check()
+    ms = sum(a.elapsed_time(b) for a, b in zip(st, en))
+    return {"value": args.steps * eng.nblocks / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
+            "refresh_every": eng.refresh_every,
+            "note": "tracks the exact cyclic sweep to 1e-10 (tests/test_gpu_sharded.py)"}
 
 
 def variant_separable(obj, dtype, torch):

@@ -213,6 +213,20 @@ int bd3mg_jacobi_sweep_incremental(const bd3mg_geom_t* g, const bd3mg_reg_t* r, 
                                    const bd3mg_sweep_t* sw, void* resid, int refresh, double* terms_out,
                                    double* info_out, void* ws, size_t ws_bytes, void* stream);
 
+/* The same variant for block steps (the deterministic cyclic schedule):
+ * bd3mg_mg_steps with every task in place on one whole-volume anchor, hd[t]
+ * the task's hd-cache rows (H E_S d_mem over rows [z_lo-rz, z_hi+rz] clamped,
+ * zero-initialised), and `resid` the kept r = H x - y of the anchor (the
+ * caller computes it exactly once, e.g. H x then minus y); each call updates
+ * both by linearity.  bd3mg_eval_f_resid is bd3mg_eval_f with the data term
+ * taken from `resid` (workspace: bd3mg_eval_f_ws_bytes). */
+size_t bd3mg_mg_steps_incremental_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks);
+int bd3mg_mg_steps_incremental(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                               const bd3mg_task_t* tasks, int ntasks, void* const* hd, void* resid,
+                               double* info_out, void* ws, size_t ws_bytes, void* stream);
+int bd3mg_eval_f_resid(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* resid, const void* x,
+                       const void* snap, double* terms_out, void* ws, size_t ws_bytes, void* stream);
+
 /* Sharded sweep with the halo exchange fused into the in-place update: the
  * updated iterate rows [z_lo, z_hi] (global depths, each inside one of the
  * sweep's blocks) are ALSO stored to dst (plane z_lo first), typically a

@@ -30,7 +30,8 @@ EXPORTS = (
     "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
     "bd3mg_jacobi_sweep_ws_bytes", "bd3mg_jacobi_cache_elems", "bd3mg_jacobi_sweep",
-    "bd3mg_jacobi_sweep_mirrored", "bd3mg_jacobi_sweep_incremental", "bd3mg_mg_steps_mirrored", "bd3mg_host_register", "bd3mg_host_unregister",
+    "bd3mg_jacobi_sweep_mirrored", "bd3mg_jacobi_sweep_incremental", "bd3mg_mg_steps_incremental_ws_bytes",
+    "bd3mg_mg_steps_incremental", "bd3mg_eval_f_resid", "bd3mg_mg_steps_mirrored", "bd3mg_host_register", "bd3mg_host_unregister",
     "bd3mg_publish", "bd3mg_peer_alloc", "bd3mg_peer_open", "bd3mg_peer_close", "bd3mg_peer_free",
     "bd3mg_problem_create", "bd3mg_problem_destroy", "bd3mg_problem_mg_direction_host",
     "bd3mg_problem_jacobi_sweep_host",
@@ -126,6 +127,11 @@ def _load() -> C.CDLL:
     lib.bd3mg_jacobi_sweep_mirrored.argtypes = [G, R, _vp, _vp, S, C.POINTER(Mirror), C.c_int, _vp, _vp, _vp, _sz,
                                                 _vp]
     lib.bd3mg_jacobi_sweep_incremental.argtypes = [G, R, _vp, _vp, S, _vp, C.c_int, _vp, _vp, _vp, _sz, _vp]
+    lib.bd3mg_mg_steps_incremental_ws_bytes.argtypes = [G, T, C.c_int]
+    lib.bd3mg_mg_steps_incremental_ws_bytes.restype = _sz
+    lib.bd3mg_mg_steps_incremental.argtypes = [G, R, _vp, _vp, T, C.c_int, C.POINTER(C.c_void_p), _vp, _vp, _vp, _sz,
+                                               _vp]
+    lib.bd3mg_eval_f_resid.argtypes = [G, R, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     lib.bd3mg_mg_steps_mirrored.argtypes = [G, R, _vp, _vp, T, C.c_int, C.POINTER(Mirror), C.c_int, _vp, _vp, _sz,
                                             _vp]
     lib.bd3mg_host_register.argtypes = [_vp, _sz, C.POINTER(C.c_void_p)]

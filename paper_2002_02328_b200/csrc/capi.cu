@@ -47,6 +47,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr double kPruneTol = 1e-14;  // directions.py:19
+constexpr int kSumsqCtas = 4 * 148;  // fixed grid of the recorder's sum of squares (deterministic)
 constexpr double kPinvTol = 1e-12;   // directions.py:22
 
 // Bump allocator over a caller workspace; measure mode sizes it.
@@ -325,7 +326,7 @@ int grad_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
 template <typename T>
 int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y_rows, const T* frag,
                    int64_t frag_z0, int64_t nzf, int64_t lo, int64_t hi, const T* snap_rows, double* terms, Ws& ws,
-                   cudaStream_t s) {
+                   cudaStream_t s, const T* resid_rows = nullptr) {
   const int64_t nz = g->nz, plane = g->ny * g->nx;
   if (lo < 0 || hi < lo || hi >= nz) return fail(BD3MG_EINVAL, "invalid rows [%lld, %lld]", (long long)lo, (long long)hi);
   const int64_t need_hi = std::min<int64_t>(nz - 1, hi + 1);
@@ -333,21 +334,28 @@ int eval_rows_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     return fail(BD3MG_EINVAL, "fragment does not cover rows [%lld, %lld]", (long long)lo, (long long)need_hi);
   const int64_t nr = hi - lo + 1, n = nr * plane;
   const long long crow = conv_rows<T>(g, M_RESID, nr);
-  double* parts = ws.take<double>(crow);
+  double* parts = ws.take<double>(std::max<long long>(crow, kSumsqCtas));
   const long long erows = nr * st_tiles(g);
   double* eparts = ws.take<double>((size_t)erows * kEvalNV);
   double* sums = ws.take<double>(8);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return ws_fail(ws);
-  ConvArgs<T> a = base_args<T>(g, r, K);
-  a.njobs = 1;
-  a.partials = parts;
-  a.jobs[0].src0 = frag; a.jobs[0].src_z0 = frag_z0; a.jobs[0].src_nz = (int)nzf;
-  a.jobs[0].dst0 = nullptr; a.jobs[0].sub = y_rows;
-  a.jobs[0].out_lo = (int)lo; a.jobs[0].nout = (int)nr;
-  CU(conv_launch<T>(M_RESID, false, a, (int)nr, s));
-  launched();
-  CU(reduce(parts, 1, {{0, crow}}, sums, 1, s));
+  if (resid_rows) {  // data term from a kept residual (variant "hd-incremental")
+    sumsq_kernel<T><<<kSumsqCtas, kEwNT, 0, s>>>(resid_rows, n, parts);
+    launched();
+    CU(cudaGetLastError());
+    CU(reduce(parts, 1, {{0, kSumsqCtas}}, sums, 1, s));
+  } else {
+    ConvArgs<T> a = base_args<T>(g, r, K);
+    a.njobs = 1;
+    a.partials = parts;
+    a.jobs[0].src0 = frag; a.jobs[0].src_z0 = frag_z0; a.jobs[0].src_nz = (int)nzf;
+    a.jobs[0].dst0 = nullptr; a.jobs[0].sub = y_rows;
+    a.jobs[0].out_lo = (int)lo; a.jobs[0].nout = (int)nr;
+    CU(conv_launch<T>(M_RESID, false, a, (int)nr, s));
+    launched();
+    CU(reduce(parts, 1, {{0, crow}}, sums, 1, s));
+  }
   StArgs<T> e = st_args<T>(g, r);
   e.njobs = 1;
   e.jobs[0].a = frag; e.jobs[0].a_z0 = frag_z0; e.jobs[0].b = snap_rows; e.jobs[0].lo = (int)lo; e.jobs[0].hi = (int)hi;
@@ -456,7 +464,6 @@ struct StepOpts {
   int64_t r_full_z0 = 0;
   bool r_refresh = false;      // recompute r_full exactly in this call
 };
-constexpr int kSumsqCtas = 4 * 148;  // fixed grid of the recorder's sum of squares (deterministic)
 
 // Small stencil grids (one block of a cyclic / asynchronous step): each
 // block's z-march is cut into chunks of c planes so a block alone fills ~2
@@ -840,8 +847,14 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
 template <typename T>
 int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y, const bd3mg_task_t* tasks,
                   int ntasks, double* info_out, Ws& ws, cudaStream_t s, const bd3mg_mirror_t* mirrors = nullptr,
-                  int nmirrors = 0) {
+                  int nmirrors = 0, T* const* hd = nullptr, T* resid = nullptr) {
   if (ntasks < 0) return fail(BD3MG_EINVAL, "negative task count");
+  if (resid) {  // variant "hd-incremental" for block steps: one launch, in place, whole-volume anchor
+    if (!hd || ntasks > kMaxJobs) return fail(BD3MG_EINVAL, "incremental steps need the hd cache and <= %d tasks", kMaxJobs);
+    for (int t = 0; t < ntasks; ++t)
+      if (!hd[t] || !tasks[t].x_rows || tasks[t].frag_z0 != 0 || tasks[t].nzf != g->nz || tasks[t].frag != tasks[0].frag)
+        return fail(BD3MG_EINVAL, "incremental steps need in-place tasks on one whole-volume anchor (task %d)", t);
+  }
   if (nmirrors < 0 || (nmirrors > 0 && (!mirrors || ntasks > kMaxJobs)))
     return fail(BD3MG_EINVAL, "invalid mirror list (mirrored calls are one launch of <= %d tasks)", kMaxJobs);
   for (int j = 0; j < nmirrors; ++j)
@@ -849,6 +862,9 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   StepOpts<T> opt;
   opt.mirrors = mirrors;
   opt.nmirrors = nmirrors;
+  opt.hd = hd;
+  opt.r_full = resid;
+  opt.r_full_z0 = 0;
   // eager block steps overlap the stencils on a side stream (measured: async
   // mode at C2 8040 -> 8880 block-it/s); inside a graph capture the extra
   // branch costs more than it hides for one-block steps (cyclic sweep 7985 ->
@@ -1343,6 +1359,48 @@ int bd3mg_jacobi_sweep_incremental(const bd3mg_geom_t* g, const bd3mg_reg_t* r, 
                                               ws, s, nullptr, 0, (double*)resid, refresh != 0),
                     jacobi_sweep_impl<float>(g, r, (const float*)kernels, (const float*)y, sw, terms_out, info_out, ws,
                                              s, nullptr, 0, (float*)resid, refresh != 0));
+}
+
+size_t bd3mg_mg_steps_incremental_ws_bytes(const bd3mg_geom_t* g, const bd3mg_task_t* tasks, int ntasks) {
+  if (check_geom(g) != BD3MG_OK || ntasks < 1 || ntasks > kMaxJobs) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  std::vector<void*> hd(ntasks, reinterpret_cast<void*>(uintptr_t(4096)));  // placeholders: sizing only
+  void* resid = reinterpret_cast<void*>(uintptr_t(4096));
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g,
+                      mg_steps_impl<double>(g, &r, nullptr, nullptr, tasks, ntasks, nullptr, ws, 0, nullptr, 0,
+                                            (double* const*)hd.data(), (double*)resid),
+                      mg_steps_impl<float>(g, &r, nullptr, nullptr, tasks, ntasks, nullptr, ws, 0, nullptr, 0,
+                                           (float* const*)hd.data(), (float*)resid));
+  });
+}
+
+int bd3mg_mg_steps_incremental(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* y,
+                               const bd3mg_task_t* tasks, int ntasks, void* const* hd, void* resid,
+                               double* info_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !info_out || !hd || !resid) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    mg_steps_impl<double>(g, r, (const double*)kernels, (const double*)y, tasks, ntasks, info_out, ws,
+                                          (cudaStream_t)stream, nullptr, 0, (double* const*)hd, (double*)resid),
+                    mg_steps_impl<float>(g, r, (const float*)kernels, (const float*)y, tasks, ntasks, info_out, ws,
+                                         (cudaStream_t)stream, nullptr, 0, (float* const*)hd, (float*)resid));
+}
+
+int bd3mg_eval_f_resid(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* resid, const void* x,
+                       const void* snap, double* terms_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !resid || !x || !terms_out) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  return DISPATCH_T(g,
+                    eval_rows_impl<double>(g, r, nullptr, nullptr, (const double*)x, 0, g->nz, 0, g->nz - 1,
+                                           (const double*)snap, terms_out, ws, s, (const double*)resid),
+                    eval_rows_impl<float>(g, r, nullptr, nullptr, (const float*)x, 0, g->nz, 0, g->nz - 1,
+                                          (const float*)snap, terms_out, ws, s, (const float*)resid));
 }
 
 /* ---- peer (NVLink) memory: halo inboxes written by other ranks' kernels ---- */

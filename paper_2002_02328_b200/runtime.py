@@ -566,9 +566,18 @@ class CyclicSweeper:
     worker: blocks 0..B-1 in order, each step seeing every earlier update,
     runtime.py:158-180) followed by the per-sweep recorder.  One fused
     ``bd3mg_mg_steps`` launch set per block (in place); capturable as a
-    CUDA graph like JacobiSweeper."""
+    CUDA graph like JacobiSweeper.
 
-    def __init__(self, obj: Objective, x0, block_height: int, dtype: torch.dtype = torch.float64):
+    ``incremental=True`` selects the "hd-incremental" variant of the same
+    schedule: each block keeps H E_S d_mem from its previous visit and the
+    residual r = H x - y is kept on the device by linearity
+    (bd3mg_mg_steps_incremental), so no step runs a residual correlation and
+    the recorder takes its data term from r (bd3mg_eval_f_resid); r is
+    recomputed exactly on the first sweep and every ``refresh_every``
+    sweeps (0: never again)."""
+
+    def __init__(self, obj: Objective, x0, block_height: int, dtype: torch.dtype = torch.float64,
+                 incremental: bool = False, refresh_every: int = 0):
         self.obj, self.dtype = obj, dtype
         self.x = D.to_device(x0, dtype).clone()
         self.prev = torch.zeros_like(self.x)
@@ -591,33 +600,71 @@ class CyclicSweeper:
         self.K = obj.psf.device_kernels(dtype, dev)
         self.Y = obj.device_y(dtype, dev)
         self.k = 0
+        self.sweeps = 0
         self.graph = None
+        self.graphs = {}
+        self.refresh_every = refresh_every
+        self.resid = None
+        if incremental:
+            rz = (obj.psf.kdims.kz - 1) // 2
+            plane = dims.ny * dims.nx
+            rows = [min(dims.nz - 1, b.z_hi + rz) - max(0, b.z_lo - rz) + 1 for b in self.blocks]
+            self.hd = torch.zeros(sum(rows) * plane, dtype=dtype, device=dev)
+            offs = np.cumsum([0] + rows[:-1]) * plane
+            esz = self.hd.element_size()
+            self._hd = [(C.c_void_p * 1)(self.hd.data_ptr() + int(o) * esz) for o in offs]
+            self.resid = torch.zeros_like(self.x)
+            self.ws_bytes = max(N.ws_bytes(N.lib.bd3mg_mg_steps_incremental_ws_bytes(D.byref(self.geom), t, 1))
+                                for t in self.tasks)
+            self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
 
     @property
     def nblocks(self) -> int:
         return len(self.blocks)
 
-    def _launch(self) -> None:
+    def _refresh_due(self) -> bool:
+        return self.sweeps == 0 or (self.refresh_every > 0 and self.sweeps % self.refresh_every == 0)
+
+    def _launch(self, refresh: bool = False) -> None:
         s = D.stream_handle()
+        if self.resid is not None and refresh:  # r = H x - y exactly (the device H, then minus y)
+            from .blur import correlate_rows
+            correlate_rows(self.obj.psf, self.x, 0, 0, self.obj.dims.nz - 1, False, out=self.resid)
+            self.resid.sub_(self.Y)
         for i, t in enumerate(self.tasks):
-            N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
-                                         t, 1, self.info[i].data_ptr(), self.ws.data_ptr(), self.ws_bytes, s))
-        N.check(N.lib.bd3mg_eval_f(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
-                                   self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
-                                   self.ews.data_ptr(), self.eval_bytes, s))
+            if self.resid is not None:
+                N.check(N.lib.bd3mg_mg_steps_incremental(
+                    D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(), t, 1, self._hd[i],
+                    self.resid.data_ptr(), self.info[i].data_ptr(), self.ws.data_ptr(), self.ws_bytes, s))
+            else:
+                N.check(N.lib.bd3mg_mg_steps(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(),
+                                             self.Y.data_ptr(), t, 1, self.info[i].data_ptr(), self.ws.data_ptr(),
+                                             self.ws_bytes, s))
+        if self.resid is not None:
+            N.check(N.lib.bd3mg_eval_f_resid(D.byref(self.geom), D.byref(self.reg), self.resid.data_ptr(),
+                                             self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
+                                             self.ews.data_ptr(), self.eval_bytes, s))
+        else:
+            N.check(N.lib.bd3mg_eval_f(D.byref(self.geom), D.byref(self.reg), self.K.data_ptr(), self.Y.data_ptr(),
+                                       self.x.data_ptr(), self.snap.data_ptr(), self.terms.data_ptr(),
+                                       self.ews.data_ptr(), self.eval_bytes, s))
         self.snap.copy_(self.x)
 
     def capture(self) -> None:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._launch()
-        self.graph = g
+        for refresh in ((False, True) if self.resid is not None else (False,)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch(refresh)
+            self.graphs[refresh] = g
+        self.graph = self.graphs[False]
 
     def sweep(self) -> None:
-        if self.graph is not None:
-            self.graph.replay()
+        refresh = self.resid is not None and self._refresh_due()
+        if self.graphs:
+            self.graphs[refresh].replay()
         else:
-            self._launch()
+            self._launch(refresh)
+        self.sweeps += 1
         self.k += len(self.blocks)
 
     def check(self) -> None:

@@ -294,3 +294,29 @@ def test_p2p_mirrors_keep_inboxes_current_on_nonfinite_gradient():
     assert torch.equal(got, want)
     for s in shards:
         s.close()
+
+
+@pytest.mark.parametrize("dtype,refresh", [(torch.float64, 0), (torch.float64, 3), (torch.float32, 0)])
+def test_cyclic_incremental_variant_tracks_exact(dtype, refresh):
+    """The deterministic cyclic schedule in the "hd-incremental" variant
+    (kept residual, cached H E_S d_mem, recorder from the kept residual)
+    tracks the exact cyclic sweep to rounding, eagerly and as graphs."""
+    from paper_2002_02328_b200 import blur, configs, objective, runtime
+    cfg = configs.CONFIGS["C1"]
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    obj = objective.Objective(psf, y, params)
+    a = runtime.CyclicSweeper(obj, x0, cfg.block_height, dtype)
+    b = runtime.CyclicSweeper(obj, x0, cfg.block_height, dtype, incremental=True, refresh_every=refresh)
+    tol_x, tol_f = (1e-10, 1e-11) if dtype == torch.float64 else (2e-5, 1e-5)
+    for it in range(20):
+        if it == 2:
+            a.capture()
+            b.capture()
+        a.sweep()
+        b.sweep()
+        assert abs(a.f() - b.f()) <= tol_f * abs(a.f()), (it, a.f(), b.f())
+    xa, xb = a.x.double().cpu().numpy(), b.x.double().cpu().numpy()
+    assert np.linalg.norm(xa - xb) <= tol_x * np.linalg.norm(xa)
+    r = blur.apply_H(psf, b.x) - obj.device_y(dtype)
+    assert float(torch.linalg.vector_norm(r - b.resid)) <= (1e-11 if dtype == torch.float64 else 1e-4) * float(
+        torch.linalg.vector_norm(r))
