@@ -128,6 +128,9 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 #ifndef BD3MG_RZ2_RY5
 #define BD3MG_RZ2_RY5 4  // rows per thread of the two-plane kernel for 3x3 / 5x5 taps (measured: 4 >= 8 with FFMA2)
 #endif
+#ifndef BD3MG_RY2
+#define BD3MG_RY2 8  // rows per thread of the fp64 dual-input (Gram) mode
+#endif
 #ifndef BD3MG_RY1
 #define BD3MG_RY1 16  // rows per thread of the single-input modes
 #endif
@@ -138,7 +141,7 @@ struct ConvCfg {
   static constexpr int VEC = 16 / sizeof(T);        // elements per 16-byte load
   static constexpr int RX = VEC;                    // outputs per thread in x
   // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32)
-  static constexpr int RY = DUAL ? (sizeof(T) == 8 ? 8 : 4) : BD3MG_RY1;
+  static constexpr int RY = DUAL ? (sizeof(T) == 8 ? BD3MG_RY2 : 4) : BD3MG_RY1;
   static constexpr int WX = 32, WY = 4;             // a warp spans one row group
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
