@@ -246,7 +246,7 @@ def _config_dict(cfg, world):
     return {"workload": f"{cfg.name}{scal}: {cfg.dims.nx}x{cfg.dims.ny}x{cfg.dims.nz} {cfg.dtype}, PSF "
                         f"{cfg.kdims[0]}x{cfg.kdims[1]}x{cfg.kdims[2]} depth-variant Gaussian, {B} blocks x "
                         f"{cfg.block_height} planes, block-Jacobi sweep (bp3mg workers=B) + per-sweep f",
-            "global_batch": B, "blocks_per_step": B, "ranks": world,
+            "blocks_per_step": B, "ranks": world,
             "l2": "flushed between timed steps (256 MB write, untimed)",
             "regulariser": {"lam": cfg.lam, "eta": cfg.eta, "kappa": cfg.kappa, "delta": cfg.delta}}
 
