@@ -113,6 +113,29 @@ def info_to_step(info: np.ndarray, increment) -> StepInfo:
     return StepInfo(increment, gram, np.asarray(info[3:3 + k]), np.asarray(info[5:5 + k]), k)
 
 
+_WS_CACHE: dict = {}
+
+
+def _ws_bytes_cached(g: N.Geom, arr, n: int) -> int:
+    """bd3mg_mg_steps_ws_bytes memoised on what it depends on: the geometry,
+    each task's rows and which of its pointers are set, and whether the
+    tasks share one fragment (the per-update host cost of the runtime's
+    schedules)."""
+    frag0 = arr[0].frag if n else None
+    key = (g.nx, g.ny, g.nz, g.kx, g.ky, g.kz, g.dtype, n,
+           all(arr[i].frag == frag0 and arr[i].frag_z0 == arr[0].frag_z0 and arr[i].nzf == arr[0].nzf
+               for i in range(n)),
+           tuple((t.frag_z0, t.nzf, t.z_lo, t.z_hi, bool(t.d_mem), bool(t.inc_out), bool(t.x_rows),
+                  bool(t.dmem_rows)) for t in arr[:n]))
+    nbytes = _WS_CACHE.get(key)
+    if nbytes is None:
+        nbytes = N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(g), arr, n))
+        if len(_WS_CACHE) > 4096:
+            _WS_CACHE.clear()
+        _WS_CACHE[key] = nbytes
+    return nbytes
+
+
 def mg_steps_device(obj: Objective, tasks: list[N.Task], dtype: torch.dtype,
                     info: torch.Tensor | None = None, stream=None, mirrors=None) -> torch.Tensor:
     """Launch the fused block steps for `tasks` (device pointers) on the
@@ -122,7 +145,7 @@ def mg_steps_device(obj: Objective, tasks: list[N.Task], dtype: torch.dtype,
     n = len(tasks)
     arr = (N.Task * max(n, 1))(*tasks)
     g = obj.geom(dtype)
-    nbytes = N.ws_bytes(N.lib.bd3mg_mg_steps_ws_bytes(D.byref(g), arr, n))
+    nbytes = _ws_bytes_cached(g, arr, n)
     ws = D.workspace(nbytes, stream)
     dev = torch.device("cuda", torch.cuda.current_device())
     if info is None:
