@@ -1,3 +1,5 @@
+"""Throughput of the reference-API driver runtime.run at C2 (bd3mg one worker,
+bp3mg 8 workers, live engine 4 workers):  python scripts/runtime_probe.py"""
 import sys, time
 sys.path.insert(0, '.')
 import torch
