@@ -329,10 +329,17 @@ def main():
 
     if args.mode == "async":
         from paper_2002_02328_b200 import distributed
-        eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2, halo=args.halo)
+        halo, why = args.halo, ""
+        try:
+            eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2, halo=halo)
+        except RuntimeError as e:  # raised on every rank alike (the setup agrees on failures)
+            if halo != "p2p" or world == 1:
+                raise
+            halo, why = "nccl", f" (p2p unavailable: {str(e).splitlines()[0][:160]})"
+            eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2, halo=halo)
         if world > 1:
             halo_note = ("p2p: update-kernel NVLink stores into the readers' halo rings, fenced version flags "
-                         "in a shared host page" if args.halo == "p2p" else "nccl: isend/irecv halo messages")
+                         "in a shared host page" if halo == "p2p" else "nccl: isend/irecv halo messages" + why)
     elif args.mode == "cyclic":
         if world > 1:
             raise SystemExit("--mode cyclic is the single-worker schedule (N=1)")

@@ -143,7 +143,16 @@ class PeerHalo:
         ptr, self.handle = C.c_void_p(), (C.c_ubyte * N.IPC_HANDLE_BYTES)()
         from . import device as D
         D.bind(shard.x.device.index)
-        N.check(N.lib.bd3mg_peer_alloc(n * self.esz, C.byref(ptr), self.handle))
+        # a failed allocation is reported by connect_ipc on EVERY rank (after
+        # the handle exchange), so no rank is left waiting in a collective
+        self.alloc_error = None
+        if N.lib.bd3mg_peer_alloc(n * self.esz, C.byref(ptr), self.handle) != N.BD3MG_OK:
+            self.alloc_error = (N.lib.bd3mg_last_error() or b"").decode() or "peer allocation failed"
+            if not dist.is_initialized():
+                raise RuntimeError(self.alloc_error)
+            n = max(1, 2 * self.nplanes * self.plane)
+            self.fallback = torch.empty(n, dtype=shard.x.dtype, device=shard.x.device)  # keeps the layout valid
+            ptr = C.c_void_p(self.fallback.data_ptr())
         self.ptr = ptr.value
         self.opened: list[int] = []
         dims = shard.x.shape[1:]
@@ -191,7 +200,10 @@ class PeerHalo:
         N, C = self.N, self.C
         world = dist.get_world_size(group)
         handles = [None] * world
-        dist.all_gather_object(handles, bytes(self.handle), group=group)
+        dist.all_gather_object(handles, None if self.alloc_error else bytes(self.handle), group=group)
+        if any(h is None for h in handles):
+            raise RuntimeError(f"p2p halos: peer allocation failed on rank(s) "
+                               f"{[q for q, h in enumerate(handles) if h is None]}")
         bases = {}
         for q in sorted({q for q, _, _ in self.send}):
             ptr = C.c_void_p()
@@ -212,7 +224,8 @@ class PeerHalo:
         self.opened = []
         if self.ptr:
             self.inbox = None
-            self.N.lib.bd3mg_peer_free(self.ptr)
+            if self.alloc_error is None:
+                self.N.lib.bd3mg_peer_free(self.ptr)
             self.ptr = 0
 
 
@@ -858,22 +871,38 @@ class RingHub:
         from . import _native as N
         hub = cls()
         world = plan.layout.world
-        name = [f"/dev/shm/bd3mg_async_{uuid.uuid4().hex}" if rank == 0 else None]
-        dist.broadcast_object_list(name, src=0, group=group)
-        hub.path = name[0]
         nbytes = plan.nflags * 8
+        # every failure is agreed on by all ranks before it is raised, so no
+        # rank is left waiting in a collective
+        msg = [None]
         if rank == 0:
-            fd = os.open(hub.path, os.O_RDWR | os.O_CREAT | os.O_EXCL, 0o600)
-            os.ftruncate(fd, max(4096, -(-nbytes // 4096) * 4096))
-            os.close(fd)
-        dist.barrier(group=group)
-        hub.mm, flags, hub.host, fdev = _map_flags(hub.path, nbytes)
+            path = f"/dev/shm/bd3mg_async_{uuid.uuid4().hex}"
+            try:
+                fd = os.open(path, os.O_RDWR | os.O_CREAT | os.O_EXCL, 0o600)
+                os.ftruncate(fd, max(4096, -(-nbytes // 4096) * 4096))
+                os.close(fd)
+                msg = [("ok", path)]
+            except OSError as e:
+                msg = [("error", f"flag page: {e}")]
+        dist.broadcast_object_list(msg, src=0, group=group)
+        if msg[0][0] != "ok":
+            raise RuntimeError(f"async peer rings: {msg[0][1]}")
+        hub.path = msg[0][1]
         ptr, h = C.c_void_p(), (C.c_ubyte * N.IPC_HANDLE_BYTES)()
-        N.check(N.lib.bd3mg_peer_alloc(max(1, plan.ring_planes[rank] * int(np.prod(x.shape[1:]))) * x.element_size(),
-                                       C.byref(ptr), h))
-        hub.own.append(ptr.value)
+        mine = None
+        try:
+            hub.mm, flags, hub.host, fdev = _map_flags(hub.path, nbytes)
+            N.check(N.lib.bd3mg_peer_alloc(
+                max(1, plan.ring_planes[rank] * int(np.prod(x.shape[1:]))) * x.element_size(), C.byref(ptr), h))
+            hub.own.append(ptr.value)
+            mine = bytes(h)
+        except (RuntimeError, ValueError, OSError):
+            mine = None
         handles = [None] * world
-        dist.all_gather_object(handles, bytes(h), group=group)
+        dist.all_gather_object(handles, mine, group=group)
+        if any(q is None for q in handles):
+            hub.close(group=None)
+            raise RuntimeError(f"async peer rings: setup failed on rank(s) {[q for q, v in enumerate(handles) if v is None]}")
         bases = {rank: ptr.value}
         for q in sorted({q for p, q, _, _, _ in plan.units if p == rank}):
             dp = C.c_void_p()
