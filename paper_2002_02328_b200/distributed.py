@@ -904,12 +904,20 @@ class RingHub:
             hub.close(group=None)
             raise RuntimeError(f"async peer rings: setup failed on rank(s) {[q for q, v in enumerate(handles) if v is None]}")
         bases = {rank: ptr.value}
+        err = ""
         for q in sorted({q for p, q, _, _, _ in plan.units if p == rank}):
             dp = C.c_void_p()
-            N.check(N.lib.bd3mg_peer_open((C.c_ubyte * N.IPC_HANDLE_BYTES).from_buffer_copy(handles[q]),
-                                          C.byref(dp)))
+            if N.lib.bd3mg_peer_open((C.c_ubyte * N.IPC_HANDLE_BYTES).from_buffer_copy(handles[q]),
+                                     C.byref(dp)) != N.BD3MG_OK:
+                err = (N.lib.bd3mg_last_error() or b"").decode() or f"cannot map rank {q}'s ring"
+                break
             bases[q] = dp.value
             hub.opened.append(dp.value)
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        if any(errs):
+            hub.close(group=None)
+            raise RuntimeError(f"async peer rings: {next(e for e in errs if e)}")
         ring = PeerRing(plan, rank, x, z0, ptr.value, bases, flags, fdev)
         torch.cuda.synchronize()  # slot 0 of every ring written before anyone reads it
         dist.barrier(group=group)
