@@ -554,6 +554,36 @@ def roofline(obj, cfg, dtype, torch, N, D, blur):
         torch.cuda.synchronize()
         t = s.elapsed_time(e) / reps / 1e3
         res["Ht" if adj else "H"] = {"ms": t * 1e3, "gvox_s": obj.dims.count / t / 1e9, "tflops": flops / t / 1e12}
+    # the fused gradient (full volume) and one fused block step
+    # (h = block height, middle block, d_mem = 0.01 N(0,1)) timed separately
+    from paper_2002_02328_b200 import directions, objective
+    from paper_2002_02328_b200.volume import SliceBlock
+
+    def timed(fn, reps=10):
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps / 1e3
+
+    t = timed(lambda: objective.grad_rows_device(obj, x, 0, 0, nz - 1))
+    fg = 2 * flops  # H over every row, then H^T over every row
+    res["grad_f"] = {"ms": t * 1e3, "tflops": fg / t / 1e12, "what": "fused gradient, full volume (H, H^T, regulariser)"}
+    h = cfg.block_height
+    lo = (nz // 2 // h) * h
+    blk = SliceBlock(lo, min(lo + h - 1, nz - 1))
+    d_mem = (0.01 * torch.randn(blk.count(obj.dims), dtype=torch.float64, device="cuda")).to(dtype)
+    inc = torch.empty_like(d_mem)
+    task = N.Task(x.data_ptr(), 0, nz, blk.z_lo, blk.z_hi, d_mem.data_ptr(), inc.data_ptr(), None, None)
+    t = timed(lambda: directions.mg_steps_device(obj, [task], dtype))
+    fb = blur.flops_jacobi_sweep(obj.dims, psf.kdims, [blk])
+    res["mg_step_block"] = {"ms": t * 1e3, "tflops": fb / t / 1e12, "planes": blk.z_hi - blk.z_lo + 1,
+                            "what": "one fused block step (gradient, forward-only Gram, 2x2 solve, increment)"}
     # FMA pipe probe
     probe = torch.empty(148 * 8 * 256, dtype=dtype, device="cuda")
     import ctypes
