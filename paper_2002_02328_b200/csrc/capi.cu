@@ -460,6 +460,8 @@ struct StepOpts {
   SideStream* ss = nullptr;    // run reg_gram next to the Gram correlation
   const bd3mg_mirror_t* mirrors = nullptr;  // rows of the updated iterate also stored to (peer) buffers
   int nmirrors = 0;
+  const double* fin_sums = nullptr;  // the sweep's recorder sums: finalised by the update launch
+  double* fin_terms = nullptr;
   T* r_full = nullptr;         // variant "hd-incremental": r = Hx - y kept across calls (plane 0 = r_full_z0)
   int64_t r_full_z0 = 0;
   bool r_refresh = false;      // recompute r_full exactly in this call
@@ -774,6 +776,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     UpdArgs<T> ua;
     memset(&ua, 0, sizeof(ua));
     ua.nblocks = nt;
+    ua.fin_sums = opt.fin_sums; ua.fin_terms = opt.fin_terms;
+    ua.fin_eta = r->eta; ua.fin_lam = r->lam; ua.fin_kappa = r->kappa;
     int mc = 1;
     for (int t = 0; t < nt; ++t) {
       UpdBlock<T>& B = ua.blk[t];
@@ -967,6 +971,10 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     opt.r_refresh = r_refresh;
   }
   if (fused) { opt.greg = grb.data(); opt.omega = wb.data(); }
+#ifndef BD3MG_EXP_SKIP_UPDATE
+  opt.fin_sums = sums;  // the update launch writes the recorder terms
+  opt.fin_terms = terms;
+#endif
   SideStream* ss = nullptr;
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
   if (!ws.measure) {
@@ -1013,8 +1021,10 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   ws.off = sub.off;
   if (rc != BD3MG_OK || ws.measure) return rc;
   if (!ws.ok()) return ws_fail(ws);
+#ifdef BD3MG_EXP_SKIP_UPDATE
   eval_finalize_kernel<<<1, 1, 0, s>>>(sums, sums + 1, r->eta, r->lam, r->kappa, terms); launched();
   CU(cudaGetLastError());
+#endif
   return BD3MG_OK;
 }
 

@@ -185,6 +185,10 @@ struct UpdBlock {
 template <typename T>
 struct UpdArgs {
   int nblocks;
+  // the sweep's recorder terms (eval_finalize_kernel), folded into this launch
+  const double* fin_sums;  // [data sum, ew5...] or null
+  double* fin_terms;
+  double fin_eta, fin_lam, fin_kappa;
   UpdBlock<T> blk[kMaxJobs];
 };
 
@@ -219,6 +223,14 @@ template <typename T, int NSEG>
 __global__ void __launch_bounds__(kEwNT) update_kernel(const __grid_constant__ UpdArgs<T> p,
                                                         const __grid_constant__ MirArgs<T, NSEG> m,
                                                         const double* __restrict__ info) {
+  if (p.fin_terms && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const double* sums = p.fin_sums;
+    const double data = 0.5 * sums[0], box = p.fin_eta * sums[1], tv = p.fin_lam * sums[2], ax = p.fin_kappa * sums[3];
+    double* t = p.fin_terms;
+    t[0] = data; t[1] = box; t[2] = tv; t[3] = ax;
+    t[4] = data + box + tv + ax;
+    t[5] = sums[4]; t[6] = sums[5];
+  }
   const UpdBlock<T>& B = p.blk[blockIdx.y];
   if ((int)blockIdx.x >= B.ctas) return;
   const double* o = info + blockIdx.y * kInfoNV;
