@@ -101,17 +101,18 @@ def main():
     fs, its = [], []
     torch.cuda.synchronize()
     t_upd = 0.0
-    for k in range(sweeps * B):
-        lo_t = min(s.t for s in ranks)
-        ready = [s for s in ranks if s.t - lo_t < 2]
+    for sweep in range(sweeps):
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rng.choice(ready).update()
+        for _ in range(B):  # one sweep's worth of updates, enqueued without host syncs
+            lo_t = min(s.t for s in ranks)
+            ready = [s for s in ranks if s.t - lo_t < 2]
+            rng.choice(ready).update()
         torch.cuda.synchronize()
         t_upd += time.perf_counter() - t0
-        if (k + 1) % B == 0:
-            full = torch.cat([s.x[s.o_lo - s.l_lo:s.o_hi - s.l_lo + 1] for s in ranks])
-            fs.append(f_of(obj, full))
-            its.append(k + 1)
+        full = torch.cat([s.x[s.o_lo - s.l_lo:s.o_hi - s.l_lo + 1] for s in ranks])
+        fs.append(f_of(obj, full))
+        its.append((sweep + 1) * B)
     st = [v for s in ranks for v in s.staleness]
     hub.close()
     out["async"] = {"block_iterations": its, "f": fs, "ms_per_update_1gpu": t_upd / (sweeps * B) * 1e3,
