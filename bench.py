@@ -154,8 +154,6 @@ def reference_arm(args, cfg_name):
     from oracle import oracle as O
     from paper_2002_02328_b200 import configs
 
-    kind = "reference" if O.ref_core_available() else "port"
-    O.core("ref" if kind == "reference" else "c", threads=1)
     cfg = bench_config(args, world)
     psf_k, y, x0 = _host_problem(cfg, O)
     crit = O.Criterion(psf_k, y, cfg.lam, cfg.eta, cfg.kappa, cfg.delta)
@@ -171,6 +169,30 @@ def reference_arm(args, cfg_name):
     x = x0.copy()
     prev = np.zeros_like(x)
     snap = x.copy()
+
+    # the reference has two CPU backends (src/kernels.py:16-28): its compiled
+    # core and the scipy fallback; report the faster on this host (SURVEY.md
+    # 8(d)), probed on one batch of `threads` block steps each
+    def probe_batch():
+        def one(b):
+            lo, hi = b
+            s_lo, s_hi = O.support(nz, crit.kz, lo, hi)
+            return O.mg_direction(crit, x[s_lo:s_hi + 1].copy(), s_lo, lo, hi, prev[lo:hi + 1].ravel().copy())
+        t0 = time.perf_counter()
+        list(pool.map(one, blocks[:threads]))
+        return time.perf_counter() - t0
+
+    cands = ["ref" if O.ref_core_available() else "c", "scipy"]
+    timing = {}
+    for name in cands:
+        O.core(name, threads=1)
+        timing[name] = probe_batch()
+    best = min(timing, key=timing.get)
+    O.core(best, threads=1)
+    kind = "reference" if best == "ref" else "port"
+    core_desc = {"ref": "reference _core.pyx compiled from /root/reference (oracle/_ref)",
+                 "c": "oracle/bd3mg_oracle.c (bitwise the reference core)",
+                 "scipy": "the reference's scipy backend (_kernels_np.py) restated in oracle/oracle.py"}
 
     def sweep():
         nonlocal x, snap
@@ -201,9 +223,9 @@ def reference_arm(args, cfg_name):
     value = args.steps * B / total
     sample = (f"{args.steps} timed steps x {B} of {len(all_blocks)} blocks of config {cfg.name} "
               f"after {args.warmup} warm-up; "
-              f"bp3mg barrier, {threads} worker threads; core: "
-              + ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if kind == "reference"
-                 else "oracle/bd3mg_oracle.c (bitwise the reference core)"))
+              f"bp3mg barrier, {threads} worker threads; core: {core_desc[best]}; the faster reference "
+              f"backend on this host (probe, {threads} block steps: "
+              + ", ".join(f"{n} {timing[n]:.2f} s" for n in cands) + ")")
     line = {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -92,15 +92,63 @@ class _RefCore:
         return self.mod.depthvar_correlate_adjoint(np.ascontiguousarray(frag, dtype=np.float64), ker, z0, lo, hi)
 
 
+class _ScipyCore:
+    """Restatement of the reference's fallback backend (src/_kernels_np.py:15-46):
+    per output row and tap page, one 2-D ``scipy.ndimage.correlate`` with
+    zero padding, accumulated in tap order; the adjoint correlates the page
+    flipped in y and x (:43).  Same contract as the compiled core; rounding
+    differs from it by <= 1e-13 (reference tests/test_blur.py:151-159).  Used
+    by bench.py's reference arm, which reports the faster of the two
+    reference backends."""
+
+    name = "scipy"
+
+    def __init__(self):
+        from scipy import ndimage
+        self.nd = ndimage
+
+    def correlate(self, frag, ker, z0, lo, hi):
+        frag = np.ascontiguousarray(frag, dtype=np.float64)
+        nzf, ny, nx = frag.shape
+        kz = ker.shape[1]
+        rz = (kz - 1) // 2
+        out = np.zeros((hi - lo + 1, ny, nx))
+        for zo in range(lo, hi + 1):
+            for a in range(kz):
+                zi = zo + a - rz - z0
+                if 0 <= zi < nzf:
+                    out[zo - lo] += self.nd.correlate(frag[zi], ker[zo, a], mode="constant", cval=0.0)
+        return out
+
+    def correlate_adjoint(self, frag, ker, z0, lo, hi):
+        frag = np.ascontiguousarray(frag, dtype=np.float64)
+        nzf, ny, nx = frag.shape
+        nzk, kz = ker.shape[0], ker.shape[1]
+        rz = (kz - 1) // 2
+        out = np.zeros((hi - lo + 1, ny, nx))
+        for zi in range(lo, hi + 1):
+            for a in range(kz):
+                zo = zi + rz - a
+                if 0 <= zo < nzk and 0 <= zo - z0 < nzf:
+                    out[zi - lo] += self.nd.correlate(frag[zo - z0], ker[zo, a, ::-1, ::-1], mode="constant",
+                                                      cval=0.0)
+        return out
+
+
 _core = None
 
 
 def core(kind: str | None = None, threads: int | None = None):
-    """Select/return the active H/H^T core ("c" default, or "ref")."""
+    """Select/return the active H/H^T core ("c" default, "ref" or "scipy")."""
     global _core
     if kind is not None or _core is None:
         kind = kind or os.environ.get("BD3MG_ORACLE_CORE", "c")
-        _core = _RefCore() if kind == "ref" else _CCore(threads or int(os.environ.get("BD3MG_ORACLE_THREADS", "1")))
+        if kind == "ref":
+            _core = _RefCore()
+        elif kind == "scipy":
+            _core = _ScipyCore()
+        else:
+            _core = _CCore(threads or int(os.environ.get("BD3MG_ORACLE_THREADS", "1")))
     return _core
 
 
