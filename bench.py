@@ -632,6 +632,9 @@ def roofline(obj, cfg, dtype, torch, N, D, blur):
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": "measured: bd3mg_fma_probe (dense FMA chains) on this GPU, this run "
                            "(MEASURED_PEAKS.json has no FP64/FP32 entry)",
+            "bound_note": "FMA-pipe bound, not hbm/tensor: the depth-variant correlation is a direct convolution "
+                          "with per-output-plane coefficients (~34 flop/B in fp64), no dense contraction for the "
+                          "tensor cores (BASELINE north_star: 'vs FP64 FMA roofline')",
             "algorithmic_flops_per_launch": flops,
             "algorithmic_bytes_per_launch": 2 * obj.dims.count * x.element_size(),
             "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram read+write)"}
