@@ -207,3 +207,29 @@ def test_peer_rings_ipc_processes(world, tmp_path, c1):
     assert x.shape == x0.shape
     assert int(np.load(tmp_path / "stale.npy").max()) <= 2
     assert objective.eval_f(obj, x) < objective.eval_f(obj, x0)
+
+
+def test_peer_rings_fp32_lockstep_tracks_fp64(c1):
+    """fp32 ranks on peer halo rings under the lockstep schedule track the
+    fp64 ranks to fp32 rounding."""
+    from paper_2002_02328_b200.distributed import AsyncShard, RingHub, RingPlan, SlabLayout, cuda_block_step, ring_slots
+    obj, x0, cfg = c1
+    out = {}
+    for dtype in (torch.float64, torch.float32):
+        lay = SlabLayout.build(obj.dims.nz, obj.psf.kdims.kz, 4, 3)
+        xs, z0s = [], []
+        for r in range(3):
+            lo, hi = lay.local(r)
+            xs.append(torch.from_numpy(np.ascontiguousarray(x0[lo:hi + 1])).cuda().to(dtype))
+            z0s.append(lo)
+        hub, rings = RingHub.local(RingPlan(lay, ring_slots(1)), xs, z0s)
+        step = cuda_block_step(obj, dtype)
+        shards = [AsyncShard(lay, r, xs[r], torch.zeros_like(xs[r]), rings[r], step, 1) for r in range(3)]
+        for _ in range(4):
+            for s in shards:
+                s.update()
+                torch.cuda.synchronize()
+        out[dtype] = _gather(shards).astype(np.float64)
+        hub.close()
+    a, b = out[torch.float64], out[torch.float32]
+    assert np.linalg.norm(a - b) <= 2e-5 * np.linalg.norm(a)
