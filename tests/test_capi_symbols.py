@@ -81,3 +81,26 @@ def test_sharded_fp32_workspace_sizing():
     a = N.lib.bd3mg_jacobi_sweep_ws_bytes(C.byref(g), C.byref(with_rec))
     b = N.lib.bd3mg_jacobi_sweep_ws_bytes(C.byref(g), C.byref(no_rec))
     assert a >= 82051328 and a > b
+
+
+def test_peer_and_flag_entry_points_validate_without_a_gpu():
+    """Argument checks of the multi-GPU entry points return EINVAL before any
+    CUDA call (runnable on the CPU-only host)."""
+    import ctypes as C
+
+    from paper_2002_02328_b200 import _native as N
+    flags = (N.Flag * (N.MAX_FLAGS + 1))()
+    assert N.lib.bd3mg_publish(flags, N.MAX_FLAGS + 1, None) == N.BD3MG_EINVAL
+    assert N.lib.bd3mg_publish(None, 1, None) == N.BD3MG_EINVAL
+    assert N.lib.bd3mg_publish(flags, 0, None) == N.BD3MG_OK  # nothing to publish
+    dev = C.c_void_p()
+    assert N.lib.bd3mg_host_register(None, 4096, C.byref(dev)) == N.BD3MG_EINVAL
+    handle = (C.c_ubyte * N.IPC_HANDLE_BYTES)()
+    assert N.lib.bd3mg_peer_alloc(0, C.byref(dev), handle) == N.BD3MG_EINVAL
+    assert N.lib.bd3mg_peer_open(None, C.byref(dev)) == N.BD3MG_EINVAL
+    g = N.Geom(16, 16, 8, 3, 3, 3, N.BD3MG_F64)
+    r = N.Reg(1e-2, 1e-1, 0.05, 1e-2, 0.0, 1.0)
+    assert N.lib.bd3mg_mg_steps_incremental(C.byref(g), C.byref(r), None, None, None, 1, None, None, None, None,
+                                            0, None) == N.BD3MG_EINVAL
+    assert N.lib.bd3mg_eval_f_resid(C.byref(g), C.byref(r), None, None, None, None, None, 0, None) == N.BD3MG_EINVAL
+    assert b"null" in N.lib.bd3mg_last_error()

@@ -320,3 +320,23 @@ def test_cyclic_incremental_variant_tracks_exact(dtype, refresh):
     r = blur.apply_H(psf, b.x) - obj.device_y(dtype)
     assert float(torch.linalg.vector_norm(r - b.resid)) <= (1e-11 if dtype == torch.float64 else 1e-4) * float(
         torch.linalg.vector_norm(r))
+
+
+def test_cyclic_incremental_ragged_blocks():
+    """Cyclic hd-incremental with a ragged tail block tracks the exact cyclic sweep."""
+    from paper_2002_02328_b200 import blur, objective, runtime
+    from paper_2002_02328_b200.volume import Dims3
+    dims = Dims3(40, 36, 22)
+    psf = blur.depth_variant_stack(dims, (5, 5, 7), (0.8, 1.6), (1.0, 2.0))
+    rng = np.random.Generator(np.random.Philox(9))
+    y = rng.uniform(0, 1, dims.shape)
+    x0 = rng.uniform(0, 1, dims.shape)
+    obj = objective.Objective(psf, y, objective.RegParams(lam=1e-2, eta=1e-1, kappa=0.05, delta=1e-2))
+    a = runtime.CyclicSweeper(obj, x0, 4, torch.float64)
+    b = runtime.CyclicSweeper(obj, x0, 4, torch.float64, incremental=True)
+    for _ in range(8):
+        a.sweep()
+        b.sweep()
+        assert abs(a.f() - b.f()) <= 1e-11 * abs(a.f())
+    xa, xb = a.x.cpu().numpy(), b.x.cpu().numpy()
+    assert np.linalg.norm(xa - xb) <= 1e-10 * np.linalg.norm(xa)
