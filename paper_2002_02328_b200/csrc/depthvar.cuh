@@ -73,10 +73,39 @@ struct ConvArgs {
   int nz_global;        // global depth (axial far-face rule)
   int njobs;
   int tiles_x, tiles_y;
+  int raster_group;     // tiles per rasterisation group (0: plain x, y, z order); see cta_pos
   double* partials;     // [gridDim.z * tiles_y * tiles_x][NV]
   double two_eta, lam, two_kappa, delta2, x_min, x_max;
   ConvJob<T> jobs[kMaxJobs];
 };
+
+// Launch-order rasterisation of the (tile, z) grid.  Plain order walks all
+// tiles of one output plane before the next, so on large planes the kz
+// input planes of the CTAs in flight outgrow L2 and are re-read from DRAM
+// (C5: each input plane ~10x).  With raster_group = G the linear launch
+// index walks z inside groups of G tiles, keeping the in-flight working set
+// at G tiles x (in-flight planes + kz) -- L2-resident.  `cta` is the logical
+// (z, tile) row of the partial sums, so layouts and reductions do not change.
+struct CtaPos {
+  int tx, ty, z;
+  long long cta;
+};
+BD3MG_D CtaPos cta_pos(int group) {
+  const long long nx = gridDim.x, ny = gridDim.y, nz = gridDim.z, T = nx * ny;
+  const long long L = blockIdx.x + nx * (blockIdx.y + ny * (long long)blockIdx.z);
+  long long t, z;
+  if (group <= 0 || group >= T) {
+    t = L % T;
+    z = L / T;
+  } else {
+    const long long g = L / ((long long)group * nz), full = T / group;
+    const long long gg = g < full ? group : T - full * group;
+    const long long rem = L - g * group * nz;
+    z = rem / gg;
+    t = g * group + rem % gg;
+  }
+  return {(int)(t % nx), (int)(t / nx), (int)z, z * T + t};
+}
 
 template <int MODE>
 struct ModeNV {
@@ -240,11 +269,12 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::coef_bytes(p.kz));
   double* red_s = reinterpret_cast<double*>(mbar + 2);
 
-  const int zidx = blockIdx.z;
+  const CtaPos pos = cta_pos(p.raster_group);
+  const int zidx = pos.z;
   const int jid = find_job(p, zidx);
   const ConvJob<T>& job = p.jobs[jid];
   const int zo = job.out_lo + (zidx - job.work_begin);
-  const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
+  const int x0 = pos.tx * Cfg::TX, y0 = pos.ty * Cfg::TY;
   const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
   const int rz = (p.kz - 1) / 2;
   const bool tma = job.use_tma != 0;
@@ -445,7 +475,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   if constexpr (NV > 0) {
     cta_reduce<NV, Cfg::NT>(part, red_s);
     if (threadIdx.x == 0) {
-      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      const long long cta = pos.cta;
 #pragma unroll
       for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
     }
@@ -601,12 +631,13 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * Cfg::BUF_BYTES + Cfg::SLICE_BYTES);
   double* red_s = reinterpret_cast<double*>(mbar + 2);
 
-  const int zidx = blockIdx.z;
+  const CtaPos pos = cta_pos(p.raster_group);
+  const int zidx = pos.z;
   const int jid = find_job(p, zidx);
   const ConvJob<T>& job = p.jobs[jid];
   const int zo0 = job.out_lo + 2 * (zidx - job.work_begin);
   const bool has1 = zo0 + 1 < job.out_lo + job.nout;
-  const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
+  const int x0 = pos.tx * Cfg::TX, y0 = pos.ty * Cfg::TY;
   const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
   const int rz = (p.kz - 1) / 2;
   const bool tma = job.use_tma != 0;
@@ -817,7 +848,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   if constexpr (NV > 0) {
     cta_reduce<NV, Cfg::NT>(part, red_s);
     if (threadIdx.x == 0) {
-      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      const long long cta = pos.cta;
 #pragma unroll
       for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
     }
@@ -836,14 +867,15 @@ __global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_c
   T* coef_s = reinterpret_cast<T*>(smem_raw);
   size_t coef_bytes = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
   double* red_s = reinterpret_cast<double*>(smem_raw + coef_bytes);
-  const int zidx = blockIdx.z;
+  const CtaPos pos = cta_pos(p.raster_group);
+  const int zidx = pos.z;
   const int jid = find_job(p, zidx);
   const ConvJob<T>& job = p.jobs[jid];
   const int zo = job.out_lo + (zidx - job.work_begin);
   stage_coefs<T, ADJ>(p, zo, coef_s, kGenericNT);
   __syncthreads();
-  const int x = blockIdx.x * kGenericTX + (threadIdx.x % kGenericTX);
-  const int y = blockIdx.y * kGenericTY + (threadIdx.x / kGenericTX);
+  const int x = pos.tx * kGenericTX + (threadIdx.x % kGenericTX);
+  const int y = pos.ty * kGenericTY + (threadIdx.x / kGenericTX);
   const int rz = (p.kz - 1) / 2, ry = (p.ky - 1) / 2, rx = (p.kx - 1) / 2;
   constexpr int NV = ModeNV<MODE>::value;
   double part[NV > 0 ? NV : 1];
@@ -894,7 +926,7 @@ __global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_c
   if constexpr (NV > 0) {
     cta_reduce<NV, kGenericNT>(part, red_s);
     if (threadIdx.x == 0) {
-      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      const long long cta = pos.cta;
       for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
     }
   }
