@@ -8,5 +8,6 @@ run C3 --config C3
 run C4 --config C4
 run C2_cyclic --config C2 --mode cyclic
 run C2_async --config C2 --mode async
+run C3_cyclic --config C3 --mode cyclic --steps 10
 run C5 --config C5 --steps 3 --warmup 3
 run ref_C2 --impl reference --config C2 --steps 2 --warmup 3
