@@ -155,12 +155,15 @@ def reference_arm(args, cfg_name):
     from paper_2002_02328_b200 import configs
 
     cfg = bench_config(args, world)
-    psf_k, y, x0 = _host_problem(cfg, O)
-    crit = O.Criterion(psf_k, y, cfg.lam, cfg.eta, cfg.kappa, cfg.delta)
     nz = cfg.dims.nz
     all_blocks = O.blocks_of(nz, cfg.block_height)
     cores = os.cpu_count() or 1
     threads = max(1, min(cores, len(all_blocks)))
+    if _ref_block_flops(cfg) > 150e9:  # ~minutes per block step on one core (C5): extrapolate
+        _reference_extrapolated(args, cfg, world, O, threads)
+        return
+    psf_k, y, x0 = _host_problem(cfg, O)
+    crit = O.Criterion(psf_k, y, cfg.lam, cfg.eta, cfg.kappa, cfg.delta)
     # bounded sample per step: at most 16 blocks of the barrier cycle (all of
     # them at N=1); every block costs the same, so block-it/s is unbiased
     blocks = all_blocks[:16]
@@ -230,6 +233,75 @@ def reference_arm(args, cfg_name):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config_dict(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _ref_block_flops(cfg) -> int:
+    """Correlation flops of one reference block step on an interior block
+    (reference arithmetic objective.py:170-172 + 2x :258-260):
+    H over the residual rows, H^T over the block, and two majorant products
+    (H of the block-embedded vector, H^T back)."""
+    from paper_2002_02328_b200 import blur
+    from paper_2002_02328_b200.volume import Dims3
+    d = Dims3(*cfg.dims)
+    k = blur.KernelDims(*cfg.kdims)
+    rz = (cfg.kdims[2] - 1) // 2
+    lo = (d.nz // 2 // cfg.block_height) * cfg.block_height
+    hi = min(lo + cfg.block_height - 1, d.nz - 1)
+    emb = blur.flops_H_embedded(d, k, lo, hi)
+    return (blur.flops_H(d, k, max(0, lo - rz), min(d.nz - 1, hi + rz)) + blur.flops_H(d, k, lo, hi)
+            + 2 * 2 * emb)
+
+
+def _reference_extrapolated(args, cfg, world, O, threads):
+    """Reference arm where one block step takes minutes per core (C5): the
+    reference core's correlation rate is measured on this host -- `threads`
+    concurrent calls of 2 output planes with the config's full kernel stack --
+    and one block-iteration is costed at _ref_block_flops.  The numpy
+    regulariser work is left out, so the value is an upper bound of the
+    reference's block-it/s."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2002_02328_b200 import blur
+    from paper_2002_02328_b200.volume import Dims3
+    d = Dims3(*cfg.dims)
+    psf = blur.depth_variant_stack(d, cfg.kdims, cfg.sigma_xy, cfg.sigma_z)
+    kz = cfg.kdims[2]
+    rz = (kz - 1) // 2
+    zo = d.nz // 2
+    rng = np.random.Generator(np.random.Philox(0))
+    frag = rng.uniform(0, 1, (kz + 1, d.ny, d.nx))
+    name = "ref" if O.ref_core_available() else "c"
+    O.core(name, threads=1)
+    core = O.core()
+    pool = ThreadPoolExecutor(max_workers=threads)
+
+    def one(_):
+        return core.correlate(frag, psf.kernels, zo - rz, zo, zo + 1)
+
+    list(pool.map(one, range(threads)))  # warm-up
+    times = []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        list(pool.map(one, range(threads)))
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    rate = threads * blur.flops_H(d, blur.KernelDims(*cfg.kdims), zo, zo + 1) / t  # flop/s, all threads
+    fblk = _ref_block_flops(cfg)
+    value = rate / fblk
+    core_desc = ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if name == "ref"
+                 else "oracle/bd3mg_oracle.c (bitwise the reference core)")
+    sample = (f"extrapolated: {threads} concurrent 2-plane H calls of config {cfg.name} "
+              f"({cfg.kdims[0]}x{cfg.kdims[1]}x{cfg.kdims[2]} taps) on the core ({core_desc}) ran at "
+              f"{rate / 1e9:.2f} GFLOP/s; one block-iteration costs {fblk / 1e9:.0f} GFLOP of correlations "
+              f"(reference arithmetic); numpy regulariser work excluded (upper bound)")
+    kind = "reference" if name == "ref" else "port"
+    line = {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * len(O.blocks_of(d.nz, cfg.block_height))
+            / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(cfg, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
