@@ -46,7 +46,7 @@ def _worker(rank, world, port, sweeps, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import oracle as O
-        from paper_2002_02328_b200.distributed import OracleShardedJacobi
+        from _oracle_shards import OracleShardedJacobi
         O.core("c", threads=1)
         crit, x0, h = _problem(O)
         eng = OracleShardedJacobi(O, crit, x0, h)
