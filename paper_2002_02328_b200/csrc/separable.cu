@@ -17,12 +17,11 @@
 // relative in fp64); the factors are detected at upload (separable.py) and
 // the dense graded kernel stays the default everywhere.
 //
-// Two streaming passes through one temporary volume (stream-ordered
-// allocation):
-//   sep_z_kernel   depth FIR, one thread per 16-byte pixel vector, the kz
-//                  source planes of consecutive outputs hit L1;
-//   sep_xy_kernel  per-plane separable 2-D filter, 64 x 32 tile + halo in
-//                  shared memory, x pass then y pass.
+// Two streaming passes through one temporary volume (grow-only scratch):
+//   sep_zw_kernel   depth FIR, a register window of source planes per 8- or
+//                   16-byte pixel vector and CH consecutive outputs;
+//   sep_xy(2)_kernel per-plane separable 2-D filter, tile + halo in shared
+//                   memory, x pass then y pass (register-blocked for fp32).
 // Forward = z then xy; adjoint = flipped xy then z.  HBM traffic per launch:
 // four volume passes (read src, write tmp, read tmp, write out).
 #include <cuda.h>
@@ -57,6 +56,24 @@ struct Vec16<double> {
 template <>
 struct Vec16<float> {
   using type = float4;
+};
+template <typename T, int VB>
+struct VecB;
+template <>
+struct VecB<double, 16> {
+  using type = double2;
+};
+template <>
+struct VecB<double, 8> {
+  using type = double;
+};
+template <>
+struct VecB<float, 16> {
+  using type = float4;
+};
+template <>
+struct VecB<float, 8> {
+  using type = float2;
 };
 
 // Depth FIR.  Forward: dst[zo] = sum_a u[zo][a] src[zo+a-rz] over the source
@@ -128,13 +145,14 @@ __global__ void __launch_bounds__(kZNT) sep_z_kernel(const __grid_constant__ Sep
 // and the CHxKZ coefficients of the chunk are staged in shared memory.
 // (Measured against a depth-marching ring over whole chunks: the window is
 // faster -- its loads are independent, the ring's are one per step.)
-template <typename T, bool ADJ, int KZ, int CH>
+template <typename T, bool ADJ, int KZ, int CH, int VB, bool ZFAST>
 __global__ void __launch_bounds__(kZNT) sep_zw_kernel(const __grid_constant__ SepZArgs p) {
-  using V = typename Vec16<T>::type;
-  constexpr int VEC = 16 / (int)sizeof(T);
+  using V = typename VecB<T, VB>::type;
+  constexpr int VEC = VB / (int)sizeof(T);
+  const int zblk = ZFAST ? blockIdx.x : blockIdx.y, pblk = ZFAST ? blockIdx.y : blockIdx.x;
   constexpr int RZ = (KZ - 1) / 2, W = CH + KZ - 1;
   __shared__ T cs[W * KZ];  // FWD: [output i][a]; ADJ: [source row j][a]
-  const int z_a = p.d_lo + blockIdx.y * CH;
+  const int z_a = p.d_lo + zblk * CH;
   const int s_lo = ADJ ? max(p.s_z0, 0) : p.s_z0;
   const int s_hi = ADJ ? min(p.s_z0 + p.s_n - 1, p.nzk - 1) : p.s_z0 + p.s_n - 1;
   const T* u = static_cast<const T*>(p.u);
@@ -151,7 +169,7 @@ __global__ void __launch_bounds__(kZNT) sep_zw_kernel(const __grid_constant__ Se
     cs[i] = c;
   }
   __syncthreads();
-  const long long q = ((long long)blockIdx.x * kZNT + threadIdx.x) * VEC;
+  const long long q = ((long long)pblk * kZNT + threadIdx.x) * VEC;
   if (q >= p.plane) return;
   const T* src = static_cast<const T*>(p.src);
   V win[W];  // window row j <-> source plane z_a - RZ + j
@@ -190,7 +208,7 @@ struct SepXYArgs {
   const void* v;
   const void* w;
   long long plane;
-  int nx, ny, s_z0, d_z0, r_lo;
+  int nx, ny, s_z0, d_z0, r_lo, r_n;
 };
 
 template <typename T, int K, bool FLIP>
@@ -250,6 +268,151 @@ __global__ void __launch_bounds__(kXNT) sep_xy_kernel(const __grid_constant__ Se
   }
 }
 
+// Register-blocked variant of sep_xy_kernel (same sums in the same order, so
+// bitwise equal): a thread produces 4 consecutive x outputs of the x pass
+// from 16-byte shared-memory loads, and a 4 (x) by RY (y) block of the y pass
+// from RY + K - 1 16-byte row loads, so shared-memory traffic per voxel drops
+// ~3x (the scalar kernel is shared-memory-bound, not HBM-bound).  Output rows
+// are stored as 16-byte vectors where the row allows.  PZ > 1: the CTA walks
+// PZ planes of its tile and the next plane's tile loads are in flight in
+// registers while the current plane is filtered (rows nx % VEC == 0 only).
+template <typename T, int K, bool FLIP, int TX, int TY, int RY, int NT, int PZ>
+__global__ void __launch_bounds__(NT, PZ > 1 ? 3 : 1) sep_xy2_kernel(const __grid_constant__ SepXYArgs p) {
+  using V = typename Vec16<T>::type;
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int G = 4;  // x outputs per thread
+  constexpr int R = (K - 1) / 2;
+  constexpr int RXA = (R + G - 1) / G * G, OFF = RXA - R;
+  constexpr int TW = TX + 2 * RXA, TH = TY + 2 * R;
+  constexpr int NC = (OFF + K - 1 + G + G - 1) / G;  // 4-element chunks one x-pass item reads
+  constexpr int GX = TX / G;
+  constexpr int CPR = TW / VEC, NLD = (TH * CPR + NT - 1) / NT;
+  static_assert(TX % G == 0 && TY % RY == 0 && (TY / RY) * GX == NT, "one y-pass item per thread");
+  __shared__ __align__(16) T ts[TH][TW];
+  __shared__ __align__(16) T rs[TH][TX];
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int za = p.r_lo + blockIdx.z * PZ, zb = min(za + PZ, p.r_lo + p.r_n);
+  const bool vec_rows = p.nx % VEC == 0;
+  V pre[NLD];
+  auto load_tile = [&](int z) {  // vector rows: into registers
+    const T* src = static_cast<const T*>(p.src) + (long long)(z - p.s_z0) * p.plane;
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int i = threadIdx.x + k * NT;
+      const int r = i / CPR, c = (i - r * CPR) * VEC;
+      const int y = y0 - R + r, x = x0 - RXA + c;
+      pre[k] = (i < TH * CPR && y >= 0 && y < p.ny && x >= 0 && x < p.nx)
+                   ? __ldg(reinterpret_cast<const V*>(src + (long long)y * p.nx + x))
+                   : V{};
+    }
+  };
+  auto stage_tile = [&]() {
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int i = threadIdx.x + k * NT;
+      const int r = i / CPR, c = (i - r * CPR) * VEC;
+      if (i < TH * CPR) *reinterpret_cast<V*>(&ts[r][c]) = pre[k];
+    }
+  };
+  if (vec_rows) {
+    load_tile(za);
+    stage_tile();
+  }
+  for (int z = za; z < zb; ++z) {
+    if (!vec_rows) {
+      const T* src = static_cast<const T*>(p.src) + (long long)(z - p.s_z0) * p.plane;
+      for (int i = threadIdx.x; i < TH * TW; i += NT) {
+        const int r = i / TW, c = i - r * TW;
+        const int y = y0 - R + r, x = x0 - RXA + c;
+        ts[r][c] = (y >= 0 && y < p.ny && x >= 0 && x < p.nx) ? src[(long long)y * p.nx + x] : T(0);
+      }
+    }
+    T wk[K], vk[K];
+    const T* wz = static_cast<const T*>(p.w) + (long long)z * K;
+    const T* vz = static_cast<const T*>(p.v) + (long long)z * K;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      wk[c] = __ldg(wz + (FLIP ? K - 1 - c : c));
+      vk[c] = __ldg(vz + (FLIP ? K - 1 - c : c));
+    }
+    __syncthreads();  // ts holds plane z; rs free
+    const bool more = vec_rows && z + 1 < zb;
+    if (more) load_tile(z + 1);
+    for (int i = threadIdx.x; i < TH * GX; i += NT) {
+      const int r = i / GX, c = (i - r * GX) * G;
+      T seg[NC * G];
+#pragma unroll
+      for (int j = 0; j < NC * G; j += VEC) *reinterpret_cast<V*>(&seg[j]) = *reinterpret_cast<const V*>(&ts[r][c + j]);
+      T o[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        T s = T(0);
+#pragma unroll
+        for (int cc = 0; cc < K; ++cc) s = fma_rn(wk[cc], seg[g + cc + OFF], s);
+        o[g] = s;
+      }
+#pragma unroll
+      for (int j = 0; j < G; j += VEC) *reinterpret_cast<V*>(&rs[r][c + j]) = *reinterpret_cast<const V*>(&o[j]);
+    }
+    __syncthreads();  // rs complete; ts free
+    const int gx = threadIdx.x % GX, gy = threadIdx.x / GX;
+    const int c = gx * G, r0 = gy * RY;
+    T acc[RY][G];
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[i][g] = T(0);
+#pragma unroll
+    for (int j = 0; j < RY + K - 1; ++j) {
+      T row[G];
+#pragma unroll
+      for (int g = 0; g < G; g += VEC) *reinterpret_cast<V*>(&row[g]) = *reinterpret_cast<const V*>(&rs[r0 + j][c + g]);
+#pragma unroll
+      for (int i = 0; i < RY; ++i) {
+        const int b = j - i;  // output row r0+i, tap b, in ascending b per output
+        if (b >= 0 && b < K) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) acc[i][g] = fma_rn(vk[b], row[g], acc[i][g]);
+        }
+      }
+    }
+    T* dst = static_cast<T*>(p.dst) + (long long)(z - p.d_z0) * p.plane;
+    const int x = x0 + c;
+#pragma unroll
+    for (int i = 0; i < RY; ++i) {
+      const int y = y0 + r0 + i;
+      if (y >= p.ny) break;
+      T* dp = dst + (long long)y * p.nx + x;
+      if (vec_rows && x + G <= p.nx) {
+#pragma unroll
+        for (int g = 0; g < G; g += VEC) *reinterpret_cast<V*>(dp + g) = *reinterpret_cast<const V*>(&acc[i][g]);
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (x + g < p.nx) dp[g] = acc[i][g];
+      }
+    }
+    if (more) stage_tile();  // after this plane's x pass: ts is free
+    __syncthreads();          // rs reads done before the next x pass
+  }
+}
+
+template <typename T>
+struct Xy2Cfg;
+template <>
+struct Xy2Cfg<float> {
+  static constexpr int TX = 64, TY = 64, RY = 4, NT = 256;
+};
+template <>
+struct Xy2Cfg<double> {
+  static constexpr int TX = 64, TY = 32, RY = 2, NT = 256;
+};
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
 int errf(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int errf(int code, const char* fmt, ...) {
   char buf[512];
@@ -263,14 +426,61 @@ int errf(int code, const char* fmt, ...) {
 template <typename T, int K>
 int launch_xy(SepXYArgs& a, int nrows, bool flip, cudaStream_t s) {
   if (nrows <= 0) return BD3MG_OK;
-  dim3 grid((a.nx + kXx - 1) / kXx, (a.ny + kXy - 1) / kXy, nrows);
-  if (flip)
-    sep_xy_kernel<T, K, true><<<grid, kXNT, 0, s>>>(a);
-  else
-    sep_xy_kernel<T, K, false><<<grid, kXNT, 0, s>>>(a);
+  // register-blocked 2-D filter for fp32 (C3 / C5: -14% / -17% per H); the
+  // scalar one stays the fp64 default (C2: within +-6% either way)
+  const int xyv = env_int("BD3MG_SEP_XY", sizeof(T) == 4 ? 2 : 1);
+  a.r_n = nrows;
+  if (xyv == 2 || xyv == 3) {
+    using C = Xy2Cfg<T>;
+    constexpr int PZ = 4;
+    const int pz = xyv == 3 ? PZ : 1;
+    dim3 grid((a.nx + C::TX - 1) / C::TX, (a.ny + C::TY - 1) / C::TY, (nrows + pz - 1) / pz);
+    if (xyv == 3) {
+      if (flip)
+        sep_xy2_kernel<T, K, true, C::TX, C::TY, C::RY, C::NT, PZ><<<grid, C::NT, 0, s>>>(a);
+      else
+        sep_xy2_kernel<T, K, false, C::TX, C::TY, C::RY, C::NT, PZ><<<grid, C::NT, 0, s>>>(a);
+    } else if (flip) {
+      sep_xy2_kernel<T, K, true, C::TX, C::TY, C::RY, C::NT, 1><<<grid, C::NT, 0, s>>>(a);
+    } else {
+      sep_xy2_kernel<T, K, false, C::TX, C::TY, C::RY, C::NT, 1><<<grid, C::NT, 0, s>>>(a);
+    }
+  } else {
+    dim3 grid((a.nx + kXx - 1) / kXx, (a.ny + kXy - 1) / kXy, nrows);
+    if (flip)
+      sep_xy_kernel<T, K, true><<<grid, kXNT, 0, s>>>(a);
+    else
+      sep_xy_kernel<T, K, false><<<grid, kXNT, 0, s>>>(a);
+  }
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+}
+
+template <typename T, bool ADJ, int KZ, int CH, int VB, bool ZFAST>
+int launch_zw(SepZArgs& a, int n, cudaStream_t s) {
+  constexpr int VEC = VB / (int)sizeof(T);
+  const unsigned pb = (unsigned)(((a.plane + VEC - 1) / VEC + kZNT - 1) / kZNT), zb = (unsigned)((n + CH - 1) / CH);
+  const dim3 g = ZFAST ? dim3(zb, pb) : dim3(pb, zb);
+  sep_zw_kernel<T, ADJ, KZ, CH, VB, ZFAST><<<g, kZNT, 0, s>>>(a);
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+}
+
+// Register-window variant: BD3MG_SEP_Z = CH * 1000 + VB * 10 + ZFAST (probe
+// knob, scripts/sep_probe.py; results are bitwise equal across variants)
+template <typename T, bool ADJ, int KZ>
+int launch_zw_var(SepZArgs& a, int n, int var, cudaStream_t s) {
+  switch (var) {
+    case 8160: return launch_zw<T, ADJ, KZ, 8, 16, false>(a, n, s);
+    case 8161: return launch_zw<T, ADJ, KZ, 8, 16, true>(a, n, s);
+    case 8080: return launch_zw<T, ADJ, KZ, 8, 8, false>(a, n, s);
+    case 8081: return launch_zw<T, ADJ, KZ, 8, 8, true>(a, n, s);
+    case 16081: return launch_zw<T, ADJ, KZ, 16, 8, true>(a, n, s);
+    case 16161: return launch_zw<T, ADJ, KZ, 16, 16, true>(a, n, s);
+    default: return -1;
+  }
 }
 
 template <typename T>
@@ -280,19 +490,17 @@ int launch_z(SepZArgs& a, bool adj, cudaStream_t s) {
   constexpr int VEC = 16 / (int)sizeof(T);
   const long long vecs = (a.plane + VEC - 1) / VEC;
   dim3 grid((unsigned)((vecs + kZNT - 1) / kZNT), (n + kZChunk - 1) / kZChunk);
-  if (a.plane % VEC == 0) {  // register-window kernel: 8 outputs per thread
-    constexpr int CH = 8;
-    dim3 gw((unsigned)((vecs + kZNT - 1) / kZNT), (n + CH - 1) / CH);
+  if (a.plane % VEC == 0) {  // register-window kernel
+    // measured defaults (profiles/r1_sep_probe.md): fp32 16 outputs per
+    // thread, 16-byte vectors, depth chunks fastest in the grid so the window
+    // overlap of neighbouring chunks is served by L2; fp64 8 outputs
+    const int var = env_int("BD3MG_SEP_Z", sizeof(T) == 4 ? 16161 : 8160);
     switch (a.kz) {
-#define BD3MG_SEPZW(KZ)                                                                       \
-  case KZ: {                                                                                  \
-    if (adj)                                                                                  \
-      sep_zw_kernel<T, true, KZ, CH><<<gw, kZNT, 0, s>>>(a);                                  \
-    else                                                                                      \
-      sep_zw_kernel<T, false, KZ, CH><<<gw, kZNT, 0, s>>>(a);                                 \
-    count_launches(1);                                                                        \
-    cudaError_t e = cudaGetLastError();                                                       \
-    return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e)); \
+#define BD3MG_SEPZW(KZ)                                                                                           \
+  case KZ: {                                                                                                      \
+    const int rc = adj ? launch_zw_var<T, true, KZ>(a, n, var, s) : launch_zw_var<T, false, KZ>(a, n, var, s); \
+    if (rc >= 0) return rc;                                                                                       \
+    return errf(BD3MG_EINVAL, "BD3MG_SEP_Z=%d: unknown depth-FIR variant", var);                                   \
   }
       BD3MG_SEPZW(3) BD3MG_SEPZW(5) BD3MG_SEPZW(7) BD3MG_SEPZW(9) BD3MG_SEPZW(11) BD3MG_SEPZW(13)
       BD3MG_SEPZW(15) BD3MG_SEPZW(17) BD3MG_SEPZW(19) BD3MG_SEPZW(21)
