@@ -25,6 +25,9 @@ VARIANTS = [("1", "8160"), ("2", "8160"), ("2", "8161"), ("2", "8080"), ("2", "8
 def main():
     peak = json.load(open(Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"))["hbm_gbs"]
     names = sys.argv[1:] or list(SHAPES)
+    variants = VARIANTS
+    if os.environ.get("SEP_PROBE_VARIANT"):  # e.g. "2:16161" (one variant, for ncu captures)
+        variants = [tuple(os.environ["SEP_PROBE_VARIANT"].split(":"))]
     for name in names:
         (nx, ny, nz), k, kz, dt = SHAPES[name]
         dims = Dims3(nx, ny, nz)
@@ -35,7 +38,7 @@ def main():
         nbytes = separable.bytes_H(dims, x.element_size())
         for adj in (False, True):
             ref = None
-            for xy, zv in VARIANTS:
+            for xy, zv in variants:
                 os.environ["BD3MG_SEP_XY"], os.environ["BD3MG_SEP_Z"] = xy, zv
                 for _ in range(3):
                     sep.correlate_rows(x, 0, 0, nz - 1, adjoint=adj, out=out)
