@@ -20,8 +20,12 @@
 // Two streaming passes through one temporary volume (grow-only scratch):
 //   sep_zw_kernel   depth FIR, a register window of source planes per 8- or
 //                   16-byte pixel vector and CH consecutive outputs;
-//   sep_xy(2)_kernel per-plane separable 2-D filter, tile + halo in shared
-//                   memory, x pass then y pass (register-blocked for fp32).
+//   sep_xyt_kernel  per-plane separable 2-D filter (fp32): a 64 x 64 tile +
+//                   halo per TMA box, double-buffered over 4 planes per CTA,
+//                   register-blocked x pass then y pass from 16-byte
+//                   shared-memory loads (sep_xy2_kernel: the same without
+//                   TMA, for rows that are not 16-byte multiples;
+//                   sep_xy_kernel: scalar, the fp64 default).
 // Forward = z then xy; adjoint = flipped xy then z.  HBM traffic per launch:
 // four volume passes (read src, write tmp, read tmp, write out).
 #include <cuda.h>
@@ -38,6 +42,7 @@
 
 #include "../../include/bd3mg_b200.h"
 #include "common.cuh"
+#include "conv_dispatch.cuh"
 #include "errors.h"
 
 namespace bd3mg {
@@ -397,6 +402,123 @@ __global__ void __launch_bounds__(NT, PZ > 1 ? 3 : 1) sep_xy2_kernel(const __gri
   }
 }
 
+// TMA-fed fp32 2-D filter: the CTA walks PZ planes of one 64 x 64 output
+// tile; each plane's (64 + 2 RXA) x (64 + 2R) source tile is a single TMA box
+// (halo zero-filled by the copy engine), double-buffered so the next plane
+// lands while the current one is filtered.  Same x / y passes as
+// sep_xy2_kernel (bitwise equal).
+struct SepXYTArgs {
+  CUtensorMap tm;  // src rows: (nx, ny, planes), box (TW, TH, 1)
+  SepXYArgs a;
+};
+
+template <int K>
+struct XytGeo {
+  static constexpr int TX = 64, TY = 64, RY = 4, NT = 256, G = 4;
+  static constexpr int R = (K - 1) / 2, RXA = (R + G - 1) / G * G, OFF = RXA - R;
+  static constexpr int TW = TX + 2 * RXA, TH = TY + 2 * R;
+  static constexpr int BS = (TH * TW + 31) / 32 * 32;  // buffer stride (floats): TMA needs 128-byte aligned boxes
+  static constexpr size_t smem() { return (2 * (size_t)BS + (size_t)TH * TX) * sizeof(float) + 16 + 128; }
+};
+
+template <int K, bool FLIP, int PZ>
+__global__ void __launch_bounds__(256) sep_xyt_kernel(const __grid_constant__ SepXYTArgs P) {
+  using Geo = XytGeo<K>;
+  constexpr int TX = Geo::TX, TY = Geo::TY, RY = Geo::RY, NT = Geo::NT, G = Geo::G;
+  constexpr int R = Geo::R, RXA = Geo::RXA, OFF = Geo::OFF, TW = Geo::TW, TH = Geo::TH;
+  constexpr int NC = (OFF + K - 1 + G + G - 1) / G;
+  constexpr int GX = TX / G;
+  static_assert((TY / RY) * GX == NT, "one y-pass item per thread");
+  const SepXYArgs& p = P.a;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* base = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float (*ts0)[TW] = reinterpret_cast<float (*)[TW]>(base);
+  float (*ts1)[TW] = reinterpret_cast<float (*)[TW]>(base + Geo::BS);
+  float (*rs)[TX] = reinterpret_cast<float (*)[TX]>(base + 2 * Geo::BS);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * Geo::BS + TH * TX);
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int za = p.r_lo + blockIdx.z * PZ, zb = min(za + PZ, p.r_lo + p.r_n);
+  constexpr uint32_t kBytes = TH * TW * sizeof(float);
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&P.tm);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar[0], kBytes);
+    tma_load_3d(&ts0[0][0], &P.tm, x0 - RXA, y0 - R, za - p.s_z0, &bar[0]);
+  }
+  __syncthreads();
+  for (int z = za, k = 0; z < zb; ++z, ++k) {
+    const int buf = k & 1;
+    if (threadIdx.x == 0 && z + 1 < zb) {  // buf^1 was last read by plane z-1's x pass (all past its barrier)
+      mbar_expect_tx(&bar[buf ^ 1], kBytes);
+      tma_load_3d(buf ? &ts0[0][0] : &ts1[0][0], &P.tm, x0 - RXA, y0 - R, z + 1 - p.s_z0, &bar[buf ^ 1]);
+    }
+    float wk[K], vk[K];
+    const float* wz = static_cast<const float*>(p.w) + (long long)z * K;
+    const float* vz = static_cast<const float*>(p.v) + (long long)z * K;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      wk[c] = __ldg(wz + (FLIP ? K - 1 - c : c));
+      vk[c] = __ldg(vz + (FLIP ? K - 1 - c : c));
+    }
+    mbar_wait(&bar[buf], (k >> 1) & 1);
+    float (*ts)[TW] = buf ? ts1 : ts0;
+    for (int i = threadIdx.x; i < TH * GX; i += NT) {
+      const int r = i / GX, c = (i - r * GX) * G;
+      float seg[NC * G];
+#pragma unroll
+      for (int j = 0; j < NC * G; j += 4) *reinterpret_cast<float4*>(&seg[j]) = *reinterpret_cast<const float4*>(&ts[r][c + j]);
+      float o[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float acc = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < K; ++cc) acc = fma_rn(wk[cc], seg[g + cc + OFF], acc);
+        o[g] = acc;
+      }
+      *reinterpret_cast<float4*>(&rs[r][c]) = *reinterpret_cast<const float4*>(o);
+    }
+    __syncthreads();  // rs complete; ts[buf] free
+    const int gx = threadIdx.x % GX, gy = threadIdx.x / GX;
+    const int c = gx * G, r0 = gy * RY;
+    float acc[RY][G];
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[i][g] = 0.f;
+#pragma unroll
+    for (int j = 0; j < RY + K - 1; ++j) {
+      const float4 rv = *reinterpret_cast<const float4*>(&rs[r0 + j][c]);
+      const float row[G] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+      for (int i = 0; i < RY; ++i) {
+        const int b = j - i;
+        if (b >= 0 && b < K) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) acc[i][g] = fma_rn(vk[b], row[g], acc[i][g]);
+        }
+      }
+    }
+    float* dst = static_cast<float*>(p.dst) + (long long)(z - p.d_z0) * p.plane;
+    const int x = x0 + c;
+#pragma unroll
+    for (int i = 0; i < RY; ++i) {
+      const int y = y0 + r0 + i;
+      if (y >= p.ny) break;
+      float* dp = dst + (long long)y * p.nx + x;
+      if (x + G <= p.nx) {
+        *reinterpret_cast<float4*>(dp) = *reinterpret_cast<const float4*>(&acc[i][0]);
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (x + g < p.nx) dp[g] = acc[i][g];
+      }
+    }
+    __syncthreads();  // rs reads done before the next x pass
+  }
+}
+
 template <typename T>
 struct Xy2Cfg;
 template <>
@@ -426,11 +548,30 @@ int errf(int code, const char* fmt, ...) {
 template <typename T, int K>
 int launch_xy(SepXYArgs& a, int nrows, bool flip, cudaStream_t s) {
   if (nrows <= 0) return BD3MG_OK;
-  // register-blocked 2-D filter for fp32 (C3 / C5: -14% / -17% per H); the
-  // scalar one stays the fp64 default (C2: within +-6% either way)
-  const int xyv = env_int("BD3MG_SEP_XY", sizeof(T) == 4 ? 2 : 1);
+  // fp32: the TMA-fed, double-buffered register-blocked filter (5; rows
+  // that are not 16-byte multiples take the register-blocked one, 2); fp64:
+  // the scalar one (1; at C2 every variant is within +-8%)
+  const int xyv = env_int("BD3MG_SEP_XY", sizeof(T) == 4 ? 5 : 1);
   a.r_n = nrows;
-  if (xyv == 2 || xyv == 3) {
+  if constexpr (sizeof(T) == 4) {
+    if (xyv == 5 && a.nx % 4 == 0 && (reinterpret_cast<uintptr_t>(a.src) & 15) == 0) {
+      using Geo = XytGeo<K>;
+      constexpr int PZ = 4;  // measured: 2 / 8 / 16 planes per CTA are 0-8% slower (profiles/r1_sep_probe.md)
+      SepXYTArgs ta;
+      ta.a = a;
+      if (!encode_tmap(&ta.tm, a.src, false, a.nx, a.ny, a.r_lo - a.s_z0 + nrows, Geo::TW, Geo::TH))
+        return errf(BD3MG_EINVAL, "separable: TMA descriptor rejected");
+      auto kern = flip ? sep_xyt_kernel<K, true, PZ> : sep_xyt_kernel<K, false, PZ>;
+      cudaError_t e = ensure_smem_attr(kern, Geo::smem());
+      if (e != cudaSuccess) return errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+      dim3 grid((a.nx + Geo::TX - 1) / Geo::TX, (a.ny + Geo::TY - 1) / Geo::TY, (nrows + PZ - 1) / PZ);
+      kern<<<grid, Geo::NT, Geo::smem(), s>>>(ta);
+      count_launches(1);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? BD3MG_OK : errf(BD3MG_ECUDA, "CUDA: %s", cudaGetErrorString(e));
+    }
+  }
+  if (xyv == 2 || xyv == 3 || xyv == 5) {
     using C = Xy2Cfg<T>;
     constexpr int PZ = 4;
     const int pz = xyv == 3 ? PZ : 1;

@@ -19,7 +19,7 @@ from paper_2002_02328_b200.volume import Dims3  # noqa: E402
 SHAPES = {"C2": ((256, 256, 64), 5, 11, torch.float64), "C3": ((512, 512, 128), 7, 15, torch.float32),
           "C5": ((1024, 1024, 512), 9, 21, torch.float32)}
 VARIANTS = [("1", "8160"), ("2", "8160"), ("2", "8161"), ("2", "8080"), ("2", "8081"), ("2", "16081"),
-            ("2", "16161"), ("3", "16161"), ("3", "8160")]
+            ("2", "16161"), ("3", "16161"), ("3", "8160"), ("5", "16161")]
 
 
 def main():

@@ -77,7 +77,7 @@ def test_variants_bitwise_equal(dt, monkeypatch):
     for adj in (False, True):
         ref = None
         for xy, zv in (("1", "8160"), ("2", "8160"), ("2", "8161"), ("2", "8080"), ("2", "8081"),
-                       ("2", "16081"), ("2", "16161"), ("3", "16161"), ("3", "8160")):
+                       ("2", "16081"), ("2", "16161"), ("3", "16161"), ("3", "8160"), ("5", "16161")):
             monkeypatch.setenv("BD3MG_SEP_XY", xy)
             monkeypatch.setenv("BD3MG_SEP_Z", zv)
             got = sep.correlate_rows(x[5:40], 5, 9, 33, adjoint=adj)
