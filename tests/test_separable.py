@@ -57,6 +57,9 @@ def test_rows_of_a_fragment_and_adjoint_identity(oracle_mod):
             want = fn(psf.kernels, frag, z0, lo, hi)
             got = sep.correlate_rows(torch.from_numpy(frag).cuda(), z0, lo, hi, adjoint=adj).cpu().numpy()
             assert np.linalg.norm(got - want) <= 1e-12 * max(np.linalg.norm(want), 1e-300)
+            # fp32 (nx = 40: the TMA-fed 2-D filter, boxes offset by the fragment origin)
+            got32 = sep.correlate_rows(torch.from_numpy(frag).cuda().float(), z0, lo, hi, adjoint=adj)
+            assert np.linalg.norm(got32.double().cpu().numpy() - want) <= 1e-5 * max(np.linalg.norm(want), 1e-300)
     y = rng.uniform(0, 1, dims.shape)
     hx = sep.apply_H(x)
     hty = sep.apply_Ht(y)
