@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 halo transport: update-kernel NVLink stores into the neighbours' inboxes "
                          "(block-Jacobi) / halo rings (async) -- the default -- or NCCL messages")
+    ap.add_argument("--ref-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--mode", default="jacobi", choices=["jacobi", "cyclic", "async"],
                     help="schedule: block-Jacobi sweeps (default), deterministic cyclic (N=1), or the "
                          "asynchronous bounded-delay mode (stale peer halos, max delay 2)")
@@ -140,65 +141,198 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-def reference_arm(args, cfg_name):
-    """The reference CPU implementation on the host cores: oracle port of
-    objective/directions/runtime driving the reference's compiled core
-    (oracle/_ref) -- or the bitwise-identical C restatement when absent --
-    with the reference's multi-core mode (bp3mg barrier, ThreadPool of
-    min(cores, B) workers, GIL released in the core)."""
+# Reference arm.  Import-clean by construction: nothing below imports torch,
+# the product's operator modules or its native library -- only the torch-free
+# workload description (configs, flops, volume generators), the unmodified
+# reference package installed into baseline/_ref, and (when that is absent)
+# the oracle port.  _assert_import_clean() checks it before the line prints.
+def _reference_pkg():
+    """The unmodified reference (pip --target baseline/_ref)
+    with its compiled core, or None when it was not installed."""
+    p = ROOT / "baseline" / "_ref"
+    if not (p / "bd3mg" / "__init__.py").exists():
+        return None
+    sys.path.insert(0, str(p))
+    import bd3mg
+    import bd3mg.blur
+    import bd3mg.directions
+    import bd3mg.kernels
+    import bd3mg.objective
+    import bd3mg.runtime
+    import bd3mg.volume  # noqa: F401
+    return bd3mg
+
+
+def _assert_import_clean():
+    bad = [m for m in ("torch", "paper_2002_02328_b200._native", "paper_2002_02328_b200.blur",
+                       "paper_2002_02328_b200.objective") if m in sys.modules]
+    if bad:
+        raise RuntimeError(f"reference arm is not import-clean: {bad}")
+
+
+def reference_arm(args):
+    """The reference CPU implementation on the host cores, rank 0 only.
+
+    * default: the UNMODIFIED reference (baseline/_ref) through its own public
+      API and stock code path -- ``bd3mg.runtime.run`` with method "bp3mg",
+      engine "live" (its multi-core mode: a ThreadPool of min(cores, B)
+      workers, GIL released in the compiled core), the per-sweep recorder
+      included -- on the same config, with the faster of its two backends on
+      this host (compiled core vs ``BD3MG_NO_EXT=1`` scipy, probed first);
+    * configs whose reference block step costs minutes per core (C5):
+      the reference core's correlation rate, extrapolated (labelled);
+    * without baseline/_ref: the oracle port (oracle/oracle.py driving the
+      reference's compiled core from oracle/_ref)."""
+    from paper_2002_02328_b200 import flops
+
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    cfg = bench_config(args, world)
+    cores = os.cpu_count() or 1
+    B = -(-cfg.dims.nz // cfg.block_height)
+    threads = max(1, min(cores, B))
+    if args.ref_probe:
+        print(json.dumps({"probe_s": _reference_probe(cfg, threads)}), flush=True)
+        return
+    if flops.ref_block_flops(cfg.dims, cfg.kdims, cfg.block_height) > 150e9:
+        line = _reference_extrapolated(args, cfg, world, threads)
+    elif (ROOT / "baseline" / "_ref" / "bd3mg").exists():
+        line = _reference_stock(args, cfg, world, threads)
+    else:
+        line = _reference_port(args, cfg, world, threads)
+    _assert_import_clean()
+    print(json.dumps(line), flush=True)
+
+
+def _ref_line(args, cfg, world, value, ms, threads, kind, sample, steps=None, warmup=None):
+    return {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps if steps is None else steps, "warmup": args.warmup if warmup is None else warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _ref_problem(R, cfg):
+    """The config's seeded inputs built with the reference's own PsfStack,
+    gaussian_kernel, apply_H, noise and init generators (the ellipsoid
+    phantom is BASELINE's, from the torch-free paper_2002_02328_b200.volume)."""
+    from paper_2002_02328_b200 import configs
+    dims = R.volume.Dims3(*cfg.dims)
+    kd = R.blur.KernelDims(*cfg.kdims)
+    params = configs.depth_variant_params(dims.nz, cfg.sigma_xy, cfg.sigma_z)
+    stack = np.stack([R.blur.gaussian_kernel(kd, *p) for p in params])
+    psf = R.blur.PsfStack(dims, kd, stack, params)
+    truth = configs.truth_of(cfg)
+    y = R.volume.add_gaussian_noise(R.blur.apply_H(psf, truth), cfg.noise, cfg.seed + 2)
+    x0 = R.volume.init_uniform(dims, float(np.max(y)), cfg.seed + 3)
+    rp = R.objective.RegParams(lam=cfg.lam, eta=cfg.eta, kappa=cfg.kappa, delta=cfg.delta, x_min=0.0, x_max=1.0)
+    return R.objective.Objective(psf, y, rp), x0
+
+
+def _reference_probe(cfg, threads):
+    """One batch of `threads` concurrent reference mg_direction calls on
+    random data with whichever backend this process's environment selects
+    (seconds).  Run twice by _reference_stock, once per backend."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2002_02328_b200 import configs
+    R = _reference_pkg()
+    dims = R.volume.Dims3(*cfg.dims)
+    kd = R.blur.KernelDims(*cfg.kdims)
+    params = configs.depth_variant_params(dims.nz, cfg.sigma_xy, cfg.sigma_z)
+    psf = R.blur.PsfStack(dims, kd, np.stack([R.blur.gaussian_kernel(kd, *p) for p in params]), params)
+    rng = np.random.Generator(np.random.Philox(0))
+    y = rng.uniform(0, 1, dims.shape)
+    x = rng.uniform(0, 1, dims.shape)
+    obj = R.objective.Objective(psf, y, R.objective.RegParams(lam=cfg.lam, eta=cfg.eta, kappa=cfg.kappa,
+                                                              delta=cfg.delta))
+    blocks = R.scheduler.partition_blocks(dims.nz, cfg.block_height)[:threads]
+
+    def one(b):
+        s = R.blur.slab_support(psf, b)
+        return R.directions.mg_direction(obj, x[s.z_lo:s.z_hi + 1], s.z_lo, b, np.zeros(b.count(dims)))
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        list(pool.map(one, blocks))  # warm-up (imports, page-in)
+        t0 = time.perf_counter()
+        list(pool.map(one, blocks))
+        return time.perf_counter() - t0
+
+
+def _reference_stock(args, cfg, world, threads):
+    # backend probe: the reference selects its backend at import from
+    # BD3MG_NO_EXT (kernels.py:14-28), so each backend is probed in its own
+    # process, and this process imports the faster one
+    timing = {}
+    for name, env in (("compiled", {}), ("numpy", {"BD3MG_NO_EXT": "1"})):
+        cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--ref-probe", "--config", args.config,
+               "--gpus", str(args.gpus)]
+        e = dict(os.environ, WORLD_SIZE=str(world), RANK="0", LOCAL_RANK="0", **env)
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=e)
+            timing[name] = json.loads(out.stdout.strip().splitlines()[-1])["probe_s"]
+        except Exception:  # a backend that fails to probe is not chosen
+            timing[name] = float("inf")
+    best = min(timing, key=timing.get)
+    if best == "numpy":
+        os.environ["BD3MG_NO_EXT"] = "1"
+    R = _reference_pkg()
+    obj, x0 = _ref_problem(R, cfg)
+    B = -(-cfg.dims.nz // cfg.block_height)
+    W, K = max(1, args.warmup), args.steps
+    if world > 1:
+        # rank 0 alone times the N-rank workload: bound it (one warm-up sweep,
+        # then as many timed sweeps as fit ~150 s, at most K)
+        rc = R.runtime.RunConfig(method="bp3mg", workers=threads, block_height=cfg.block_height, tol=1e-30,
+                                 max_updates=B, engine="live")
+        t_sweep = R.runtime.run(obj, x0, rc).wall_seconds
+        W, K = 1, max(1, min(K, int(150.0 / max(t_sweep, 1e-3))))
+    rc = R.runtime.RunConfig(method="bp3mg", workers=threads, block_height=cfg.block_height, tol=1e-30,
+                             max_updates=B * (W + K), engine="live")
+    res = R.runtime.run(obj, x0, rc)
+    walls = [e.wall_seconds for e in res.log]
+    # log entry i is stamped when sweep i's increments are computed (before
+    # its recorder f); entries W-1 .. W+K-1 bracket exactly K sweeps, each
+    # with its recorder pass, as in the GPU arm's step
+    t = walls[W + K - 1] - walls[W - 1]
+    value = K * B / t
+    sample = (f"{K} timed sweeps x {B} blocks of config {cfg.name} after {W} warm-up sweeps, one call of the "
+              f"unmodified reference bd3mg.runtime.run(method='bp3mg', workers={threads}, engine='live') from "
+              f"baseline/_ref (ThreadPool workers, per-sweep eval_f recorder included), timed by its own log "
+              f"clock; backend: {R.kernels.backend_name()} (probe of {threads} concurrent mg_direction calls: "
+              + ", ".join(f"{n} {timing[n]:.2f} s" for n in timing) + ")")
+    return _ref_line(args, cfg, world, value, 1e3 * t / K, threads, "reference", sample, steps=K, warmup=W)
+
+
+def _reference_port(args, cfg, world, threads):
+    """Fallback without baseline/_ref: the oracle port of objective /
+    directions / the bp3mg barrier driving the reference's compiled core
+    (oracle/_ref) or, when that is absent too, its C restatement."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
     from paper_2002_02328_b200 import configs
+    from paper_2002_02328_b200.volume import add_gaussian_noise, init_uniform
 
-    cfg = bench_config(args, world)
     nz = cfg.dims.nz
     all_blocks = O.blocks_of(nz, cfg.block_height)
-    cores = os.cpu_count() or 1
-    threads = max(1, min(cores, len(all_blocks)))
-    if _ref_block_flops(cfg) > 150e9:  # ~minutes per block step on one core (C5): extrapolate
-        _reference_extrapolated(args, cfg, world, O, threads)
-        return
-    psf_k, y, x0 = _host_problem(cfg, O)
-    crit = O.Criterion(psf_k, y, cfg.lam, cfg.eta, cfg.kappa, cfg.delta)
-    # bounded sample per step: at most 16 blocks of the barrier cycle (all of
-    # them at N=1); every block costs the same, so block-it/s is unbiased
-    blocks = all_blocks[:16]
+    name = "ref" if O.ref_core_available() else "c"
+    O.core(name, threads=1)
+    params = configs.depth_variant_params(nz, cfg.sigma_xy, cfg.sigma_z)
+    kx, ky, kz = cfg.kdims
+    kern = np.stack([O.gaussian_psf(kx, ky, kz, *p) for p in params])
+    y = add_gaussian_noise(O.H(kern, configs.truth_of(cfg)), cfg.noise, cfg.seed + 2)
+    x0 = init_uniform(cfg.dims, float(np.max(y)), cfg.seed + 3)
+    crit = O.Criterion(kern, y, cfg.lam, cfg.eta, cfg.kappa, cfg.delta)
+    blocks = all_blocks[:16]  # bounded sample: every block costs the same, so block-it/s is unbiased
     B = len(blocks)
     pool = ThreadPoolExecutor(max_workers=threads)
-    x = x0.copy()
-    prev = np.zeros_like(x)
+    x, prev = x0.copy(), np.zeros_like(x0)
     snap = x.copy()
 
-    # the reference has two CPU backends (src/kernels.py:16-28): its compiled
-    # core and the scipy fallback; report the faster on this host (SURVEY.md
-    # 8(d)), probed on one batch of `threads` block steps each
-    def probe_batch():
-        def one(b):
-            lo, hi = b
-            s_lo, s_hi = O.support(nz, crit.kz, lo, hi)
-            return O.mg_direction(crit, x[s_lo:s_hi + 1].copy(), s_lo, lo, hi, prev[lo:hi + 1].ravel().copy())
-        t0 = time.perf_counter()
-        list(pool.map(one, blocks[:threads]))
-        return time.perf_counter() - t0
-
-    cands = ["ref" if O.ref_core_available() else "c", "scipy"]
-    timing = {}
-    for name in cands:
-        O.core(name, threads=1)
-        timing[name] = probe_batch()
-    best = min(timing, key=timing.get)
-    O.core(best, threads=1)
-    kind = "reference" if best == "ref" else "port"
-    core_desc = {"ref": "reference _core.pyx compiled from /root/reference (oracle/_ref)",
-                 "c": "oracle/bd3mg_oracle.c (bitwise the reference core)",
-                 "scipy": "the reference's scipy backend (_kernels_np.py) restated in oracle/oracle.py"}
-
     def sweep():
-        nonlocal x, snap
+        nonlocal snap
 
         def one(b):
             lo, hi = b
@@ -217,94 +351,74 @@ def reference_arm(args, cfg_name):
 
     for _ in range(args.warmup):
         sweep()
-    t = []
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        t0 = time.perf_counter()
         sweep()
-        t.append(time.perf_counter() - t0)
-    total = sum(t)
+    total = time.perf_counter() - t0
     value = args.steps * B / total
-    sample = (f"{args.steps} timed steps x {B} of {len(all_blocks)} blocks of config {cfg.name} "
-              f"after {args.warmup} warm-up; "
-              f"bp3mg barrier, {threads} worker threads; core: {core_desc[best]}; the faster reference "
-              f"backend on this host (probe, {threads} block steps: "
-              + ", ".join(f"{n} {timing[n]:.2f} s" for n in cands) + ")")
-    line = {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(cfg, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    core_desc = ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if name == "ref"
+                 else "oracle/bd3mg_oracle.c (bitwise the reference core)")
+    sample = (f"baseline/_ref absent: oracle port; {args.steps} timed steps x {B} of {len(all_blocks)} blocks of "
+              f"config {cfg.name} after {args.warmup} warm-up; bp3mg barrier, {threads} worker threads; core: "
+              f"{core_desc}")
+    return _ref_line(args, cfg, world, value, 1e3 * total / args.steps, threads,
+                     "reference" if name == "ref" else "port", sample)
 
 
-def _ref_block_flops(cfg) -> int:
-    """Correlation flops of one reference block step on an interior block
-    (reference arithmetic objective.py:170-172 + 2x :258-260):
-    H over the residual rows, H^T over the block, and two majorant products
-    (H of the block-embedded vector, H^T back)."""
-    from paper_2002_02328_b200 import blur
-    from paper_2002_02328_b200.volume import Dims3
-    d = Dims3(*cfg.dims)
-    k = blur.KernelDims(*cfg.kdims)
-    rz = (cfg.kdims[2] - 1) // 2
-    lo = (d.nz // 2 // cfg.block_height) * cfg.block_height
-    hi = min(lo + cfg.block_height - 1, d.nz - 1)
-    emb = blur.flops_H_embedded(d, k, lo, hi)
-    return (blur.flops_H(d, k, max(0, lo - rz), min(d.nz - 1, hi + rz)) + blur.flops_H(d, k, lo, hi)
-            + 2 * 2 * emb)
-
-
-def _reference_extrapolated(args, cfg, world, O, threads):
+def _reference_extrapolated(args, cfg, world, threads):
     """Reference arm where one block step takes minutes per core (C5): the
     reference core's correlation rate is measured on this host -- `threads`
     concurrent calls of 2 output planes with the config's full kernel stack --
-    and one block-iteration is costed at _ref_block_flops.  The numpy
+    and one block-iteration is costed at flops.ref_block_flops.  The numpy
     regulariser work is left out, so the value is an upper bound of the
     reference's block-it/s."""
     from concurrent.futures import ThreadPoolExecutor
 
-    from paper_2002_02328_b200 import blur
-    from paper_2002_02328_b200.volume import Dims3
-    d = Dims3(*cfg.dims)
-    psf = blur.depth_variant_stack(d, cfg.kdims, cfg.sigma_xy, cfg.sigma_z)
-    kz = cfg.kdims[2]
+    from paper_2002_02328_b200 import configs, flops
+    nz = cfg.dims.nz
+    params = configs.depth_variant_params(nz, cfg.sigma_xy, cfg.sigma_z)
+    kx, ky, kz = cfg.kdims
+    R = _reference_pkg()
+    if R is not None:
+        kd = R.blur.KernelDims(*cfg.kdims)
+        kern = np.stack([R.blur.gaussian_kernel(kd, *p) for p in params])
+        correlate = R.kernels.depthvar_correlate
+        core_desc = f"the unmodified reference's bound core (baseline/_ref, {R.kernels.backend_name()})"
+        kind = "reference"
+    else:
+        from oracle import oracle as O
+        kern = np.stack([O.gaussian_psf(kx, ky, kz, *p) for p in params])
+        name = "ref" if O.ref_core_available() else "c"
+        O.core(name, threads=1)
+        correlate = O.core().correlate
+        core_desc = ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if name == "ref"
+                     else "oracle/bd3mg_oracle.c (bitwise the reference core)")
+        kind = "reference" if name == "ref" else "port"
     rz = (kz - 1) // 2
-    zo = d.nz // 2
+    zo = nz // 2
     rng = np.random.Generator(np.random.Philox(0))
-    frag = rng.uniform(0, 1, (kz + 1, d.ny, d.nx))
-    name = "ref" if O.ref_core_available() else "c"
-    O.core(name, threads=1)
-    core = O.core()
+    frag = rng.uniform(0, 1, (kz + 1, cfg.dims.ny, cfg.dims.nx))
     pool = ThreadPoolExecutor(max_workers=threads)
 
     def one(_):
-        return core.correlate(frag, psf.kernels, zo - rz, zo, zo + 1)
+        return correlate(frag, kern, zo - rz, zo, zo + 1)
 
     list(pool.map(one, range(threads)))  # warm-up
     times = []
-    for _ in range(max(1, args.steps)):
+    for _ in range(max(1, min(args.steps, 5))):
         t0 = time.perf_counter()
         list(pool.map(one, range(threads)))
         times.append(time.perf_counter() - t0)
     t = min(times)
-    rate = threads * blur.flops_H(d, blur.KernelDims(*cfg.kdims), zo, zo + 1) / t  # flop/s, all threads
-    fblk = _ref_block_flops(cfg)
+    rate = threads * flops.flops_H(cfg.dims, cfg.kdims, zo, zo + 1) / t  # flop/s, all threads
+    fblk = flops.ref_block_flops(cfg.dims, cfg.kdims, cfg.block_height)
     value = rate / fblk
-    core_desc = ("reference _core.pyx compiled from /root/reference (oracle/_ref)" if name == "ref"
-                 else "oracle/bd3mg_oracle.c (bitwise the reference core)")
     sample = (f"extrapolated: {threads} concurrent 2-plane H calls of config {cfg.name} "
-              f"({cfg.kdims[0]}x{cfg.kdims[1]}x{cfg.kdims[2]} taps) on the core ({core_desc}) ran at "
-              f"{rate / 1e9:.2f} GFLOP/s; one block-iteration costs {fblk / 1e9:.0f} GFLOP of correlations "
-              f"(reference arithmetic); numpy regulariser work excluded (upper bound)")
-    kind = "reference" if name == "ref" else "port"
-    line = {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * len(O.blocks_of(d.nz, cfg.block_height))
-            / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(cfg, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+              f"({kx}x{ky}x{kz} taps) on {core_desc} ran at {rate / 1e9:.2f} GFLOP/s; one block-iteration costs "
+              f"{fblk / 1e9:.0f} GFLOP of correlations (reference arithmetic); numpy regulariser work excluded "
+              f"(upper bound)")
+    B = -(-nz // cfg.block_height)
+    return _ref_line(args, cfg, world, value, 1e3 * B / value, threads, kind, sample)
 
 
 def bench_config(args, world):
@@ -320,18 +434,6 @@ def bench_config(args, world):
         d = cfg.dims
         cfg = dataclasses.replace(cfg, name=f"{cfg.name}x{world}", dims=Dims3(d.nx, d.ny, d.nz * world))
     return cfg
-
-
-def _host_problem(cfg, O):
-    """Seeded inputs on the host: kernels, y (through the oracle H, bitwise
-    the reference's), x0."""
-    from paper_2002_02328_b200 import blur, configs
-    from paper_2002_02328_b200.volume import add_gaussian_noise, init_uniform
-    psf = blur.depth_variant_stack(cfg.dims, cfg.kdims, cfg.sigma_xy, cfg.sigma_z)
-    truth = configs.truth_of(cfg)
-    y = add_gaussian_noise(O.H(psf.kernels, truth), cfg.noise, cfg.seed + 2)
-    x0 = init_uniform(cfg.dims, float(np.max(y)), cfg.seed + 3)
-    return psf.kernels, y, x0
 
 
 def _config_dict(cfg, world):
@@ -395,7 +497,7 @@ def sharded_engine(distributed, obj, x0, cfg, dtype, halo, dist, torch):
 def main():
     args = parse()
     if args.impl == "reference":
-        reference_arm(args, args.config)
+        reference_arm(args)
         return
     import torch
     import torch.distributed as dist
@@ -433,7 +535,8 @@ def main():
             eng = distributed.AsyncEngine(obj, x0, cfg.block_height, dtype, max_delay=2, halo=halo)
         if world > 1:
             halo_note = ("p2p: update-kernel NVLink stores into the readers' halo rings, fenced version flags "
-                         "in a shared host page" if halo == "p2p" else "nccl: isend/irecv halo messages" + why)
+                         "in a shared host page" if halo == "p2p" else
+                         "messages: versioned halo isend/irecv over a gloo group through host memory" + why)
     elif args.mode == "cyclic":
         if world > 1:
             raise SystemExit("--mode cyclic is the single-worker schedule (N=1)")
@@ -798,9 +901,10 @@ def runtime_block(lo, hi):
 
 
 def cpu_baseline(cfg):
-    """Reference CPU path on this host, bounded sample: one block-Jacobi
-    sweep (B block-iterations) with the reference's compiled core."""
-    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "0",
+    """Reference CPU path on this host, bounded sample: the reference arm
+    (unmodified reference, bp3mg live engine) for 3 timed sweeps after 1
+    warm-up, in its own process so this one stays out of its timing."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "3", "--warmup", "1",
            "--config", cfg.name]
     env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
     try:

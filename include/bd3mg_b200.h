@@ -68,7 +68,8 @@ typedef struct {
 
 /* Per-task StepInfo record (reference directions.py:29-40), 16 doubles:
  * [0..2] gram (00,01,11 over the kept columns; one column -> [0]),
- * [3..4] rhs, [5..6] coeffs, [7] ncols, [8] status (1 = non-finite g),
+ * [3..4] rhs, [5..6] coeffs, [7] ncols, [8] status (1 = non-finite g, 2 = non-finite
+ * increment: the 2x2 solve overflowed; in both cases nothing is applied),
  * [9] |g|, [10] coefficient of -g, [11] coefficient of d_mem,
  * [12] kept-column mask (1 = -g, 2 = d_mem). */
 #define BD3MG_INFO_DOUBLES 16
@@ -275,7 +276,10 @@ int bd3mg_peer_free(void* dev);
 /* ---- host-buffer problem handle (worker-task boundary of the reference:
  * TaskMessage -> UpdateMessage, scheduler.py:36-57, runtime.py:92-105) ---- */
 typedef struct bd3mg_problem bd3mg_problem;
-/* kernels/y are host float64 arrays; dtype selects the device arithmetic. */
+/* kernels/y are host float64 arrays; dtype selects the device arithmetic.
+ * Thread safety: calls on one handle are serialised by a per-handle mutex
+ * (they share its stream and buffers).  Threads that must run concurrently
+ * (the reference's live engine, runtime.py:188-241) use one handle each. */
 int bd3mg_problem_create(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const double* kernels_host,
                          const double* y_host, int device, bd3mg_problem** out);
 int bd3mg_problem_destroy(bd3mg_problem* p);

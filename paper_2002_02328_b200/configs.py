@@ -59,6 +59,21 @@ CONFIGS = {
 }
 
 
+def depth_variant_params(nz: int, sigma_xy: tuple[float, float], sigma_z: tuple[float, float]) -> np.ndarray:
+    """BASELINE.json PSF family, one (sigma1, sigma2, sigma3, phi, theta)
+    record per output plane: axis-aligned, sigma_xy and sigma_z linear in
+    t = z/(nz-1).  Torch-free, shared by the GPU arm (blur.depth_variant_stack)
+    and bench.py's reference arm (which builds the kernels with the
+    reference's own gaussian_kernel)."""
+    params = np.empty((nz, 5))
+    for z in range(nz):
+        t = z / (nz - 1) if nz > 1 else 0.0
+        sxy = sigma_xy[0] + (sigma_xy[1] - sigma_xy[0]) * t
+        sz = sigma_z[0] + (sigma_z[1] - sigma_z[0]) * t
+        params[z] = (sxy, sxy, sz, 0.0, 0.0)
+    return params
+
+
 def truth_of(cfg: Config) -> np.ndarray:
     return ellipsoid_phantom(cfg.dims, cfg.n_ellipsoids, cfg.seed + 1, cfg.amplitude)
 

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1568,6 +1569,11 @@ struct bd3mg_problem {
   cudaGraphExec_t graph = nullptr;
   std::vector<int64_t> graph_key;
   int graph_groups = 0;
+  // calls on one handle share its stream, staging buffers and workspace:
+  // they serialise here (the reference's live engine calls its core from
+  // several worker threads at once; give each thread its own handle for
+  // concurrent work)
+  std::mutex mu;
 };
 
 static int download_f64(bd3mg_problem* p, const DevBuf& src, size_t n, double* host) {
@@ -1650,6 +1656,7 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
                                     int64_t z_lo, int64_t z_hi, const double* d_mem, double* inc_out,
                                     double* info_out) {
   if (!p || !x_slab || !inc_out) return fail(BD3MG_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
   CU(cudaSetDevice(p->device));
   const bd3mg_geom_t* g = &p->g;
   const int64_t plane = g->ny * g->nx, h = z_hi - z_lo + 1;
@@ -1685,7 +1692,8 @@ int bd3mg_problem_mg_direction_host(bd3mg_problem* p, const double* x_slab, int6
   CU(cudaMemcpyAsync(info, p->info.p, sizeof(info), cudaMemcpyDeviceToHost, p->s));
   CU(cudaStreamSynchronize(p->s));
   if (info_out) memcpy(info_out, info, sizeof(info));
-  if (info[8] != 0.0) return fail(BD3MG_ENONFINITE, "non-finite gradient");
+  if (info[8] != 0.0)
+    return fail(BD3MG_ENONFINITE, info[8] == 2.0 ? "non-finite increment" : "non-finite gradient");
   return BD3MG_OK;
 }
 
@@ -1869,13 +1877,16 @@ static int pipelined_session_sweep(bd3mg_problem* p, double* x, const int64_t* b
     }
   if (info_out) memcpy(info_out, info, (size_t)nblocks * BD3MG_INFO_DOUBLES * sizeof(double));
   for (int b = 0; b < nblocks; ++b)
-    if (info[(size_t)b * BD3MG_INFO_DOUBLES + 8] != 0.0) return fail(BD3MG_ENONFINITE, "non-finite gradient");
+    if (info[(size_t)b * BD3MG_INFO_DOUBLES + 8] != 0.0)
+      return fail(BD3MG_ENONFINITE, info[(size_t)b * BD3MG_INFO_DOUBLES + 8] == 2.0 ? "non-finite increment"
+                                                                                   : "non-finite gradient");
   return BD3MG_OK;
 }
 
 int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, int64_t frag_z0, int64_t nzf,
                                     const int64_t* blocks, int nblocks, double* terms_out, double* info_out) {
   if (!p || !x || !blocks || nblocks < 1) return fail(BD3MG_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
   CU(cudaSetDevice(p->device));
   const bd3mg_geom_t* g = &p->g;
   if (frag_z0 < 0 || nzf < 1 || frag_z0 + nzf > g->nz) return fail(BD3MG_EINVAL, "invalid fragment");
@@ -1936,7 +1947,9 @@ int bd3mg_problem_jacobi_sweep_host(bd3mg_problem* p, double* x, double* dmem, i
   CU(cudaStreamSynchronize(p->s));
   if (info_out) memcpy(info_out, info.data(), info.size() * sizeof(double));
   for (int b = 0; b < nblocks; ++b)
-    if (info[(size_t)b * BD3MG_INFO_DOUBLES + 8] != 0.0) return fail(BD3MG_ENONFINITE, "non-finite gradient");
+    if (info[(size_t)b * BD3MG_INFO_DOUBLES + 8] != 0.0)
+      return fail(BD3MG_ENONFINITE, info[(size_t)b * BD3MG_INFO_DOUBLES + 8] == 2.0 ? "non-finite increment"
+                                                                                   : "non-finite gradient");
   return BD3MG_OK;
 }
 

@@ -115,7 +115,7 @@ struct SolveArgs {
 
 // info layout per block (kInfoNV doubles):
 // 0-2 gram (00,01,11 of the kept columns; 1 column -> [0]), 3-4 rhs,
-// 5-6 coeffs, 7 ncols, 8 status (0 ok, 1 non-finite g), 9 |g|, 10 c_g
+// 5-6 coeffs, 7 ncols, 8 status (0 ok, 1 non-finite g, 2 non-finite increment), 9 |g|, 10 c_g
 // (coefficient of -g), 11 c_d (coefficient of d), 12 column mask (1:-g, 2:d)
 __device__ void solve_one(const SolveArgs& p, int j, const double* D, const double* R, double* o) {
   for (int k = 0; k < kInfoNV; ++k) o[k] = 0.0;
@@ -152,6 +152,10 @@ __device__ void solve_one(const SolveArgs& p, int j, const double* D, const doub
   }
   o[10] = cg;
   o[11] = cd;
+  // a finite gradient whose solve overflowed: the increment would be
+  // non-finite (the reference master refuses it, scheduler.py:147-148);
+  // status 2, nothing applied
+  if (!isfinite(cg) || !isfinite(cd)) o[8] = 2.0;
 }
 
 // One CTA per block: reduce its conv and regulariser partial rows (same

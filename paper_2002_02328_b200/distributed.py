@@ -388,8 +388,8 @@ class ShardedJacobi:
             self.peer.close()
 
     def check(self) -> None:
-        if bool((self.info[:, 8] != 0).any().item()):
-            raise ValueError("non-finite gradient")
+        from . import scheduler
+        scheduler.raise_step_status(self.info[:, 8])
 
     def f(self) -> float:
         return float(self.terms[4].item())
@@ -425,10 +425,24 @@ class ShardedJacobi:
 # TraceEvent ledger (scheduler.py:60-67, :156-160).
 
 class TorchP2P:
-    """Halo transport over torch.distributed (NCCL on GPUs, gloo on CPUs)."""
+    """Halo transport over torch.distributed messages: gloo (on CPU tensors,
+    or through host memory when the run's group is NCCL, see __init__)."""
 
     def __init__(self, buf: torch.Tensor, z0: int, plan, group=None):
         self.buf, self.z0, self.group = buf, z0, group
+        # NCCL runs every point-to-point op of a rank pair on one stream, so a
+        # receive posted ahead of its send (this protocol keeps one posted per
+        # neighbour) would block the peer's send queued behind the peer's own
+        # posted receive: a deadlock.  On an NCCL group the messages therefore
+        # travel over a gloo group through host memory, whose receives
+        # complete on gloo's own threads.  Collective: every rank of `group`
+        # builds its transport at the same point (AsyncEngine.__init__).
+        self.dev = buf.device
+        self.host = dist.get_backend(group) == "nccl"
+        if self.host:
+            ranks = dist.get_process_group_ranks(group) if group is not None else None
+            self.group = dist.new_group(ranks=ranks, backend="gloo")
+        self.mdev = torch.device("cpu") if self.host else self.dev
         self.recvs = {}   # peer -> (lo, hi, staging, header, [reqs])
         self.sends = {}   # peer -> (lo, hi)
         for peer, lo, hi, kind in plan:
@@ -446,8 +460,8 @@ class TorchP2P:
 
     def _post(self, peer):
         shape = self._planes(self.recvs[peer]).shape
-        stage = torch.empty(shape, dtype=self.buf.dtype, device=self.buf.device)
-        hdr = torch.zeros(1, dtype=torch.int64, device=self.buf.device)
+        stage = torch.empty(shape, dtype=self.buf.dtype, device=self.mdev)
+        hdr = torch.zeros(1, dtype=torch.int64, device=self.mdev)
         reqs = [dist.irecv(hdr, peer, group=self.group), dist.irecv(stage, peer, group=self.group)]
         self.pending[peer] = (stage, hdr, reqs)
 
@@ -455,8 +469,8 @@ class TorchP2P:
         return list(self.sends)
 
     def send(self, peer, version: int):
-        data = self._planes(self.sends[peer]).contiguous()
-        hdr = torch.tensor([version], dtype=torch.int64, device=self.buf.device)
+        data = self._planes(self.sends[peer]).contiguous().to(self.mdev)
+        hdr = torch.tensor([version], dtype=torch.int64, device=self.mdev)
         self.inflight.append((data, hdr, [dist.isend(hdr, peer, group=self.group),
                                           dist.isend(data, peer, group=self.group)]))
         self.inflight = [m for m in self.inflight if not all(r.is_completed() for r in m[2])]
@@ -967,8 +981,8 @@ class AsyncEngine:
 
     def check(self) -> None:
         for info in self.shard.infos:
-            if bool((info[:, 8] != 0).any().item()):
-                raise ValueError("non-finite gradient")
+            from . import scheduler
+            scheduler.raise_step_status(info[:, 8])
 
     def f(self) -> float:
         return float("nan")

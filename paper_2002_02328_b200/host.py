@@ -10,7 +10,9 @@ uploaded once) and serves the two host-level contracts of the reference:
   blocks (runtime.py:244-292) on host arrays, updated in place.
 
 Both go through ``bd3mg_problem_*_host`` (include/bd3mg_b200.h); pass pinned
-host memory (``pinned_empty``) for full PCIe bandwidth.
+host memory (``pinned_empty``) for full PCIe bandwidth.  Calls on one handle are
+serialised by the library (one stream and buffer set per handle); worker
+threads that should overlap each open their own ``HostProblem``.
 """
 
 from __future__ import annotations

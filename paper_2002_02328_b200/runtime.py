@@ -117,8 +117,11 @@ def compute_increment(obj: Objective, task: scheduler.TaskMessage, method: str, 
 
 # ---------------------------------------------------------------------------
 class _StepLog:
-    """Device record of every fused step's StepInfo; non-finite gradients are
-    raised (as the reference's ValueError) at the next host sync."""
+    """Device record of every fused step's StepInfo.  A failed step (status
+    1 = non-finite gradient, 2 = non-finite increment; nothing applied) is
+    raised as the reference's ValueError / ProtocolError: before its ledger
+    entry where the engine checks each step (one worker, barrier cycles),
+    else at the next host sync."""
 
     def __init__(self, device):
         self.buf = torch.empty((256, N.INFO_DOUBLES), dtype=torch.float64, device=device)
@@ -130,16 +133,20 @@ class _StepLog:
             self.check()
             if self.n + count > self.buf.shape[0]:
                 self.n = self.checked = 0
+            if count > self.buf.shape[0]:
+                # a batch wider than the ring (e.g. a barrier cycle of > 256
+                # workers): the native step writes count rows, so grow first
+                self.buf = torch.empty((max(count, 2 * self.buf.shape[0]), N.INFO_DOUBLES),
+                                       dtype=torch.float64, device=self.buf.device)
         out = self.buf[self.n:self.n + count]
         self.n += count
         return out
 
     def check(self) -> None:
         if self.n > self.checked:
-            bad = bool((self.buf[self.checked:self.n, 8] != 0).any().item())
+            status = self.buf[self.checked:self.n, 8]
             self.checked = self.n
-            if bad:
-                raise ValueError("non-finite gradient")
+            scheduler.raise_step_status(status)
 
 
 class _Recorder:
@@ -239,7 +246,12 @@ def _run_simulated(obj, x0, cfg, truth, x_star, L) -> RunResult:
         now, _, task = heapq.heappop(heap)
         msg = scheduler.UpdateMessage(task.worker_id, task.block, None, task.issue_k)
         if _fused(cfg.method):
-            directions.mg_steps_device(obj, [_fused_task(state, task)], cfg.torch_dtype, info=steps.slot(1))
+            info = directions.mg_steps_device(obj, [_fused_task(state, task)], cfg.torch_dtype,
+                                              info=steps.slot(1))
+            # the reference raises in the worker (ValueError) or in
+            # receive_update (ProtocolError) before its ledger moves
+            scheduler.raise_step_status(info[:, 8])
+            steps.checked = steps.n
             scheduler.receive_applied(state, msg)
         else:
             inc = compute_increment(obj, task, cfg.method, L, cfg.cg_tol, cfg.cg_maxit)
@@ -296,6 +308,10 @@ def run_bp3mg_barrier(obj: Objective, x0, cfg: RunConfig, truth=None, x_star=Non
         now += max(draw() for _ in tasks)
         if live:
             torch.cuda.current_stream().synchronize()
+        if _fused(cfg.method):
+            # one check per cycle, before any of its ledger entries
+            # (the reference's pool.map raises before receive_update)
+            steps.check()
         wall = (time.perf_counter() - t0) if live else now
         for t, inc in zip(tasks, incs):
             msg = scheduler.UpdateMessage(t.worker_id, t.block, inc, t.issue_k)
@@ -356,8 +372,7 @@ def _run_live(obj, x0, cfg, truth, x_star, L) -> RunResult:
                             obj, [N.Task(task.x_slab.data_ptr(), task.slab.z_lo, task.x_slab.shape[0],
                                          task.block.z_lo, task.block.z_hi, task.d_mem.data_ptr(),
                                          inc.data_ptr(), None, None)], cfg.torch_dtype, stream=stream)
-                        if info[0, 8].item() != 0.0:
-                            raise ValueError("non-finite gradient")
+                        scheduler.raise_step_status(info[:, 8])
                     else:
                         inc = compute_increment(obj, task, cfg.method, L, cfg.cg_tol, cfg.cg_maxit)
                     done = torch.cuda.Event()
@@ -553,8 +568,7 @@ class JacobiSweeper:
         return self.f()
 
     def check(self) -> None:
-        if bool((self.info[:, 8] != 0).any().item()):
-            raise ValueError("non-finite gradient")
+        scheduler.raise_step_status(self.info[:, 8])
 
     def f(self) -> float:
         """f of the anchor recorded by the last sweep (or by finish())."""
@@ -668,8 +682,7 @@ class CyclicSweeper:
         self.k += len(self.blocks)
 
     def check(self) -> None:
-        if bool((self.info[:, 8] != 0).any().item()):
-            raise ValueError("non-finite gradient")
+        scheduler.raise_step_status(self.info[:, 8])
 
     def f(self) -> float:
         """f after the last sweep (the reference's per-sweep log value)."""

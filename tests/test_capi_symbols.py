@@ -104,3 +104,53 @@ def test_peer_and_flag_entry_points_validate_without_a_gpu():
                                             0, None) == N.BD3MG_EINVAL
     assert N.lib.bd3mg_eval_f_resid(C.byref(g), C.byref(r), None, None, None, None, None, 0, None) == N.BD3MG_EINVAL
     assert b"null" in N.lib.bd3mg_last_error()
+
+
+def test_integration_stub_mirrors_cython_buffer_errors():
+    """integration/_b200.py (the maintainer's binding)
+    raises the reference core's buffer errors -- type, message, order -- for
+    every malformed input the Cython typed memoryviews reject (compared
+    with the reference core compiled in oracle/_ref when present; no GPU
+    work: every case fails before the foreign call)."""
+    import importlib.util
+    import os
+
+    import numpy as np
+    import pytest
+
+    lib = ROOT / "paper_2002_02328_b200" / "_lib" / "libbd3mg_b200.so"
+    if not lib.exists():
+        pytest.skip("library not built")
+    os.environ["BD3MG_B200_LIB"] = str(lib)
+    spec = importlib.util.spec_from_file_location("_b200_stub", ROOT / "integration" / "_b200.py")
+    stub = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(stub)
+    k = np.ones((4, 3, 3, 3)) / 27
+    x = np.zeros((4, 5, 6))
+    ro = x.copy()
+    ro.flags.writeable = False
+    ro_str = x[:, :, ::2]
+    ro_str.flags.writeable = False
+    cases = [(x.astype(np.float32), k), (x, k.astype(np.float32)), (x[:, :, ::2], k), (np.asfortranarray(x), k),
+             (x[0], k), (x.tolist(), k), (x.astype(np.int64), k), (x, k[0]), (ro, k), (ro_str, k),
+             (x[0].astype(np.float32), k), (x.astype(np.float16), k), (x.astype(">f8"), k),
+             (x.astype(np.complex128), k), (x.astype(np.uint8), k), (x.astype(np.bool_), k), (b"abc", k),
+             (x.astype(np.float32), k[0]), (x, k[:, :, :, ::2])]
+    want = None
+    if (ROOT / "oracle" / "_ref").exists():
+        from oracle import oracle as O
+        if O.ref_core_available():
+            want = O._RefCore().mod
+    for frag, ker in cases:
+        for name in ("depthvar_correlate", "depthvar_correlate_adjoint"):
+            with pytest.raises((ValueError, TypeError, BufferError)) as got:
+                getattr(stub, name)(frag, ker, 0, 0, 3)
+            if want is not None:
+                with pytest.raises((ValueError, TypeError, BufferError)) as ref:
+                    getattr(want, name)(frag, ker, 0, 0, 3)
+                assert type(got.value) is type(ref.value) and str(got.value) == str(ref.value), (
+                    str(got.value), str(ref.value))
+    # negative extent: numpy's error, as the reference's np.zeros
+    with pytest.raises(ValueError, match="negative dimensions"):
+        stub.depthvar_correlate(x, k, 0, 3, 0)
+    assert stub.depthvar_correlate(x, k, 0, 3, 2).shape == (0, 5, 6)

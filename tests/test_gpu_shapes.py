@@ -134,3 +134,23 @@ def test_ragged_blocks_p2p_shards_bitwise_and_incremental(dtype):
     assert np.linalg.norm(xa - xb) <= tol * np.linalg.norm(xa)
     for s in shards:
         s.close()
+
+
+def test_barrier_more_workers_than_step_log_rows(oracle_mod):
+    """runtime.run(bp3mg) with 300 workers (one-plane blocks): a cycle is
+    wider than the 256-row device step log, which must grow instead of
+    letting the native step write past it; iterate vs the oracle."""
+    from paper_2002_02328_b200 import blur, objective, runtime
+    from paper_2002_02328_b200.volume import Dims3
+    dims = Dims3(10, 9, 300)
+    psf = blur.depth_variant_stack(dims, (3, 3, 3), (0.8, 1.6), (1.0, 2.0))
+    rng = np.random.Generator(np.random.Philox(300))
+    y = rng.uniform(0, 1, dims.shape)
+    x0 = rng.uniform(0, 1, dims.shape)
+    params = objective.RegParams(lam=1e-2, eta=1e-1, kappa=0.05, delta=1e-2)
+    obj = objective.Objective(psf, y, params)
+    res = runtime.run(obj, x0, runtime.RunConfig(method="bp3mg", workers=300, block_height=1, tol=1e-30,
+                                                 max_updates=600, engine="simulated"))
+    crit = oracle_mod.Criterion(psf.kernels, y, lam=1e-2, eta=1e-1, kappa=0.05, delta=1e-2)
+    want, _, _ = oracle_mod.run_bp3mg(crit, x0, 300, 1, max_updates=600)
+    assert np.linalg.norm(res.x_final - want) <= 1e-12 * np.linalg.norm(want)

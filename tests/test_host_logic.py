@@ -188,3 +188,17 @@ class TestGenerators:
         assert set(configs.CONFIGS) >= {"C1", "C2", "C3", "C4", "C5"}
         c = configs.CONFIGS["C5"]
         assert c.dims == Dims3(1024, 1024, 512) and c.kdims == (9, 9, 21) and c.dtype == "f32"
+
+
+def test_raise_step_status_maps_reference_errors():
+    """StepInfo status column -> the reference's error at the same point:
+    1 = non-finite gradient (ValueError from subspace_step,
+    directions.py:64-65), 2 = non-finite increment (ProtocolError from
+    receive_update, scheduler.py:147-148); the first failed step decides."""
+    import pytest
+    from paper_2002_02328_b200 import scheduler
+    scheduler.raise_step_status(np.zeros(5))
+    with pytest.raises(ValueError, match="non-finite gradient"):
+        scheduler.raise_step_status(np.array([0.0, 1.0, 2.0]))
+    with pytest.raises(scheduler.ProtocolError, match="non-finite increment"):
+        scheduler.raise_step_status(np.array([0.0, 2.0, 1.0]))
