@@ -159,6 +159,29 @@ int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void
                          const void* v, int64_t lo, int64_t hi, void* out, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* Conjugate gradients for A_S(x~) w = b on block [lo, hi] (reference
+ * directions.py:117-149, the inner solve of mm_direction :152-168), entirely
+ * on the device: the recursion's scalars stay in device memory and the call
+ * never waits on an iteration (it only keeps at most 3 iterations queued
+ * ahead of the device).  x_out: x if converged, else the best iterate (as
+ * the reference).  state_out (device, 16 doubles, may be NULL):
+ * [0] |b|, [1] r.r, [2] best residual norm, [5] status (1 converged, 2
+ * stopped: breakdown p.Ap <= 0 or budget; 0 only when maxit == 0),
+ * [6] iterations, [7] relative residual of x_out. */
+size_t bd3mg_cg_solve_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi);
+int bd3mg_cg_solve(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* omega, const void* b,
+                   int64_t lo, int64_t hi, double tol, int32_t maxit, void* x_out, double* state_out, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/* `iters` power-iteration steps on H^T H over the full volume (reference
+ * objective.py:358-366): v <- H^T H v / |H^T H v| in place; norms_out
+ * (device, iters doubles) receives every |H^T H v|.  state_out (device, 2
+ * doubles, may be NULL): [0] = 1 if a norm was 0 (the remaining steps were
+ * skipped; the caller restarts from its RNG as the reference does). */
+size_t bd3mg_power_hth_ws_bytes(const bd3mg_geom_t* g);
+int bd3mg_power_hth(const bd3mg_geom_t* g, const void* kernels, void* v, int32_t iters, double* norms_out,
+                    double* state_out, void* ws, size_t ws_bytes, void* stream);
+
 /* Batched memory-gradient block steps (mg_direction + receive_update) with
  * the forward-only Gram.  `y` must satisfy: y + z*ny*nx is observation row z
  * for every row the tasks touch (a shard may pass its local rows shifted).  Tasks sharing one anchor fragment compute the

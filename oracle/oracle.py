@@ -527,3 +527,112 @@ def run_bp3mg(crit, x0, workers, h, tol=1e-30, max_updates=None, seed=0):
             grant(L, c)
         tasks = [task(L, crit, c) for c in range(1, workers + 1)]
     return L.x.copy(), log, L
+
+
+# ---------------------------------------------------------------------------
+# ablation directions + Lipschitz estimate (reference directions.py:97-168,
+# objective.py:301-375)
+def gd_direction(crit: Criterion, slab, z0, lo, hi, L):
+    """-g / L (directions.py:95-104)."""
+    if L <= 0:
+        raise ValueError("L must be strictly positive")
+    g = crit.grad_block(slab, lo, hi, z0)
+    if not np.isfinite(g).all():
+        raise ValueError("non-finite gradient")
+    return -g / L
+
+
+def cg_direction(crit: Criterion, slab, z0, lo, hi, d_mem, L):
+    """Memory-gradient step with the scalar metric L*Id (directions.py:107-114)."""
+    if L <= 0:
+        raise ValueError("L must be strictly positive")
+    g = crit.grad_block(slab, lo, hi, z0)
+    return subspace_step(g, d_mem, lambda v: L * v).increment
+
+
+def cg_solve(apply_A, b, tol, maxit):
+    """Conjugate gradients, best iterate on breakdown / budget (directions.py:117-149)."""
+    b = np.asarray(b, dtype=np.float64)
+    x = np.zeros_like(b)
+    b_norm = float(np.linalg.norm(b))
+    if b_norm == 0.0:
+        return x, True, 0, 0.0
+    r = b.copy()
+    p = r.copy()
+    rs = float(r @ r)
+    best, best_res = x.copy(), b_norm
+    it = 0
+    for it in range(1, maxit + 1):
+        ap = apply_A(p)
+        p_ap = float(p @ ap)
+        if p_ap <= 0.0:
+            break
+        alpha = rs / p_ap
+        x += alpha * p
+        r -= alpha * ap
+        rs_new = float(r @ r)
+        res = rs_new ** 0.5
+        if res < best_res:
+            best, best_res = x.copy(), res
+        if res <= tol * b_norm:
+            return x, True, it, res / b_norm
+        p = r + (rs_new / rs) * p
+        rs = rs_new
+    return best, False, it, best_res / b_norm
+
+
+def mm_direction(crit: Criterion, slab, z0, lo, hi, cg_tol=1e-8, cg_maxit=200):
+    """A_S(x) d = -g by CG (directions.py:152-168); the warning is the caller's."""
+    if cg_tol <= 0:
+        raise ValueError("cg_tol must be strictly positive")
+    g = crit.grad_block(slab, lo, hi, z0)
+    if not np.isfinite(g).all():
+        raise ValueError("non-finite gradient")
+    if not g.any():
+        return np.zeros_like(g)
+    d, _, _, _ = cg_solve(crit.majorant(slab, lo, hi, z0), -g, cg_tol, cg_maxit)
+    return d
+
+
+def operator_norm_bound(ker):
+    """||H||_1 ||H||_inf (objective.py:322-342)."""
+    nz, kz = ker.shape[0], ker.shape[1]
+    rz = (kz - 1) // 2
+    a = np.abs(ker)
+    hinf = float(a.reshape(nz, -1).sum(axis=1).max())
+    page = a.sum(axis=(2, 3))
+    h1 = 0.0
+    for zi in range(nz):
+        tot = 0.0
+        for k in range(kz):
+            zo = zi + rz - k
+            if 0 <= zo < nz:
+                tot += page[zo, k]
+        h1 = max(h1, tot)
+    return h1 * hinf
+
+
+def rho_hth_estimate(ker, shape, iters=50, seed=0):
+    """Power iteration on H^T H, +5%, capped by the norm bound (objective.py:345-370)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    v = rng.uniform(0.1, 1.0, shape)
+    v /= np.linalg.norm(v)
+    est = prev = 0.0
+    for _ in range(iters):
+        w = Ht(ker, H(ker, v))
+        nrm = float(np.linalg.norm(w))
+        if nrm == 0.0:
+            v = rng.uniform(0.1, 1.0, shape)
+            v /= np.linalg.norm(v)
+            continue
+        prev, est = est, nrm
+        v = w / nrm
+    bound = operator_norm_bound(ker)
+    if not (est > 0 and abs(est - prev) <= 1e-3 * est):
+        return bound
+    return min(1.05 * est, bound)
+
+
+def lipschitz_bound(rho, lam, eta, kappa, delta):
+    """rho + 2 eta + (lam/delta) 2*4 + 2 kappa 4 (objective.py:307-319)."""
+    return rho + 2.0 * eta + (lam / delta) * 2.0 * 4.0 + 2.0 * kappa * 4.0

@@ -6,3 +6,9 @@ entry points kept as a drop-in (blur, objective, directions, scheduler,
 runtime)."""
 
 __version__ = "0.1.0"
+
+
+def N_launches() -> int:
+    """Kernels the native library has launched in this process (eager calls)."""
+    from . import _native
+    return int(_native.lib.bd3mg_launch_count())

@@ -19,6 +19,7 @@
 #include "../../include/bd3mg_b200.h"
 #include "conv_dispatch.cuh"
 #include "errors.h"
+#include "krylov.cuh"
 #include "solver.cuh"
 #include "stencil_tma.cuh"
 
@@ -376,7 +377,7 @@ int eval_f_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T
 
 template <typename T>
 int majorant_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* omega, const T* v, int64_t lo,
-                  int64_t hi, T* out, Ws& ws, cudaStream_t s) {
+                  int64_t hi, T* out, Ws& ws, cudaStream_t s, const double* gate = nullptr) {
   const int64_t nz = g->nz, plane = g->ny * g->nx, rz = (g->kz - 1) / 2;
   if (lo < 0 || hi < lo || hi >= nz) return fail(BD3MG_EINVAL, "invalid block [%lld, %lld]", (long long)lo, (long long)hi);
   const int64_t o_lo = std::max<int64_t>(0, lo - rz), o_hi = std::min<int64_t>(nz - 1, hi + rz);
@@ -386,12 +387,14 @@ int majorant_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   if (!ws.ok()) return ws_fail(ws);
   ConvArgs<T> a = base_args<T>(g, r, K);
   a.njobs = 1;
+  a.gate = gate;
   a.jobs[0].src0 = v; a.jobs[0].src_z0 = lo; a.jobs[0].src_nz = (int)h;
   a.jobs[0].dst0 = hv; a.jobs[0].out_lo = (int)o_lo; a.jobs[0].nout = (int)nr;
   CU(conv_launch<T>(M_STORE, false, a, (int)nr, s));
   launched();
   ConvArgs<T> b = base_args<T>(g, r, K);
   b.njobs = 1;
+  b.gate = gate;
   b.jobs[0].src0 = hv; b.jobs[0].src_z0 = o_lo; b.jobs[0].src_nz = (int)nr;
   b.jobs[0].dst0 = out; b.jobs[0].out_lo = (int)lo; b.jobs[0].nout = (int)h;
   CU(conv_launch<T>(M_STORE, true, b, (int)h, s));
@@ -400,6 +403,7 @@ int majorant_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
   m.v = v; m.omega = omega; m.out = out; m.lo = (int)lo; m.hi = (int)hi; m.nz = (int)nz;
   m.ny = (int)g->ny; m.nx = (int)g->nx; m.plane = plane; m.n = h * plane;
   m.two_eta = 2.0 * r->eta; m.lam = r->lam; m.two_kappa = 2.0 * r->kappa;
+  m.gate = gate;
   majorant_reg_kernel<T><<<(unsigned)((m.n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(m); launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
@@ -414,6 +418,129 @@ int omega_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* frag, int64
   XView<T> xv{frag, frag_z0, (int)nzf, (int)g->ny, (int)g->nx, plane};
   omega_kernel<T><<<(unsigned)((n + kEwNT - 1) / kEwNT), kEwNT, 0, s>>>(xv, (int)lo, n, (T)(r->delta * r->delta), out); launched();
   CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device CG on the block majorant (reference directions.py:117-149) and the
+// power iteration of rho(H^T H) (objective.py:345-370): see krylov.cuh.
+// The host enqueues iterations without waiting on them; it only reads a
+// host-mapped mirror of the iteration counter to stay at most kCgAhead
+// iterations ahead of the device (and to stop enqueueing once the solve has
+// stopped).  Inside a graph capture every iteration is enqueued (gated).
+constexpr int kCgAhead = 3;
+
+struct HostMirror {
+  volatile double* h = nullptr;
+  double* d = nullptr;
+  int device = -1;
+};
+cudaError_t host_mirror(HostMirror** out) {
+  thread_local HostMirror m;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (m.device != dev) {
+    void* hp = nullptr;
+    e = cudaHostAlloc(&hp, 64, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return e;
+    void* dp = nullptr;
+    e = cudaHostGetDevicePointer(&dp, hp, 0);
+    if (e != cudaSuccess) return e;
+    m.h = (volatile double*)hp;
+    m.d = (double*)dp;
+    m.device = dev;
+  }
+  *out = &m;
+  return cudaSuccess;
+}
+
+template <typename T>
+int cg_solve_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* omega, const T* b, int64_t lo,
+                  int64_t hi, double tol, int maxit, T* x_out, double* state_out, Ws& ws, cudaStream_t s) {
+  if (lo < 0 || hi < lo || hi >= g->nz) return fail(BD3MG_EINVAL, "invalid block [%lld, %lld]", (long long)lo, (long long)hi);
+  if (maxit < 0) return fail(BD3MG_EINVAL, "negative iteration budget");
+  const long long n = (hi - lo + 1) * g->ny * g->nx;
+  CgVecs<T> v;
+  v.n = n;
+  v.b = b;
+  v.x = ws.take<T>(n); v.r = ws.take<T>(n); v.p = ws.take<T>(n); v.ap = ws.take<T>(n); v.best = ws.take<T>(n);
+  double* parts = ws.take<double>(kKryCtas);
+  double* st = ws.take<double>(CG_NV);
+  const size_t off_maj = ws.off;  // the majorant's own scratch follows, reused every iteration
+  int rc = majorant_impl<T>(g, r, K, omega, v.p, lo, hi, v.ap, ws, s, st + CG_STATUS);
+  if (rc || ws.measure) return rc;
+  if (!ws.ok()) return ws_fail(ws);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cap));
+  HostMirror* hm = nullptr;
+  if (cap == cudaStreamCaptureStatusNone) CU(host_mirror(&hm));
+  volatile double* hmir = hm ? hm->h : nullptr;
+  double* dmir = hm ? hm->d : nullptr;
+  if (hmir) { hmir[0] = -1.0; hmir[1] = 0.0; }
+  cg_init_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(v, parts); launched();
+  cg_init_state_kernel<<<1, kEwNT, 0, s>>>(parts, st, dmir); launched();
+  CU(cudaGetLastError());
+  for (int it = 1; it <= maxit; ++it) {
+    Ws mw = ws;
+    mw.off = off_maj;
+    rc = majorant_impl<T>(g, r, K, omega, v.p, lo, hi, v.ap, mw, s, st + CG_STATUS);
+    if (rc) return rc;
+    cg_pap_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(v, st, parts); launched();
+    cg_alpha_kernel<<<1, kEwNT, 0, s>>>(parts, st); launched();
+    cg_xr_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(v, st, parts); launched();
+    cg_check_kernel<<<1, kEwNT, 0, s>>>(parts, st, tol, maxit, dmir); launched();
+    cg_p_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(v, st); launched();
+    CU(cudaGetLastError());
+    if (hmir) {
+      // stay at most kCgAhead iterations ahead; stop enqueueing once stopped
+      while (hmir[1] == 0.0 && hmir[0] < (double)(it - kCgAhead)) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) break;  // drained: the mirror is final
+        if (q != cudaErrorNotReady) return fail(BD3MG_ECUDA, "cg: %s", cudaGetErrorString(q));
+      }
+      if (hmir[1] != 0.0) break;
+    }
+  }
+  cg_result_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(v, st, x_out); launched();
+  if (state_out) CU(cudaMemcpyAsync(state_out, st, CG_NV * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CU(cudaGetLastError());
+  return BD3MG_OK;
+}
+
+template <typename T>
+int power_hth_impl(const bd3mg_geom_t* g, const T* K, T* v, int iters, double* norms, double* state_out, Ws& ws,
+                   cudaStream_t s) {
+  if (iters < 0) return fail(BD3MG_EINVAL, "negative iteration count");
+  const long long n = g->nz * g->ny * g->nx;
+  T* hv = ws.take<T>(n);
+  T* w = ws.take<T>(n);
+  double* parts = ws.take<double>(kKryCtas);
+  double* st = ws.take<double>(2);
+  if (ws.measure) return BD3MG_OK;
+  if (!ws.ok()) return ws_fail(ws);
+  CU(cudaMemsetAsync(st, 0, 2 * sizeof(double), s));
+  for (int it = 0; it < iters; ++it) {
+    ConvArgs<T> a = base_args<T>(g, nullptr, K);
+    a.gate = st;
+    a.njobs = 1;
+    a.jobs[0].src0 = v; a.jobs[0].src_z0 = 0; a.jobs[0].src_nz = (int)g->nz;
+    a.jobs[0].dst0 = hv; a.jobs[0].out_lo = 0; a.jobs[0].nout = (int)g->nz;
+    CU(conv_launch<T>(M_STORE, false, a, (int)g->nz, s));
+    launched();
+    ConvArgs<T> b2 = base_args<T>(g, nullptr, K);
+    b2.gate = st;
+    b2.njobs = 1;
+    b2.jobs[0].src0 = hv; b2.jobs[0].src_z0 = 0; b2.jobs[0].src_nz = (int)g->nz;
+    b2.jobs[0].dst0 = w; b2.jobs[0].out_lo = 0; b2.jobs[0].nout = (int)g->nz;
+    CU(conv_launch<T>(M_STORE, true, b2, (int)g->nz, s));
+    launched();
+    pw_norm_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(w, n, st, parts); launched();
+    pw_finish_kernel<<<1, kEwNT, 0, s>>>(parts, st, norms, it); launched();
+    pw_scale_kernel<T><<<kKryCtas, kEwNT, 0, s>>>(w, v, n, st); launched();
+    CU(cudaGetLastError());
+  }
+  if (state_out) CU(cudaMemcpyAsync(state_out, st, 2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
   return BD3MG_OK;
 }
 
@@ -1305,6 +1432,50 @@ int bd3mg_majorant_apply(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void
                                           hi, (double*)out, ws, (cudaStream_t)stream),
                     majorant_impl<float>(g, r, (const float*)kernels, (const float*)omega, (const float*)v, lo, hi,
                                          (float*)out, ws, (cudaStream_t)stream));
+}
+
+size_t bd3mg_cg_solve_ws_bytes(const bd3mg_geom_t* g, int64_t lo, int64_t hi) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  bd3mg_reg_t r{1, 1, 1, 1, 0, 1};
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, cg_solve_impl<double>(g, &r, nullptr, nullptr, nullptr, lo, hi, 1.0, 1, nullptr, nullptr, ws, 0),
+                      cg_solve_impl<float>(g, &r, nullptr, nullptr, nullptr, lo, hi, 1.0, 1, nullptr, nullptr, ws, 0));
+  });
+}
+
+int bd3mg_cg_solve(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kernels, const void* omega, const void* b,
+                   int64_t lo, int64_t hi, double tol, int32_t maxit, void* x_out, double* state_out, void* wsp,
+                   size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!r || !kernels || !omega || !b || !x_out) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    cg_solve_impl<double>(g, r, (const double*)kernels, (const double*)omega, (const double*)b, lo, hi,
+                                          tol, maxit, (double*)x_out, state_out, ws, (cudaStream_t)stream),
+                    cg_solve_impl<float>(g, r, (const float*)kernels, (const float*)omega, (const float*)b, lo, hi,
+                                         tol, maxit, (float*)x_out, state_out, ws, (cudaStream_t)stream));
+}
+
+size_t bd3mg_power_hth_ws_bytes(const bd3mg_geom_t* g) {
+  if (check_geom(g) != BD3MG_OK) return (size_t)-1;
+  return measure([&](Ws& ws) {
+    return DISPATCH_T(g, power_hth_impl<double>(g, nullptr, nullptr, 1, nullptr, nullptr, ws, 0),
+                      power_hth_impl<float>(g, nullptr, nullptr, 1, nullptr, nullptr, ws, 0));
+  });
+}
+
+int bd3mg_power_hth(const bd3mg_geom_t* g, const void* kernels, void* v, int32_t iters, double* norms_out,
+                    double* state_out, void* wsp, size_t ws_bytes, void* stream) {
+  int rc = check_geom(g);
+  if (rc) return rc;
+  if (!kernels || !v || (iters > 0 && !norms_out)) return fail(BD3MG_EINVAL, "null argument");
+  Ws ws = make_ws(wsp, ws_bytes);
+  return DISPATCH_T(g,
+                    power_hth_impl<double>(g, (const double*)kernels, (double*)v, iters, norms_out, state_out, ws,
+                                           (cudaStream_t)stream),
+                    power_hth_impl<float>(g, (const float*)kernels, (float*)v, iters, norms_out, state_out, ws,
+                                          (cudaStream_t)stream));
 }
 
 size_t bd3mg_jacobi_sweep_ws_bytes(const bd3mg_geom_t* g, const bd3mg_sweep_t* sw) {

@@ -76,6 +76,7 @@ struct ConvArgs {
   int raster_group;     // tiles per rasterisation group (0: plain x, y, z order); see cta_pos
   double* partials;     // [gridDim.z * tiles_y * tiles_x][NV]
   double two_eta, lam, two_kappa, delta2, x_min, x_max;
+  const double* gate;   // optional: the launch is a no-op while *gate != 0 (device-side loops, krylov.cuh)
   ConvJob<T> jobs[kMaxJobs];
 };
 
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   T* coef_s = reinterpret_cast<T*>(sbase + 2 * NIN * Cfg::TILE_BYTES);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::coef_bytes(p.kz));
   double* red_s = reinterpret_cast<double*>(mbar + 2);
+  if (p.gate && *p.gate != 0.0) return;
 
   const CtaPos pos = cta_pos(p.raster_group);
   const int zidx = pos.z;
@@ -630,6 +632,7 @@ __global__ void __launch_bounds__(Rz2Cfg<T, KY, KX, MODE>::NT)
   T* slices = reinterpret_cast<T*>(sbase + 2 * Cfg::BUF_BYTES);  // [buf][out][KS]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * Cfg::BUF_BYTES + Cfg::SLICE_BYTES);
   double* red_s = reinterpret_cast<double*>(mbar + 2);
+  if (p.gate && *p.gate != 0.0) return;
 
   const CtaPos pos = cta_pos(p.raster_group);
   const int zidx = pos.z;
@@ -867,6 +870,7 @@ __global__ void __launch_bounds__(kGenericNT) conv_generic_kernel(const __grid_c
   T* coef_s = reinterpret_cast<T*>(smem_raw);
   size_t coef_bytes = ((size_t)p.kz * p.ky * p.kx * sizeof(T) + 15) & ~size_t(15);
   double* red_s = reinterpret_cast<double*>(smem_raw + coef_bytes);
+  if (p.gate && *p.gate != 0.0) return;
   const CtaPos pos = cta_pos(p.raster_group);
   const int zidx = pos.z;
   const int jid = find_job(p, zidx);

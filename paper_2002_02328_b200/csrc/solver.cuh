@@ -286,12 +286,13 @@ struct MajArgs {
   int lo, hi, nz, ny, nx;
   long long plane, n;
   double two_eta, lam, two_kappa;
+  const double* gate;  // optional: no-op while *gate != 0 (krylov.cuh)
 };
 
 template <typename T>
 __global__ void __launch_bounds__(kEwNT) majorant_reg_kernel(const __grid_constant__ MajArgs<T> p) {
   const long long i = (long long)blockIdx.x * kEwNT + threadIdx.x;
-  if (i >= p.n) return;
+  if (i >= p.n || (p.gate && *p.gate != 0.0)) return;
   const int h = p.hi - p.lo + 1;
   const int t = (int)(i / p.plane);  // local plane
   const long long rem = i % p.plane;

@@ -214,7 +214,13 @@ def cg_direction(obj: Objective, x_slab, slab_z0: int, block: SliceBlock, d_mem,
 
 
 def cg_solve(apply_A, b, tol: float, maxit: int):
-    """Conjugate gradients for SPD A; best iterate on breakdown/budget."""
+    """Conjugate gradients for SPD A; best iterate on breakdown/budget
+    (reference directions.py:117-149).  When A is a block majorant
+    (``MajorantOperator.apply``) the whole solve runs on the device
+    (bd3mg_cg_solve); any other callable runs this host-driven loop."""
+    maj = getattr(apply_A, "__self__", None)
+    if isinstance(maj, MajorantOperator) and getattr(apply_A, "__func__", None) is MajorantOperator.apply:
+        return maj.solve_cg(b, tol, maxit)
     b = _vec(b)
     x = b * 0
     b_norm = _dot(b, b) ** 0.5

@@ -212,6 +212,30 @@ class MajorantOperator:
             raise ValueError(f"expected flat vector of length {self.n}, got {tuple(v.shape)}")
         return self.apply_device(v)
 
+    def solve_cg(self, b, tol: float, maxit: int):
+        """Conjugate gradients for A_S(x~) w = b on the device
+        (bd3mg_cg_solve; reference directions.py:117-149): no host round trip
+        per iteration.  Returns (w, converged, iterations, relative_residual)
+        with w a device tensor for tensor input, numpy otherwise."""
+        bt = D.to_device(b, self.dtype).reshape(-1)
+        if bt.numel() != self.n:
+            raise ValueError(f"expected flat vector of length {self.n}, got {tuple(bt.shape)}")
+        g = self.obj.geom(self.dtype)
+        blk = self.block
+        nbytes = N.ws_bytes(N.lib.bd3mg_cg_solve_ws_bytes(D.byref(g), blk.z_lo, blk.z_hi))
+        ws = D.workspace(nbytes)
+        out = torch.empty(self.n, dtype=self.dtype, device=bt.device)
+        state = torch.zeros(16, dtype=torch.float64, device=bt.device)
+        k = self.obj.psf.device_kernels(self.dtype, bt.device)
+        N.check(N.lib.bd3mg_cg_solve(D.byref(g), D.byref(D.reg(self.obj.params)), k.data_ptr(), self.omega.data_ptr(),
+                                     bt.contiguous().data_ptr(), blk.z_lo, blk.z_hi, float(tol), int(maxit),
+                                     out.data_ptr(), state.data_ptr(), ws.data_ptr(), nbytes, D.stream_handle()))
+        st = state.cpu().numpy()
+        status, iters = int(st[5]), int(st[6])
+        relres = float(st[7]) if status != 0 else float(st[2] / st[0])
+        w = out if D.is_tensor(b) else D.to_host(out)
+        return w, status == 1, iters, relres
+
     def _anchor_data(self):
         if self._g_anchor is None:
             if self.anchor_z0 != 0 or self.anchor.shape[0] != self.obj.dims.nz:
@@ -273,8 +297,39 @@ def operator_norm_bound(psf: blur.PsfStack) -> float:
 
 
 def rho_hth_estimate(psf: blur.PsfStack, iters: int = 50, seed: int = 0) -> float:
-    """Power iteration on H^T H (device), inflated 5%, capped by the norm
-    bound (reference objective.py:345-370)."""
+    """Power iteration on H^T H, inflated 5%, capped by the norm bound
+    (reference objective.py:345-370).  The iteration runs on the device
+    (bd3mg_power_hth: every |H^T H v| is kept in a device array, one host
+    read at the end); should H annihilate an iterate, the remaining steps
+    replay the reference's RNG restarts on the host path."""
+    rng = philox(seed)
+    dev = D.default_device()
+    v = torch.from_numpy(rng.uniform(0.1, 1.0, psf.dims.shape)).to(dev)
+    v /= torch.linalg.vector_norm(v)
+    dt = torch.float64
+    g = D.geom(psf.dims, psf.kdims, dt)
+    nbytes = N.ws_bytes(N.lib.bd3mg_power_hth_ws_bytes(D.byref(g)))
+    ws = D.workspace(nbytes)
+    norms = torch.zeros(max(iters, 1), dtype=torch.float64, device=dev)
+    state = torch.zeros(2, dtype=torch.float64, device=dev)
+    k = psf.device_kernels(dt, dev)
+    N.check(N.lib.bd3mg_power_hth(D.byref(g), k.data_ptr(), v.data_ptr(), int(iters), norms.data_ptr(),
+                                  state.data_ptr(), ws.data_ptr(), nbytes, D.stream_handle()))
+    nrm = norms.cpu().numpy()[:iters]
+    bound = operator_norm_bound(psf)
+    if state[0].item() != 0.0:
+        return _rho_hth_host(psf, iters, seed)
+    est = float(nrm[-1]) if iters >= 1 else 0.0
+    prev = float(nrm[-2]) if iters >= 2 else 0.0
+    if not (est > 0 and abs(est - prev) <= 1e-3 * est):
+        return bound
+    return min(1.05 * est, bound)
+
+
+def _rho_hth_host(psf: blur.PsfStack, iters: int, seed: int) -> float:
+    """Host-orchestrated power iteration (device operators, one sync per
+    step) reproducing the reference's RNG restarts when H annihilates an
+    iterate (objective.py:361-364)."""
     rng = philox(seed)
     v = torch.from_numpy(rng.uniform(0.1, 1.0, psf.dims.shape)).to(D.default_device())
     v /= torch.linalg.vector_norm(v)

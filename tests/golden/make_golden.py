@@ -170,6 +170,50 @@ def c1_case(blur, objective, runtime, volume):
     return out
 
 
+def ablation_cases(blur, directions, objective, volume):
+    """The ablation directions and the Lipschitz estimate (directions.py:97-168,
+    objective.py:301-375) as the reference computes them."""
+    import warnings
+    out = {}
+    for i, (dims, kd, seed) in enumerate([((12, 10, 16), (3, 3, 5), 3), ((9, 11, 12), (5, 5, 3), 4)]):
+        d3 = volume.Dims3(*dims)
+        ranges = blur.ParamRanges(sigma1=(0.6, 1.1), sigma2=(0.6, 1.1), sigma3=(0.6, 1.1))
+        psf = blur.generate_psf_stack(d3, blur.KernelDims(*kd), ranges, seed)
+        truth = volume.phantom(d3, 20 + i)
+        y = volume.add_gaussian_noise(blur.apply_H(psf, truth), 0.05, 30 + i)
+        params = objective.RegParams(lam=1e-2, eta=1e-1, kappa=0.05, delta=1e-2)
+        obj = objective.Objective(psf, y, params)
+        rng = philox(300 + i)
+        x = rng.uniform(-0.2, 1.2, d3.shape)
+        L = objective.lipschitz_estimate(obj)
+        case = dict(kernels=psf.kernels, y=y, x=x, reg=np.array([params.lam, params.eta, params.kappa, params.delta,
+                                                                  params.x_min, params.x_max]),
+                    rho=np.array(objective.rho_hth_estimate(psf)),
+                    rho3=np.array(objective.rho_hth_estimate(psf, iters=3, seed=1)),
+                    norm_bound=np.array(objective.operator_norm_bound(psf)), L=np.array(L))
+        for j, (lo, hi) in enumerate([(4, 7), (0, 2)]):
+            blk = volume.SliceBlock(lo, hi)
+            slab = blur.slab_support(psf, blk)
+            frag = x[slab.z_lo:slab.z_hi + 1]
+            n = blk.count(d3)
+            dmem = 0.01 * rng.standard_normal(n)
+            g = objective.grad_block(obj, frag, blk, slab.z_lo)
+            maj = objective.MajorantOperator(obj, frag, blk, slab.z_lo)
+            case[f"b{j}_blk"] = np.array([lo, hi])
+            case[f"b{j}_dmem"] = dmem
+            case[f"b{j}_gd"] = directions.gd_direction(obj, frag, slab.z_lo, blk, L)
+            case[f"b{j}_cg"] = directions.cg_direction(obj, frag, slab.z_lo, blk, dmem, L)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                case[f"b{j}_mm"] = directions.mm_direction(obj, frag, slab.z_lo, blk, cg_tol=1e-8, cg_maxit=200)
+            for tag, tol, maxit in (("conv", 1e-10, 400), ("budget", 1e-12, 4)):
+                xs, conv, iters, relres = directions.cg_solve(maj.apply, -g, tol, maxit)
+                case[f"b{j}_cg_{tag}_x"] = xs
+                case[f"b{j}_cg_{tag}_meta"] = np.array([float(conv), float(iters), relres, tol, float(maxit)])
+        out[f"abl{i}"] = case
+    return out
+
+
 def io_cases(blur, volume):
     """Container files written by the reference's own writers
     (volume.py:104-114, blur.py:201-211) plus the arrays they hold."""
@@ -190,11 +234,19 @@ def main():
         io_cases(blur, volume)
         return
     print("reference backend:", kernels.backend_name())
+    if "--only-ablation" in sys.argv:
+        ab = ablation_cases(blur, directions, objective, volume)
+        np.savez_compressed(OUT / "ablation.npz", **{f"{c}/{k}": v for c, d in ab.items() for k, v in d.items()})
+        return
     cases = {}
     cases.update(blur_cases(blur, kernels, volume))
     np.savez_compressed(OUT / "blur.npz", **{f"{c}/{k}": v for c, d in cases.items() for k, v in d.items()})
     oc = objective_cases(blur, directions, objective, volume)
     np.savez_compressed(OUT / "objective.npz", **{f"{c}/{k}": v for c, d in oc.items() for k, v in d.items()})
+    ab = ablation_cases(blur, directions, objective, volume)
+    np.savez_compressed(OUT / "ablation.npz", **{f"{c}/{k}": v for c, d in ab.items() for k, v in d.items()})
+    if "--only-ablation" in sys.argv:
+        return
     c1 = c1_case(blur, objective, runtime, volume)
     np.savez_compressed(OUT / "c1.npz", **c1)
     io_cases(blur, volume)
