@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          *os.environ.get("BD3MG_DEFS", "").split()]
-UNITS = ["capi.cu", "conv_f64.cu", "conv_f32.cu", "microbench.cu", "io.cu", "separable.cu"]
+UNITS = ["capi.cu", "conv_f64.cu", "conv_f32.cu", "microbench.cu", "io.cu", "separable.cu", "sweep_pk.cu"]
 
 
 def _deps() -> list[Path]:

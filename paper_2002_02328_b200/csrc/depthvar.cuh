@@ -40,6 +40,8 @@ enum ConvMode : int {
   M_GRAM1 = 3,  // partial: sum acc0^2               (+ optional store dst0 = acc0)
   M_GRAM2 = 4,  // partial: acc0^2, acc0*acc1, acc1^2 (dual input, shared taps)
   M_GRAMC = 5,  // dst0 = acc0 (H E_S g); partial: acc0^2, acc0*c, c^2 with c = sub[o] (cached H E_S d)
+  M_GRAM2P = 6, // M_GRAM2 as two single-input passes over one tile ring (input 1, then input 0):
+                // the same tile, sums and partials bit for bit, half the staging smem
 };
 
 constexpr int kMaxJobs = 32;
@@ -64,13 +66,20 @@ struct alignas(64) ConvJob {
                         //    staged by TMA into the free tile buffer during the last tap plane
 };
 
+// Geometry / coefficient part of the launch arguments: everything one output
+// tile needs besides its own job (conv_tile takes this; the persistent sweep
+// kernel, sweep_pk.cuh, embeds one).
 template <typename T>
-struct ConvArgs {
+struct ConvGeom {
   const T* K;           // (nzk, kz, ky, kx) coefficient stack
   int nzk, kz, ky, kx;  // runtime kz; ky/kx also template params on fast path
   int ny, nx;
   long long plane;      // ny*nx
   int nz_global;        // global depth (axial far-face rule)
+};
+
+template <typename T>
+struct ConvArgs : ConvGeom<T> {
   int njobs;
   int tiles_x, tiles_y;
   int raster_group;     // tiles per rasterisation group (0: plain x, y, z order); see cta_pos
@@ -111,7 +120,7 @@ BD3MG_D CtaPos cta_pos(int group) {
 template <int MODE>
 struct ModeNV {
   static constexpr int value =
-      (MODE == M_RESID || MODE == M_GRAM1) ? 1 : ((MODE == M_GRAM2 || MODE == M_GRAMC) ? 3 : 0);
+      (MODE == M_RESID || MODE == M_GRAM1) ? 1 : ((MODE == M_GRAM2 || MODE == M_GRAMC || MODE == M_GRAM2P) ? 3 : 0);
 };
 
 // ---------------------------------------------------------------------------
@@ -167,11 +176,13 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 template <typename T, int KY_, int KX_, int MODE>
 struct ConvCfg {
   static constexpr bool DUAL = (MODE == M_GRAM2);
+  static constexpr bool TWOPASS = (MODE == M_GRAM2P);
   static constexpr int KY = KY_, KX = KX_;
   static constexpr int VEC = 16 / sizeof(T);        // elements per 16-byte load
   static constexpr int RX = VEC;                    // outputs per thread in x
-  // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32)
-  static constexpr int RY = DUAL ? (sizeof(T) == 8 ? BD3MG_RY2 : 4) : BD3MG_RY1;
+  // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32); the two-pass
+  // Gram keeps the dual-input tile (same pixels per CTA, so the same partial sums)
+  static constexpr int RY = (DUAL || TWOPASS) ? (sizeof(T) == 8 ? BD3MG_RY2 : 4) : BD3MG_RY1;
   static constexpr int WX = 32, WY = 4;             // a warp spans one row group
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
@@ -196,9 +207,11 @@ struct ConvCfg {
   static constexpr size_t TILE_BYTES = (size_t)TILE * sizeof(T);  // 128-byte aligned buffer stride
   static constexpr size_t BOX_BYTES = (size_t)BOX * sizeof(T);
   BD3MG_HD static size_t coef_bytes(int kz) { return ((size_t)kz * KY * KX * sizeof(T) + 127) & ~size_t(127); }
-  static size_t smem_bytes(int kz) {
-    return coef_bytes(kz) + 2 * NIN * TILE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + 128;
+  // bytes conv_tile uses from its 128-byte aligned base
+  static size_t layout_bytes(int kz) {
+    return coef_bytes(kz) + 2 * NIN * TILE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double);
   }
+  static size_t smem_bytes(int kz) { return layout_bytes(kz) + 128; }
 };
 
 template <typename T>
@@ -210,7 +223,7 @@ BD3MG_D int find_job(const ConvArgs<T>& p, int zidx) {
 
 // Stage the coefficient set of output plane `zo` (adjoint: gathered) into smem.
 template <typename T, bool ADJ>
-BD3MG_D void stage_coefs(const ConvArgs<T>& p, int zo, T* cs, int nt) {
+BD3MG_D void stage_coefs(const ConvGeom<T>& p, int zo, T* cs, int nt) {
   const int KYX = p.ky * p.kx, n = p.kz * KYX;
   const int rz = (p.kz - 1) / 2;
   for (int i = threadIdx.x; i < n; i += nt) {
@@ -254,37 +267,62 @@ struct Vec16<float> {
   using type = float4;
 };
 
+// One input of a tile: TMA map (box PITCH x BOXH at z = depth - z0) and the
+// same fragment for the cp.async fallback.
+template <typename T>
+struct TileSrc {
+  const CUtensorMap* tm;
+  const T* src;  // plane 0 = global depth z0 (cp.async fallback)
+  long long z0;  // global depth of the fragment's first plane
+  int nz;        // planes in the fragment (taps outside read zero)
+  long long tz0; // global depth of the TMA map's z = 0 (<= z0; a map may span more rows than the fragment)
+};
+
+// Everything one output tile of one output plane reads and writes.
+template <typename T>
+struct TileIO {
+  TileSrc<T> in0, in1;          // in1: second input (M_GRAM2; M_GRAM2P runs it as the first pass)
+  T* dst;                       // output plane (row y at dst + y*nx), or null
+  const T* sub;                 // epilogue operand plane, same alignment, or null
+  const CUtensorMap* tm_epi;    // epilogue operand TMA (TX x TY box at (x0, y0, epi_z)), or null
+  int epi_z;
+  bool use_tma;
+};
+
+// One TY x TX output tile of output plane zo: the kz-tap walk over the staged
+// input planes (double-buffered TMA ring, mbarrier completion), the register-
+// tiled FMA loop, and the mode's epilogue; `part` receives the CTA's NV
+// partial sums (thread 0).  `sbase` is the 128-byte aligned shared memory of
+// ConvCfg::smem_bytes.  Shared by conv_tiled_kernel (one tile per CTA) and
+// the persistent sweep kernel (sweep_pk.cuh: many tiles per CTA), so both
+// compute bit-identical values.
 template <typename T, int KY, int KX, int MODE, bool ADJ>
-__global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
-    conv_tiled_kernel(const __grid_constant__ ConvArgs<T> p) {
+BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0, int y0, double* part_out,
+                       unsigned char* sbase, uint64_t* bars = nullptr) {
   using Cfg = ConvCfg<T, KY, KX, MODE>;
   using V = typename Vec16<T>::type;
   constexpr int RX = Cfg::RX, RY = Cfg::RY, NIN = Cfg::NIN, VEC = Cfg::VEC;
   constexpr int WINP = Cfg::WINP, OFF = Cfg::OFF;
   constexpr int RYH = Cfg::RYH, RXA = Cfg::RXA;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr bool TWOPASS = Cfg::TWOPASS;
   // 128-byte aligned carve-out: [tiles][coefs][mbarriers][reduction scratch]
-  unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // stays in .shared
   T* tiles = reinterpret_cast<T*>(sbase);
   T* coef_s = reinterpret_cast<T*>(sbase + 2 * NIN * Cfg::TILE_BYTES);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::coef_bytes(p.kz));
-  double* red_s = reinterpret_cast<double*>(mbar + 2);
-  if (p.gate && *p.gate != 0.0) return;
+  uint64_t* mbar_l = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::coef_bytes(p.kz));
+  double* red_s = reinterpret_cast<double*>(mbar_l + 2);
+  uint64_t* mbar = bars ? bars : mbar_l;  // persistent kernel: barriers at a fixed location
 
-  const CtaPos pos = cta_pos(p.raster_group);
-  const int zidx = pos.z;
-  const int jid = find_job(p, zidx);
-  const ConvJob<T>& job = p.jobs[jid];
-  const int zo = job.out_lo + (zidx - job.work_begin);
-  const int x0 = pos.tx * Cfg::TX, y0 = pos.ty * Cfg::TY;
   const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
   const int rz = (p.kz - 1) / 2;
-  const bool tma = job.use_tma != 0;
+  const bool tma = io.use_tma;
 
   // taps a whose input plane zo+a-rz lies inside the fragment
-  const long long zlo_in = job.src_z0, zhi_in = job.src_z0 + job.src_nz - 1;
+  const long long zlo_in = io.in0.z0, zhi_in = io.in0.z0 + io.in0.nz - 1;
   const int a_lo = (int)max(0LL, zlo_in - zo + rz);
   const int a_hi = (int)min((long long)p.kz - 1, zhi_in - zo + rz);
+  const int ntap = a_hi - a_lo + 1;
+  // steps of the walk: the taps (two-pass Gram: the taps over input 1, then over input 0)
+  const int nstep = TWOPASS ? 2 * ntap : ntap;
 
   if (tma && threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
@@ -294,20 +332,23 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   stage_coefs<T, ADJ>(p, zo, coef_s, Cfg::NT);
   __syncthreads();
 
-  auto issue = [&](int a, int b) {
+  auto issue = [&](int step, int b) {
     T* dst = tiles + b * NIN * Cfg::TILE;
+    const bool second = TWOPASS && step < ntap;  // pass 0 of the two-pass Gram reads input 1
+    const int a = a_lo + (TWOPASS && step >= ntap ? step - ntap : step);
     const int zi = zo + a - rz;
+    const TileSrc<T>& in = second ? io.in1 : io.in0;
     if (tma) {
       if (threadIdx.x == 0) {
         mbar_expect_tx(&mbar[b], (uint32_t)(NIN * Cfg::BOX_BYTES));
-        tma_load_3d(dst, &job.tmap0, x0 - RXA, y0 - RYH, (int)(zi - job.src_z0), &mbar[b]);
+        tma_load_3d(dst, in.tm, x0 - RXA, y0 - RYH, (int)(zi - in.tz0), &mbar[b]);
         if constexpr (NIN == 2)
-          tma_load_3d(dst + Cfg::TILE, &job.tmap1, x0 - RXA, y0 - RYH, (int)(zi - job.src_z0), &mbar[b]);
+          tma_load_3d(dst + Cfg::TILE, io.in1.tm, x0 - RXA, y0 - RYH, (int)(zi - io.in1.tz0), &mbar[b]);
       }
     } else {
-      stage_tile_fallback<Cfg>(dst, job.src0, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
+      stage_tile_fallback<Cfg>(dst, in.src, in.z0, zi, y0, x0, p.ny, p.nx, p.plane);
       if constexpr (NIN == 2)
-        stage_tile_fallback<Cfg>(dst + Cfg::TILE, job.src1, job.src_z0, zi, y0, x0, p.ny, p.nx, p.plane);
+        stage_tile_fallback<Cfg>(dst + Cfg::TILE, io.in1.src, io.in1.z0, zi, y0, x0, p.ny, p.nx, p.plane);
       cp_async_commit();
     }
   };
@@ -319,42 +360,58 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
     for (int r = 0; r < RY; ++r)
 #pragma unroll
       for (int i = 0; i < RX; ++i) acc[s][r][i] = T(0);
+  T accp[TWOPASS ? RY : 1][RX];  // two-pass Gram: input 1's sums, parked after pass 0
+#pragma unroll
+  for (int r = 0; r < (TWOPASS ? RY : 1); ++r)
+#pragma unroll
+    for (int i = 0; i < RX; ++i) accp[r][i] = T(0);
 
-  if (a_lo <= a_hi) issue(a_lo, 0);
+  if (nstep > 0) issue(0, 0);
   // the epilogue operand rows of this tile are pulled into L2 two taps before
   // the end, so the epilogue's loads do not wait on DRAM
   constexpr bool kEpiLoad = MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC;
-  const long long orow = (long long)(zo - job.out_lo) * p.plane;
   const bool vec_io = (p.nx % VEC) == 0;  // rows are whole 16-byte chunks
-  const int a_pf = max(a_lo, a_hi - 1);
+  const int s_pf = max(0, nstep - 2);
   // RESID / GRAD: the epilogue operand tile (y rows or the regulariser
   // gradient) is loaded by TMA into the tile buffer the last tap plane frees,
   // while that plane computes; the epilogue then reads it from shared memory
   constexpr bool kEpiTma = (MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC) && NIN == 1 && sizeof(T) == 8;
-  const bool epi_tma = kEpiTma && tma && job.epi_tma && a_lo <= a_hi;
+  const bool epi_tma = kEpiTma && tma && io.tm_epi != nullptr && nstep > 0;
   uint32_t phase = 0;  // bit b = parity of buffer b
   int buf = 0;
-  for (int a = a_lo; a <= a_hi; ++a) {
-    if (a < a_hi) {
-      issue(a + 1, buf ^ 1);
+  for (int st = 0; st < nstep; ++st) {
+    if (st < nstep - 1) {
+      issue(st + 1, buf ^ 1);
     } else if (epi_tma && threadIdx.x == 0) {
       mbar_expect_tx(&mbar[buf ^ 1], (uint32_t)(Cfg::TX * Cfg::TY * sizeof(T)));
-      tma_load_3d(tiles + (buf ^ 1) * NIN * Cfg::TILE, &job.tmap1, x0, y0, zo - job.out_lo, &mbar[buf ^ 1]);
+      tma_load_3d(tiles + (buf ^ 1) * NIN * Cfg::TILE, io.tm_epi, x0, y0, io.epi_z, &mbar[buf ^ 1]);
     }
     if constexpr (kEpiLoad) {
-      if (a == a_pf && vec_io && job.sub && threadIdx.x < Cfg::TY) {
+      if (st == s_pf && vec_io && io.sub && threadIdx.x < Cfg::TY) {
         const int y = y0 + threadIdx.x, w = min(Cfg::TX, p.nx - x0);
-        if (y < p.ny && w > 0) prefetch_l2_bulk(job.sub + orow + (long long)y * p.nx + x0, (uint32_t)(w * sizeof(T)));
+        if (y < p.ny && w > 0) prefetch_l2_bulk(io.sub + (long long)y * p.nx + x0, (uint32_t)(w * sizeof(T)));
+      }
+    }
+    if constexpr (TWOPASS) {
+      if (st == ntap) {  // pass 0 (input 1) done: park its sums, restart for input 0
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int i = 0; i < RX; ++i) {
+            accp[r][i] = acc[0][r][i];
+            acc[0][r][i] = T(0);
+          }
       }
     }
     if (tma) {
       mbar_wait(&mbar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
     } else {
-      if (a < a_hi) cp_async_wait<1>();
+      if (st < nstep - 1) cp_async_wait<1>();
       else cp_async_wait<0>();
       __syncthreads();
     }
+    const int a = a_lo + (TWOPASS && st >= ntap ? st - ntap : st);
     const T* cs = coef_s + a * (KY * KX);
     const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
 #pragma unroll
@@ -408,14 +465,14 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
       for (int r = 0; r < RY; ++r) {
         const int y = y0 + ty * RY + r;
         if (y >= p.ny) continue;
-        const long long o = orow + (long long)y * p.nx + xt;
+        const long long o = (long long)y * p.nx + xt;
         T res[RX];
         if constexpr (MODE == M_STORE) {
 #pragma unroll
           for (int i = 0; i < RX; ++i) res[i] = acc[0][r][i];
         } else {
           const V q = epi_tma ? *reinterpret_cast<const V*>(etile + (ty * RY + r) * Cfg::TX + tx * RX)
-                              : *reinterpret_cast<const V*>(job.sub + o);
+                              : *reinterpret_cast<const V*>(io.sub + o);
           const T* qs = reinterpret_cast<const T*>(&q);
 #pragma unroll
           for (int i = 0; i < RX; ++i) {
@@ -433,7 +490,7 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
             }
           }
         }
-        if (MODE != M_RESID || job.dst0) *reinterpret_cast<V*>(job.dst0 + o) = *reinterpret_cast<const V*>(res);
+        if (MODE != M_RESID || io.dst) *reinterpret_cast<V*>(io.dst + o) = *reinterpret_cast<const V*>(res);
       }
     }
   }
@@ -446,27 +503,27 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
     for (int i = 0; i < RX; ++i) {
       const int x = x0 + tx * RX + i;
       if (x >= p.nx) continue;
-      const long long o = orow + (long long)y * p.nx + x;
+      const long long o = (long long)y * p.nx + x;
       const T a0 = acc[0][r][i];
       if constexpr (MODE == M_STORE) {
-        job.dst0[o] = a0;
+        io.dst[o] = a0;
       } else if constexpr (MODE == M_RESID) {
-        const T res = sub_rn(a0, job.sub[o]);
-        if (job.dst0) job.dst0[o] = res;
+        const T res = sub_rn(a0, io.sub[o]);
+        if (io.dst) io.dst[o] = res;
         part[0] += (double)res * (double)res;
       } else if constexpr (MODE == M_GRAD) {
-        job.dst0[o] = add_rn(a0, job.sub[o]);
+        io.dst[o] = add_rn(a0, io.sub[o]);
       } else if constexpr (MODE == M_GRAM1) {
-        if (job.dst0) job.dst0[o] = a0;
+        if (io.dst) io.dst[o] = a0;
         part[0] += (double)a0 * (double)a0;
-      } else if constexpr (MODE == M_GRAM2) {
-        const T a1 = acc[NIN - 1][r][i];
+      } else if constexpr (MODE == M_GRAM2 || MODE == M_GRAM2P) {
+        const T a1 = TWOPASS ? accp[TWOPASS ? r : 0][i] : acc[NIN - 1][r][i];
         part[0] += (double)a0 * (double)a0;
         part[1] += (double)a0 * (double)a1;
         part[2] += (double)a1 * (double)a1;
       } else if constexpr (MODE == M_GRAMC) {
-        const double c0 = (double)job.sub[o];
-        job.dst0[o] = a0;
+        const double c0 = (double)io.sub[o];
+        io.dst[o] = a0;
         part[0] += (double)a0 * (double)a0;
         part[1] += (double)a0 * c0;
         part[2] += c0 * c0;
@@ -476,12 +533,36 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   }  // !vec_here
   if constexpr (NV > 0) {
     cta_reduce<NV, Cfg::NT>(part, red_s);
-    if (threadIdx.x == 0) {
-      const long long cta = pos.cta;
+    if (threadIdx.x == 0 && part_out) {
 #pragma unroll
-      for (int k = 0; k < NV; ++k) p.partials[cta * NV + k] = part[k];
+      for (int k = 0; k < NV; ++k) part_out[k] = part[k];
     }
   }
+}
+
+template <typename T, int KY, int KX, int MODE, bool ADJ>
+__global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
+    conv_tiled_kernel(const __grid_constant__ ConvArgs<T> p) {
+  using Cfg = ConvCfg<T, KY, KX, MODE>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* sbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // stays in .shared
+  if (p.gate && *p.gate != 0.0) return;
+  const CtaPos pos = cta_pos(p.raster_group);
+  const int zidx = pos.z;
+  const ConvJob<T>& job = p.jobs[find_job(p, zidx)];
+  const int zo = job.out_lo + (zidx - job.work_begin);
+  const long long orow = (long long)(zo - job.out_lo) * p.plane;
+  TileIO<T> io;
+  io.in0 = {&job.tmap0, job.src0, job.src_z0, job.src_nz, job.src_z0};
+  io.in1 = {&job.tmap1, job.src1, job.src_z0, job.src_nz, job.src_z0};
+  io.dst = job.dst0 ? job.dst0 + orow : nullptr;
+  io.sub = job.sub ? job.sub + orow : nullptr;
+  io.tm_epi = job.epi_tma ? &job.tmap1 : nullptr;
+  io.epi_z = zo - job.out_lo;
+  io.use_tma = job.use_tma != 0;
+  constexpr int NV = Cfg::NV;
+  conv_tile<T, KY, KX, MODE, ADJ>(p, io, zo, pos.tx * Cfg::TX, pos.ty * Cfg::TY,
+                                  NV > 0 ? p.partials + pos.cta * NV : nullptr, sbase);
 }
 
 
@@ -530,7 +611,7 @@ struct Rz2Cfg {
 };
 
 template <typename T>
-BD3MG_D bool tap_ok(const ConvArgs<T>& p, bool adj, int zo, int a) {
+BD3MG_D bool tap_ok(const ConvGeom<T>& p, bool adj, int zo, int a) {
   if (a < 0 || a >= p.kz) return false;
   if (!adj) return true;
   const int zsrc = zo + a - (p.kz - 1) / 2;
@@ -539,7 +620,7 @@ BD3MG_D bool tap_ok(const ConvArgs<T>& p, bool adj, int zo, int a) {
 
 // coefficient (b, c) of tap a for output plane zo (adjoint: gathered, flipped)
 template <typename T, bool ADJ>
-BD3MG_D T coef_of(const ConvArgs<T>& p, int zo, int a, int b, int c) {
+BD3MG_D T coef_of(const ConvGeom<T>& p, int zo, int a, int b, int c) {
   const int KYX = p.ky * p.kx, K3 = p.kz * KYX;
   if (!ADJ) return p.K[(long long)zo * K3 + a * KYX + b * p.kx + c];
   const int zsrc = zo + a - (p.kz - 1) / 2;

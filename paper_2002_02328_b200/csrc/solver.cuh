@@ -27,7 +27,7 @@ constexpr int kRedMaxNV = 12;
 // holds the same sum), then the 8 warp sums in warp order.  Result in
 // res[0:nv] for every thread (after the barrier).  Latency: 5 shuffles and
 // one barrier instead of an 8-level shared-memory tree.
-__device__ __forceinline__ void cta_sum_rows(const double* __restrict__ rows, int nv, long long begin,
+static __device__ __forceinline__ void cta_sum_rows(const double* __restrict__ rows, int nv, long long begin,
                                              long long end, double (*s)[kEwNT / 32], double* res) {
   constexpr int NW = kEwNT / 32;
   double acc[kRedMaxNV];
@@ -64,7 +64,7 @@ __device__ __forceinline__ void cta_sum_rows(const double* __restrict__ rows, in
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
+static __global__ void __launch_bounds__(kEwNT) reduce_rows_kernel(const double* __restrict__ rows, int nv,
                                                             const __grid_constant__ RowRanges rr,
                                                             double* __restrict__ out, int out_stride) {
   __shared__ double s[kRedMaxNV][kEwNT / 32];
@@ -117,7 +117,7 @@ struct SolveArgs {
 // 0-2 gram (00,01,11 of the kept columns; 1 column -> [0]), 3-4 rhs,
 // 5-6 coeffs, 7 ncols, 8 status (0 ok, 1 non-finite g, 2 non-finite increment), 9 |g|, 10 c_g
 // (coefficient of -g), 11 c_d (coefficient of d), 12 column mask (1:-g, 2:d)
-__device__ void solve_one(const SolveArgs& p, int j, const double* D, const double* R, double* o) {
+static __device__ void solve_one(const SolveArgs& p, int j, const double* D, const double* R, double* o) {
   for (int k = 0; k < kInfoNV; ++k) o[k] = 0.0;
   const double gg = R[0], dd = R[2], gd = R[9];
   const double gn = sqrt(gg);
@@ -160,7 +160,7 @@ __device__ void solve_one(const SolveArgs& p, int j, const double* D, const doub
 
 // One CTA per block: reduce its conv and regulariser partial rows (same
 // deterministic order as reduce_rows_kernel), then the 2x2 solve.
-__global__ void __launch_bounds__(kEwNT) reduce_solve_kernel(const __grid_constant__ SolveArgs p,
+static __global__ void __launch_bounds__(kEwNT) reduce_solve_kernel(const __grid_constant__ SolveArgs p,
                                                              const double* __restrict__ gram_rows,
                                                              const double* __restrict__ reg_rows,
                                                              double* __restrict__ info) {
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kEwNT) update_kernel(const __grid_constant__ U
 }
 
 // terms: [data, box, tv, axial, f, |x-snap|^2, |snap|^2]
-__global__ void eval_finalize_kernel(const double* __restrict__ data1, const double* __restrict__ ew5,
+static __global__ void eval_finalize_kernel(const double* __restrict__ data1, const double* __restrict__ ew5,
                                      double eta, double lam, double kappa, double* __restrict__ terms) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double data = 0.5 * data1[0];

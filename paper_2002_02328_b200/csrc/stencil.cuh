@@ -36,14 +36,22 @@ struct StJob {
   int work_begin;  // first grid.z index of the job
   int chunk;       // reg_gram (TMA path): [lo, hi] is a z-chunk of the block [blo, bhi]
   int blo, bhi;
+  T* snap_out;     // greg with recorder terms: snapshot roll, snap_out row z-lo = x row z after it is read (or null)
+  int tz_off, tz_off_b;  // reg_gram TMA: z coordinate of row lo in the maps of a / b (0: maps start at row lo)
+};
+
+// geometry and regulariser weights of a stencil launch (the tile functions
+// of stencil_tma.cuh take this; the persistent sweep kernel embeds one)
+template <typename T>
+struct StGeom {
+  int nz, ny, nx;
+  long long plane;
+  double two_eta, lam, two_kappa, delta2, x_min, x_max;
 };
 
 template <typename T>
-struct StArgs {
-  int nz, ny, nx;
-  long long plane;
+struct StArgs : StGeom<T> {
   int njobs, tiles_x, tiles_y;
-  double two_eta, lam, two_kappa, delta2, x_min, x_max;
   double* partials;  // reg_gram / eval: [grid.z * tiles][NV]
   StJob<T> jobs[kMaxJobs];
 };
@@ -333,6 +341,7 @@ __global__ void __launch_bounds__(kStNT) greg_z_kernel(const __grid_constant__ S
           ev[3] += ((double)xc - (double)sn[j]) * ((double)xc - (double)sn[j]);
           ev[4] += (double)sn[j] * (double)sn[j];
         }
+        if (J.snap_out) J.snap_out[orow + (long long)y * p.nx + x] = xc;
       }
     }
     __syncthreads();  // ring slot of z-1 is refilled next iteration; px/py rewritten

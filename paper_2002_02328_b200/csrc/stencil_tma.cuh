@@ -77,23 +77,22 @@ inline long long tm_tiles(long long ny, long long nx) {
 }
 
 // ---------------------------------------------------------------------------
+// Regulariser gradient, omega (+ recorder terms, snapshot roll when EVAL) of
+// the 32 x 16 pixel column (bx, by) over every row of job J.  `tma_a` maps
+// J.a with the GregGeo box; `base` is 128-byte aligned smem of GregGeo::smem.
 template <typename T, bool EVAL>
-__global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ StArgs<T> p,
-                                                       const __grid_constant__ StTma<T> tm) {
+BD3MG_D void greg_tile(const StGeom<T>& p, const StJob<T>& J, const CUtensorMap* tma_a, int bx, int by,
+                       double* part_out, unsigned char* base, uint64_t* bars_ext = nullptr) {
   using G = GregGeo<T>;
   constexpr int VEC = G::VEC;
-  extern __shared__ __align__(128) unsigned char st_smem[];
-  unsigned char* base = st_smem + ((128 - (smem_u32(st_smem) & 127)) & 127);
   T (*xs)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base);
   T* hpy = reinterpret_cast<T*>(base + G::RING * G::PL * sizeof(T));  // py of row y0-1, cols x0..x0+31
   T* hpx = hpy + kTmX;                                                // px of col x0-1, rows y0..y0+15
   T* lastpy = hpx + kTmY;                                             // [warp][lane]: py of the warp's last row
   double* red = reinterpret_cast<double*>(lastpy + G::NW * kTmX);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kEvalNV);
+  uint64_t* bars = bars_ext ? bars_ext : reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kEvalNV);
 
-  const int job = blockIdx.z;
-  const StJob<T>& J = p.jobs[job];
-  const int x0 = blockIdx.x * kTmX, y0 = blockIdx.y * kTmY;
+  const int x0 = bx * kTmX, y0 = by * kTmY;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int zfirst = max(J.lo - 1, 0), zlast = min(J.hi + 1, p.nz - 1);
   const int nx = p.nx, ny = p.ny;
@@ -107,10 +106,10 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
   auto issue = [&](int z) {  // thread 0
     const int s = slot(z);
     mbar_expect_tx(&bars[s], G::PL * sizeof(T));
-    tma_load_3d(xs[s], &tm.a[job], x0 - VEC, y0 - 1, (int)(z - J.a_z0), &bars[s]);
+    tma_load_3d(xs[s], tma_a, x0 - VEC, y0 - 1, (int)(z - J.a_z0), &bars[s]);
   };
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tm.a[job]);
+    tma_prefetch_desc(tma_a);
     for (int z = zfirst; z <= min(J.lo + 1, zlast); ++z) issue(z);
   }
   for (int z = zfirst; z <= J.lo; ++z) mbar_wait(&bars[slot(z)], phase(z));
@@ -207,35 +206,45 @@ __global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ S
           ev[3] += ((double)xc[j] - (double)sn[j]) * ((double)xc[j] - (double)sn[j]);
           ev[4] += (double)sn[j] * (double)sn[j];
         }
+        if (J.snap_out) J.snap_out[orow + (long long)y * nx + x] = xc[j];
       }
     }
     __syncthreads();  // halo px/py rewritten and the slot of z-1 refilled next iteration
   }
   if constexpr (EVAL) {
     cta_reduce<kEvalNV, kTmNT>(ev, red);
-    if (threadIdx.x == 0) {
-      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0 && part_out) {
 #pragma unroll
-      for (int k = 0; k < kEvalNV; ++k) p.partials[cta * kEvalNV + k] = ev[k];
+      for (int k = 0; k < kEvalNV; ++k) part_out[k] = ev[k];
     }
   }
 }
 
-// ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant__ StArgs<T> p,
-                                                           const __grid_constant__ StTma<T> tm) {
-  using G = RgGeo<T>;
+template <typename T, bool EVAL>
+__global__ void __launch_bounds__(kTmNT) greg_t_kernel(const __grid_constant__ StArgs<T> p,
+                                                       const __grid_constant__ StTma<T> tm) {
   extern __shared__ __align__(128) unsigned char st_smem[];
   unsigned char* base = st_smem + ((128 - (smem_u32(st_smem) & 127)) & 127);
+  const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  greg_tile<T, EVAL>(p, p.jobs[blockIdx.z], &tm.a[blockIdx.z], blockIdx.x, blockIdx.y,
+                     EVAL ? p.partials + cta * kEvalNV : nullptr, base);
+}
+
+// ---------------------------------------------------------------------------
+// Regulariser Gram terms, rhs and flags of the 32 x 16 column (bx, by) over
+// the rows of job J (g = J.a via tma_a, d = J.b via tma_b, omega = J.w).
+// `ldcg`: omega is read through L2 only (written by another CTA of the same
+// persistent kernel).
+template <typename T, bool LDCG = false>
+BD3MG_D void reg_gram_tile(const StGeom<T>& p, const StJob<T>& J, const CUtensorMap* tma_a, const CUtensorMap* tma_b,
+                           int bx, int by, double* part_out, unsigned char* base, uint64_t* bars_ext = nullptr) {
+  using G = RgGeo<T>;
   T (*gs)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base);
   T (*dss)[G::PL] = reinterpret_cast<T (*)[G::PL]>(base + G::RING * G::PL * sizeof(T));
   double* red = reinterpret_cast<double*>(base + 2 * G::RING * G::PL * sizeof(T));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kRegNV);
+  uint64_t* bars = bars_ext ? bars_ext : reinterpret_cast<uint64_t*>(red + (kTmNT / 32) * kRegNV);
 
-  const int job = blockIdx.z;
-  const StJob<T>& J = p.jobs[job];
-  const int x0 = blockIdx.x * kTmX, y0 = blockIdx.y * kTmY;
+  const int x0 = bx * kTmX, y0 = by * kTmY;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool has_d = J.b != nullptr;
   const int nx = p.nx, ny = p.ny;
@@ -254,12 +263,12 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
   auto issue = [&](int z) {  // thread 0
     const int s = slot(z);
     mbar_expect_tx(&bars[s], (has_d ? 2 : 1) * G::PL * sizeof(T));
-    tma_load_3d(gs[s], &tm.a[job], x0, y0, z - J.lo, &bars[s]);
-    if (has_d) tma_load_3d(dss[s], &tm.b[job], x0, y0, z - J.lo, &bars[s]);
+    tma_load_3d(gs[s], tma_a, x0, y0, z - J.lo + J.tz_off, &bars[s]);
+    if (has_d) tma_load_3d(dss[s], tma_b, x0, y0, z - J.lo + J.tz_off_b, &bars[s]);
   };
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tm.a[job]);
-    if (has_d) tma_prefetch_desc(&tm.b[job]);
+    tma_prefetch_desc(tma_a);
+    if (has_d) tma_prefetch_desc(tma_b);
     issue(J.lo);
     if (J.lo + 1 <= zend) issue(J.lo + 1);
   }
@@ -275,7 +284,8 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
 #pragma unroll
     for (int j = 0; j < kTmR; ++j) {
       const int y = y0 + warp * kTmR + j;
-      wv[j] = (y < ny && x < nx) ? J.w[orow + (long long)y * nx + x] : T(0);
+      if constexpr (LDCG) wv[j] = (y < ny && x < nx) ? __ldcg(J.w + orow + (long long)y * nx + x) : T(0);
+      else wv[j] = (y < ny && x < nx) ? J.w[orow + (long long)y * nx + x] : T(0);
     }
     if (threadIdx.x == 0 && z + 2 <= zend) issue(z + 2);
     if (z + 1 <= zend) mbar_wait(&bars[slot(z + 1)], phase(z + 1));
@@ -328,11 +338,20 @@ __global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant
     __syncthreads();  // slot of z is refilled next iteration
   }
   cta_reduce<kRegNV, kTmNT>(v, red);
-  if (threadIdx.x == 0) {
-    const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0 && part_out) {
 #pragma unroll
-    for (int k = 0; k < kRegNV; ++k) p.partials[cta * kRegNV + k] = v[k];
+    for (int k = 0; k < kRegNV; ++k) part_out[k] = v[k];
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTmNT) reg_gram_t_kernel(const __grid_constant__ StArgs<T> p,
+                                                           const __grid_constant__ StTma<T> tm) {
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  unsigned char* base = st_smem + ((128 - (smem_u32(st_smem) & 127)) & 127);
+  const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  reg_gram_tile<T>(p, p.jobs[blockIdx.z], &tm.a[blockIdx.z], &tm.b[blockIdx.z], blockIdx.x, blockIdx.y,
+                   p.partials + cta * kRegNV, base);
 }
 
 }  // namespace bd3mg
