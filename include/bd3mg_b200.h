@@ -173,6 +173,13 @@ int bd3mg_cg_solve(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kern
                    int64_t lo, int64_t hi, double tol, int32_t maxit, void* x_out, double* state_out, void* ws,
                    size_t ws_bytes, void* stream);
 
+/* Diagnostics of the persistent sweep: with BD3MG_PK_TRACE=1 set, every
+ * persistent bd3mg_jacobi_sweep records per item 4 u64: dequeue, dependencies
+ * met and completion times (ns, %globaltimer) and (sm << 48 | type << 40 |
+ * block << 32 | z << 16 | aux).  Copies the last sweep's records (after a
+ * device synchronise); *n_out = items of that sweep. */
+int bd3mg_pk_trace(void* host, int64_t max_items, int64_t* n_out);
+
 /* `iters` power-iteration steps on H^T H over the full volume (reference
  * objective.py:358-366): v <- H^T H v / |H^T H v| in place; norms_out
  * (device, iters doubles) receives every |H^T H v|.  state_out (device, 2

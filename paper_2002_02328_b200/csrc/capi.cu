@@ -1042,69 +1042,108 @@ int mg_steps_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const
 // order).
 constexpr int kPkIneligible = 1000;
 
+// BD3MG_PK_TRACE=1: per-item timestamps of the last persistent sweep
+// (diagnostics; bd3mg_pk_trace copies them out)
+struct PkTrace {
+  std::mutex mu;
+  unsigned long long* buf = nullptr;
+  size_t cap = 0, n = 0;
+};
+PkTrace& pk_trace() {
+  static PkTrace t;
+  return t;
+}
+
 struct PkGroup {
   int type, b, z, aux;
   int n;         // items
-  double cost;   // per item (model microseconds)
+  double cost;   // per item (model microseconds on a slot of its class)
+  int aff;       // the earliest block whose update depends on the group (pipelining bias)
   std::vector<int> succ;
   int npred = 0;
-  double bl = 0;
+  double bl = 0, prio = 0;
   int started = 0, finished = 0;
 };
 
+// FMA-bound correlation tiles vs memory-bound items (stencils, solve,
+// update, reductions).  The simulation gives every SM one memory slot and
+// the rest to correlations (an idle slot takes the other class when its own
+// has nothing ready), so the order interleaves the HBM-bound items with the
+// correlations at the rate the SMs can overlap them.
+inline bool pk_is_conv(int type) { return type == PK_RESID || type == PK_GRAD || type == PK_GRAM; }
+
 // returns false when the order does not fit kPkMaxSeg segments
-static bool pk_schedule(std::vector<PkGroup>& G, int slots, std::vector<PkSeg>& segs, uint32_t& total) {
+static bool pk_schedule(std::vector<PkGroup>& G, int slots, int sms, int nb, std::vector<PkSeg>& segs,
+                        uint32_t& total) {
   const int ng = (int)G.size();
   for (int i = ng - 1; i >= 0; --i) {  // groups are created in a topological order
     double m = 0;
     for (int j : G[i].succ) m = std::max(m, G[j].bl);
     G[i].bl = G[i].cost + m;
+    // longest path first; among comparable paths the earlier block (its
+    // update then overlaps the later blocks' correlations)
+    G[i].prio = G[i].bl + 4.0 * (nb - G[i].aff);
   }
   for (auto& g : G)
     for (int j : g.succ) G[j].npred++;
-  auto cmp = [&](int a, int b) { return G[a].bl != G[b].bl ? G[a].bl < G[b].bl : a > b; };
-  std::priority_queue<int, std::vector<int>, decltype(cmp)> ready(cmp);
+  auto cmp = [&](int a, int b) { return G[a].prio != G[b].prio ? G[a].prio < G[b].prio : a > b; };
+  using PQ = std::priority_queue<int, std::vector<int>, decltype(cmp)>;
+  PQ ready[2] = {PQ(cmp), PQ(cmp)};  // [0] correlation items, [1] memory-bound items
   for (int i = 0; i < ng; ++i)
-    if (G[i].npred == 0 && G[i].n > 0) ready.push(i);
-  using Ev = std::pair<double, int>;
+    if (G[i].npred == 0 && G[i].n > 0) ready[pk_is_conv(G[i].type) ? 0 : 1].push(i);
+  struct Ev {
+    double t;
+    int g, cls;
+    bool operator>(const Ev& o) const { return t > o.t; }
+  };
   std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> running;
+  const int mem_slots = std::max(1, std::min(slots / 2, sms));  // one memory-bound item per SM
+  int free_slots[2] = {slots - mem_slots, mem_slots};
   double t = 0;
-  int free_slots = slots;
   segs.clear();
   total = 0;
   int last_group = -1;
+  auto start = [&](int cls, int q) {
+    const int gi = ready[q].top();
+    PkGroup& g = G[gi];
+    if (last_group != gi) {  // a new segment (a group's items are taken in order)
+      PkSeg sg;
+      sg.first = total;
+      sg.type = (uint8_t)g.type;
+      sg.b = (uint8_t)g.b;
+      if (pk_is_conv(g.type)) { sg.z = (uint16_t)g.z; sg.aux = (uint16_t)g.started; }
+      else if (g.type == PK_RG) { sg.z = (uint16_t)g.started; sg.aux = (uint16_t)g.aux; }
+      else if (g.type == PK_RED) { sg.z = (uint16_t)g.z; sg.aux = 0; }
+      else { sg.z = (uint16_t)g.started; sg.aux = 0; }  // GREG: first tile, UPD: first chunk, SOLVE: 0
+      segs.push_back(sg);
+      last_group = gi;
+    }
+    ++total;
+    ++g.started;
+    --free_slots[cls];
+    running.push({t + g.cost, gi, cls});
+    if (g.started == g.n) ready[q].pop();
+  };
   while (true) {
-    while (free_slots > 0 && !ready.empty()) {
-      const int gi = ready.top();
-      PkGroup& g = G[gi];
-      if (last_group != gi) {  // a new segment (a group's items are taken in order)
-        PkSeg sg;
-        sg.first = total;
-        sg.type = (uint8_t)g.type;
-        sg.b = (uint8_t)g.b;
-        if (g.type == PK_RESID || g.type == PK_GRAD || g.type == PK_GRAM) { sg.z = (uint16_t)g.z; sg.aux = (uint16_t)g.started; }
-        else if (g.type == PK_RG) { sg.z = (uint16_t)g.started; sg.aux = (uint16_t)g.aux; }
-        else if (g.type == PK_RED) { sg.z = (uint16_t)g.z; sg.aux = 0; }
-        else { sg.z = (uint16_t)g.started; sg.aux = 0; }  // GREG: first tile, UPD: first chunk, SOLVE: 0
-        segs.push_back(sg);
-        last_group = gi;
-        if ((int)segs.size() > kPkMaxSeg) return false;
+    bool progress = true;
+    while (progress) {
+      progress = false;
+      for (int cls = 0; cls < 2; ++cls) {
+        if (free_slots[cls] == 0) continue;
+        if (!ready[cls].empty()) { start(cls, cls); progress = true; }
+        else if (!ready[1 - cls].empty()) { start(cls, 1 - cls); progress = true; }
       }
-      ++total;
-      ++g.started;
-      --free_slots;
-      running.push({t + g.cost, gi});
-      if (g.started == g.n) ready.pop();
+      if ((int)segs.size() > kPkMaxSeg) return false;
     }
     if (running.empty()) break;
     const Ev e = running.top();
     running.pop();
-    t = e.first;
-    ++free_slots;
-    PkGroup& g = G[e.second];
+    t = e.t;
+    ++free_slots[e.cls];
+    PkGroup& g = G[e.g];
     if (++g.finished == g.n)
       for (int j : g.succ)
-        if (--G[j].npred == 0) ready.push(j);
+        if (--G[j].npred == 0) ready[pk_is_conv(G[j].type) ? 0 : 1].push(j);
   }
   for (auto& g : G)
     if (g.started != g.n) return false;  // unreachable group: malformed plan
@@ -1115,7 +1154,7 @@ template <int K>
 static bool pk_maps(PkArgs<double>& a, const bd3mg_geom_t* g, const double* x, int64_t nzf, const double* y_rows,
                     const double* r, int64_t nres, const double* gb, const double* greg, int64_t hsum,
                     const double* dm) {
-  using CR = ConvCfg<double, K, K, M_RESID>;
+  using CR = ConvCfg<double, K, K, M_RESID, kPkRY>;
   using CM = ConvCfg<double, K, K, M_GRAM2P>;
   using GG = GregGeo<double>;
   using RG = RgGeo<double>;
@@ -1143,7 +1182,10 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
   if constexpr (!std::is_same<T, double>::value) {
     return kPkIneligible;
   } else {
-    const bool off = getenv("BD3MG_NO_PK") != nullptr;  // read per call: tests compare both paths
+    // opt-in (BD3MG_PK=1): measured slower than the multi-kernel sweep at C2 so far (535 vs 424 us, see
+    // DESIGN.md); read per call so tests can compare both paths
+    const char* pk_env = getenv("BD3MG_PK");
+    const bool off = getenv("BD3MG_NO_PK") != nullptr || !pk_env || pk_env[0] == '0';
     const int Kk = g->kx;
     if (off || g->kx != g->ky || !(Kk == 3 || Kk == 5 || Kk == 7 || Kk == 9) || !st_use_tma<T>(g->nx) || !sw->dmem ||
         sw->hd_cache || nmirrors > kMaxMirSegs)
@@ -1154,7 +1196,7 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
     const int64_t u_lo = std::max<int64_t>(0, rec_lo - rz), u_hi = std::min<int64_t>(nz - 1, rec_hi + rz);
     if (u_lo < sw->frag_z0 || u_hi > sw->frag_z0 + sw->nzf - 1 + rz) return kPkIneligible;
     const int64_t P = u_hi - u_lo + 1;
-    using CR = ConvCfg<double, 5, 5, M_RESID>;
+    using CR = ConvCfg<double, 5, 5, M_RESID, kPkRY>;
     using CM = ConvCfg<double, 5, 5, M_GRAM2P>;
     const int conv_tx = (int)((g->nx + CR::TX - 1) / CR::TX), conv_ty = (int)((g->ny + CR::TY - 1) / CR::TY);
     const int gram_tx = (int)((g->nx + CM::TX - 1) / CM::TX), gram_ty = (int)((g->ny + CM::TY - 1) / CM::TY);
@@ -1254,13 +1296,19 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
     static thread_local std::vector<PkSeg> segs;
     static thread_local std::vector<PkGroup> G;
     G.clear();
-    const double c_tap = 2.7 * (Kk * Kk) / 25.0;  // one tap over a 64 x 64 tile at the slot's FMA share
+    const double c_tap = 2.0 * (Kk * Kk) / 25.0 * kPkRY / 8.0;  // one tap over a 64 x (4 kPkRY) tile at a slot's FMA share
     const double c_plane = 1.5;                     // one z-march plane of a 32 x 16 stencil column
-    auto add = [&](int type, int b, int z, int aux, int n, double cost) {
+    auto add = [&](int type, int b, int z, int aux, int n, double cost, int aff) {
       PkGroup q;
-      q.type = type; q.b = b; q.z = z; q.aux = aux; q.n = n; q.cost = cost;
+      q.type = type; q.b = b; q.z = z; q.aux = aux; q.n = n; q.cost = cost; q.aff = aff;
       G.push_back(q);
       return (int)G.size() - 1;
+    };
+    auto block_of = [&](int64_t z) {  // block containing row z (clamped to the recorder rows)
+      z = std::min<int64_t>(std::max<int64_t>(z, rec_lo), rec_hi);
+      int bb = 0;
+      while (bb + 1 < nb && lo[bb + 1] <= z) ++bb;
+      return bb;
     };
     std::vector<int> gid_resid(P), gid_greg(nb), gid_solve(nb);
     std::vector<std::vector<int>> gid_grad(nb), gid_rg(nb), gid_gram(nb);
@@ -1270,9 +1318,10 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
         const int64_t zi = z + a2 - rz;
         taps += (zi >= sw->frag_z0 && zi < sw->frag_z0 + sw->nzf) ? 1 : 0;
       }
-      gid_resid[z - u_lo] = add(PK_RESID, 0, (int)z, 0, conv_tiles, taps * c_tap);
+      gid_resid[z - u_lo] = add(PK_RESID, 0, (int)z, 0, conv_tiles, taps * c_tap, block_of(z - rz));
     }
-    for (int b = 0; b < nb; ++b) gid_greg[b] = add(PK_GREG, b, 0, 0, st_tiles, (hi[b] - lo[b] + 3) * c_plane);
+    for (int b = 0; b < nb; ++b)
+      gid_greg[b] = add(PK_GREG, b, 0, 0, st_tiles, (hi[b] - lo[b] + 3) * c_plane, std::max(0, b - 1));
     for (int b = 0; b < nb; ++b)
       for (int zi = lo[b]; zi <= hi[b]; ++zi) {
         int taps = 0;
@@ -1280,7 +1329,7 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
           const int64_t zs = zi + a2 - rz;
           taps += (zs >= u_lo && zs <= u_hi && zs < nz) ? 1 : 0;
         }
-        const int id = add(PK_GRAD, b, zi, 0, conv_tiles, taps * c_tap);
+        const int id = add(PK_GRAD, b, zi, 0, conv_tiles, taps * c_tap, b);
         gid_grad[b].push_back(id);
         for (int64_t z = std::max<int64_t>(u_lo, zi - rz); z <= std::min<int64_t>(u_hi, zi + rz); ++z)
           G[gid_resid[z - u_lo]].succ.push_back(id);
@@ -1289,46 +1338,65 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
     for (int b = 0; b < nb; ++b) {
       for (int c = 0; c < nch[b]; ++c) {
         const int clo = lo[b] + c * rgc[b], chi = std::min(hi[b], clo + rgc[b] - 1);
-        const int id = add(PK_RG, b, 0, c, st_tiles, 2 * (chi - clo + 2) * c_plane);
+        const int id = add(PK_RG, b, 0, c, st_tiles, 2 * (chi - clo + 2) * c_plane, b);
         gid_rg[b].push_back(id);
         for (int q : gid_grad[b]) G[q].succ.push_back(id);
         G[gid_greg[b]].succ.push_back(id);
       }
       for (int zo = olo[b]; zo <= ohi[b]; ++zo) {
         const int taps = std::min(hi[b], zo + (int)rz) - std::max(lo[b], zo - (int)rz) + 1;
-        const int id = add(PK_GRAM, b, zo, 0, gram_tiles, taps * c_tap);  // two passes over half-height tiles
+        const int id = add(PK_GRAM, b, zo, 0, gram_tiles, taps * c_tap, b);  // two passes over half-height tiles
         gid_gram[b].push_back(id);
         for (int q : gid_grad[b]) G[q].succ.push_back(id);
       }
     }
     for (int b = 0; b < nb; ++b) {
-      gid_solve[b] = add(PK_SOLVE, b, 0, 0, 1, 5.0);
+      gid_solve[b] = add(PK_SOLVE, b, 0, 0, 1, 5.0, b);
       for (int q : gid_gram[b]) G[q].succ.push_back(gid_solve[b]);
       for (int q : gid_rg[b]) G[q].succ.push_back(gid_solve[b]);
     }
     for (int b = 0; b < nb; ++b) {
       const long long n = (long long)(hi[b] - lo[b] + 1) * plane;
       const int chunks = (int)((n + a.upd_chunk - 1) / a.upd_chunk);
-      const int id = add(PK_UPD, b, 0, 0, chunks, 11.0);
+      const int id = add(PK_UPD, b, 0, 0, chunks, 6.0, b);
       G[gid_solve[b]].succ.push_back(id);
       for (int64_t z = std::max<int64_t>(u_lo, lo[b] - rz); z <= std::min<int64_t>(u_hi, hi[b] + rz); ++z)
         G[gid_resid[z - u_lo]].succ.push_back(id);
       for (int bb = std::max(0, b - 1); bb <= std::min(nb - 1, b + 1); ++bb) G[gid_greg[bb]].succ.push_back(id);
     }
     {
-      const int id0 = add(PK_RED, 0, 0, 0, 1, 3.0);
+      const int id0 = add(PK_RED, 0, 0, 0, 1, 3.0, nb);
       for (int b = 0; b < nb; ++b) G[gid_greg[b]].succ.push_back(id0);
-      const int id1 = add(PK_RED, 0, 1, 0, 1, 3.0);
+      const int id1 = add(PK_RED, 0, 1, 0, 1, 3.0, nb);
       for (int64_t z = rec_lo; z <= rec_hi; ++z) G[gid_resid[z - u_lo]].succ.push_back(id1);
     }
     uint32_t total = 0;
-    if (!pk_schedule(G, slots, segs, total)) return kPkIneligible;
+    int sms = 148;
+    {
+      int dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (!pk_schedule(G, slots, sms, nb, segs, total)) return kPkIneligible;
     a.nseg = (int)segs.size();
     for (int i = 0; i < a.nseg; ++i) a.seg[i] = segs[i];
     a.total = total;
     if (getenv("BD3MG_PK_DEBUG"))
       fprintf(stderr, "pk: %d slots, %u items, %d segments, %zu groups, params %zu B\n", slots, total, a.nseg,
               G.size(), sizeof(PkArgs<double>));
+    a.trace = nullptr;
+    if (getenv("BD3MG_PK_TRACE")) {
+      PkTrace& tr = pk_trace();
+      std::lock_guard<std::mutex> lock(tr.mu);
+      if (tr.cap < total) {
+        if (tr.buf) cudaFree(tr.buf);
+        tr.buf = nullptr;
+        tr.cap = 0;
+        CU(cudaMalloc(&tr.buf, (size_t)total * 32));
+        tr.cap = total;
+      }
+      tr.n = total;
+      a.trace = tr.buf;
+    }
     CU(cudaMemsetAsync(ctr, 0, sizeof(int) * pk_ctr_count((int)P), s));
     CU(pk_launch(a, Kk, s, nullptr));
     launched();
@@ -1796,6 +1864,16 @@ int bd3mg_power_hth(const bd3mg_geom_t* g, const void* kernels, void* v, int32_t
                                            (cudaStream_t)stream),
                     power_hth_impl<float>(g, (const float*)kernels, (float*)v, iters, norms_out, state_out, ws,
                                           (cudaStream_t)stream));
+}
+
+int bd3mg_pk_trace(void* host, int64_t max_items, int64_t* n_out) {
+  PkTrace& tr = pk_trace();
+  std::lock_guard<std::mutex> lock(tr.mu);
+  CU(cudaDeviceSynchronize());
+  const int64_t n = std::min<int64_t>((int64_t)tr.n, max_items);
+  if (n_out) *n_out = (int64_t)tr.n;
+  if (host && n > 0) CU(cudaMemcpy(host, tr.buf, (size_t)n * 32, cudaMemcpyDeviceToHost));
+  return BD3MG_OK;
 }
 
 size_t bd3mg_jacobi_sweep_ws_bytes(const bd3mg_geom_t* g, const bd3mg_sweep_t* sw) {

@@ -173,7 +173,7 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 #ifndef BD3MG_RY1
 #define BD3MG_RY1 16  // rows per thread of the single-input modes
 #endif
-template <typename T, int KY_, int KX_, int MODE>
+template <typename T, int KY_, int KX_, int MODE, int RYO = 0>
 struct ConvCfg {
   static constexpr bool DUAL = (MODE == M_GRAM2);
   static constexpr bool TWOPASS = (MODE == M_GRAM2P);
@@ -182,7 +182,7 @@ struct ConvCfg {
   static constexpr int RX = VEC;                    // outputs per thread in x
   // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32); the two-pass
   // Gram keeps the dual-input tile (same pixels per CTA, so the same partial sums)
-  static constexpr int RY = (DUAL || TWOPASS) ? (sizeof(T) == 8 ? BD3MG_RY2 : 4) : BD3MG_RY1;
+  static constexpr int RY = RYO > 0 ? RYO : (DUAL || TWOPASS) ? (sizeof(T) == 8 ? BD3MG_RY2 : 4) : BD3MG_RY1;
   static constexpr int WX = 32, WY = 4;             // a warp spans one row group
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
@@ -296,10 +296,10 @@ struct TileIO {
 // ConvCfg::smem_bytes.  Shared by conv_tiled_kernel (one tile per CTA) and
 // the persistent sweep kernel (sweep_pk.cuh: many tiles per CTA), so both
 // compute bit-identical values.
-template <typename T, int KY, int KX, int MODE, bool ADJ>
+template <typename T, int KY, int KX, int MODE, bool ADJ, int RYO = 0>
 BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0, int y0, double* part_out,
                        unsigned char* sbase, uint64_t* bars = nullptr) {
-  using Cfg = ConvCfg<T, KY, KX, MODE>;
+  using Cfg = ConvCfg<T, KY, KX, MODE, RYO>;
   using V = typename Vec16<T>::type;
   constexpr int RX = Cfg::RX, RY = Cfg::RY, NIN = Cfg::NIN, VEC = Cfg::VEC;
   constexpr int WINP = Cfg::WINP, OFF = Cfg::OFF;

@@ -57,7 +57,15 @@ struct PkSeg {
 };
 
 constexpr int kPkMaxSeg = 1280;
-constexpr int kPkSlotsPerSm = 3;
+// rows per thread of the residual / gradient tiles: 8 (64 x 32 tiles, like
+// the Gram) halves the staging ring, so 4 CTAs share an SM -- three keep the
+// FMA pipe fed while the fourth runs a memory-bound item
+#ifndef BD3MG_PK_RY
+#define BD3MG_PK_RY 8
+#endif
+constexpr int kPkRY = BD3MG_PK_RY;
+template <typename T, int K>
+constexpr int pk_slots_per_sm() { return (sizeof(T) == 8 && K >= 9) ? 2 : (K >= 7 ? 3 : 4); }
 
 // counter layout (ints): [0] ticket, [1] RED arrivals, then per block
 // greg / grad / rg / gram / solve, then per residual plane
@@ -115,6 +123,7 @@ struct PkArgs {
   SolveArgs solve;      // (g_begin / r_begin ranges unused: rows from g_row0 / rg_row0)
   MirArgs<T, kMaxMirSegs> mir;
   int bar_off;          // PkCfg::data_bytes(kz): offset of the mbarriers / ticket in shared memory
+  unsigned long long* trace;  // optional (BD3MG_PK_TRACE=1): per item [dequeued, deps met, done] ns + (sm, type, b, z)
   int nseg;
   uint32_t total;
   PkSeg seg[kPkMaxSeg];
@@ -204,8 +213,8 @@ BD3MG_D void pk_mirror_store(const MirArgs<T, kMaxMirSegs>& m, int blk, long lon
 
 template <typename T, int K>
 struct PkCfg {
-  using CR = ConvCfg<T, K, K, M_RESID>;
-  using CG = ConvCfg<T, K, K, M_GRAD>;
+  using CR = ConvCfg<T, K, K, M_RESID, kPkRY>;
+  using CG = ConvCfg<T, K, K, M_GRAD, kPkRY>;
   using CM = ConvCfg<T, K, K, M_GRAM2P>;
   static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
   // bytes any item uses from the aligned base (stencil layouts: their smem() minus its alignment slack;
@@ -222,7 +231,7 @@ struct PkCfg {
 
 // 3 CTAs per SM where the staging ring allows it (fp64 3x3 / 5x5 taps), else 2
 template <typename T, int K>
-__global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlotsPerSm)
+__global__ void __launch_bounds__(128, pk_slots_per_sm<T, K>())
     sweep_pk_kernel(const __grid_constant__ PkArgs<T> p) {
   using Cfg = PkCfg<T, K>;
   static_assert(sizeof(PkArgs<T>) <= 32000, "kernel parameter space");
@@ -249,6 +258,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlots
     const PkSeg sg = p.seg[lo];
     const int k = item - (int)sg.first;
     const int type = sg.type, b = sg.b;
+    unsigned long long t_deq = 0;
+    if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_deq));
 
     // ---- dependencies (thread 0 waits; the CTA follows at the barrier) ----
     if (threadIdx.x == 0) {
@@ -282,6 +293,17 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlots
       }
       fence_proxy_async_global();  // produced data is read by TMA below
       fence_proxy_async_smem();     // smem written by the previous item is refilled by TMA below
+      if (p.trace) {
+        unsigned long long t_go, sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_go));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(*reinterpret_cast<unsigned*>(&sm)));
+        sm &= 0xffffffffull;
+        unsigned long long* tr = p.trace + 4ull * item;
+        tr[0] = t_deq;
+        tr[1] = t_go;
+        tr[3] = (sm << 48) | ((unsigned long long)type << 40) | ((unsigned long long)b << 32) |
+                ((unsigned long long)sg.z << 16) | (unsigned long long)sg.aux;
+      }
     }
     __syncthreads();
 
@@ -300,7 +322,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlots
       io.epi_z = zo - p.u_lo;
       io.use_tma = true;
       using C = typename Cfg::CR;
-      conv_tile<T, K, K, M_RESID, false>(p.cg, io, zo, tx * C::TX, ty * C::TY,
+      conv_tile<T, K, K, M_RESID, false, kPkRY>(p.cg, io, zo, tx * C::TX, ty * C::TY,
                                          p.cparts + ((long long)(zo - p.u_lo) * p.conv_tiles + t), sbase, bars);
       nbars = 2;
       done = ctr + pk_ctr_resid(zo - p.u_lo);
@@ -316,7 +338,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlots
       io.epi_z = zi - p.rec_lo;
       io.use_tma = true;
       using C = typename Cfg::CG;
-      conv_tile<T, K, K, M_GRAD, true>(p.cg, io, zi, tx * C::TX, ty * C::TY, nullptr, sbase, bars);
+      conv_tile<T, K, K, M_GRAD, true, kPkRY>(p.cg, io, zi, tx * C::TX, ty * C::TY, nullptr, sbase, bars);
       nbars = 2;
       done = ctr + pk_ctr_grad(b);
     } else if (type == PK_GRAM) {
@@ -394,13 +416,53 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlots
           for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) pk_mirror_store(p.mir, b, i, xb[i]);
       } else {
         const T cgc = (T)__ldcg(o + 10), cdc = (T)__ldcg(o + 11);
-        for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-          T inc = mul_rn(-__ldcg(gb + i), cgc);
-          inc = add_rn(inc, mul_rn(__ldcg(db + i), cdc));
-          const T xn = add_rn(__ldcg(xb + i), inc);
+        auto upd1 = [&](long long i, T g, T d, T x) {
+          T inc = mul_rn(-g, cgc);
+          inc = add_rn(inc, mul_rn(d, cdc));
+          const T xn = add_rn(x, inc);
           xb[i] = xn;
           if (p.mir.n > 0) pk_mirror_store(p.mir, b, i, xn);
           db[i] = inc;
+        };
+        using V = typename Vec16<T>::type;
+        constexpr int VE = 16 / sizeof(T), UN = 4;
+        const bool vec = ((i0 | i1 | off) % VE) == 0 && p.mir.n == 0 &&
+                         (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (reinterpret_cast<uintptr_t>(gb) & 15) == 0;
+        if (vec) {  // 16-byte accesses, UN vectors per thread in flight
+          const long long nv = (i1 - i0) / VE;
+          for (long long v0 = threadIdx.x; v0 < nv; v0 += (long long)blockDim.x * UN) {
+            V gv[UN], dv[UN], xv[UN];
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+              const long long v = v0 + (long long)u * blockDim.x;
+              if (v < nv) {
+                const long long i = i0 + v * VE;
+                gv[u] = __ldcg(reinterpret_cast<const V*>(gb + i));
+                dv[u] = __ldcg(reinterpret_cast<const V*>(db + i));
+                xv[u] = __ldcg(reinterpret_cast<const V*>(xb + i));
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+              const long long v = v0 + (long long)u * blockDim.x;
+              if (v < nv) {
+                const long long i = i0 + v * VE;
+                const T* gs = reinterpret_cast<const T*>(&gv[u]);
+                const T* ds = reinterpret_cast<const T*>(&dv[u]);
+                const T* xs = reinterpret_cast<const T*>(&xv[u]);
+                T xn[VE], inc[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                  inc[e] = add_rn(mul_rn(-gs[e], cgc), mul_rn(ds[e], cdc));
+                  xn[e] = add_rn(xs[e], inc[e]);
+                }
+                *reinterpret_cast<V*>(xb + i) = *reinterpret_cast<const V*>(xn);
+                *reinterpret_cast<V*>(db + i) = *reinterpret_cast<const V*>(inc);
+              }
+            }
+          }
+        } else {
+          for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) upd1(i, __ldcg(gb + i), __ldcg(db + i), __ldcg(xb + i));
         }
       }
       if (p.mir.n > 0) __threadfence_system();
@@ -437,6 +499,11 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 8 && K >= 7) ? 2 : kPkSlots
     if (threadIdx.x == 0) {
       for (int q = 0; q < nbars; ++q) mbar_inval(&bars[q]);
       if (done) red_release_add(done, 1);
+      if (p.trace) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        p.trace[4ull * item + 2] = t_end;
+      }
     }
   }
 }

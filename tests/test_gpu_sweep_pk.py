@@ -1,6 +1,7 @@
 """The persistent one-launch block-Jacobi sweep (csrc/sweep_pk.cuh) against
 the multi-kernel sweep it replaces (BD3MG_NO_PK=1): iterate, memory store,
 recorder terms and StepInfo must be BIT-identical after several sweeps --
+(opt-in with BD3MG_PK=1 while it is slower than the multi-kernel sweep) --
 both run the same tile functions with the same tile -> partial-row mapping
 and the same final reduction trees.  Covers every tuned tap width, ragged
 blocks and tiles, C1 / C2, fragments of a sharded layout with mirror
@@ -18,9 +19,9 @@ pytestmark = pytest.mark.gpu
 def _run(obj, x0, h, sweeps, pk: bool, graph=False):
     from paper_2002_02328_b200 import runtime
     if pk:
-        os.environ.pop("BD3MG_NO_PK", None)
+        os.environ["BD3MG_PK"] = "1"
     else:
-        os.environ["BD3MG_NO_PK"] = "1"
+        os.environ.pop("BD3MG_PK", None)
     try:
         eng = runtime.JacobiSweeper(obj, x0, h, torch.float64)
         eng.sweep()
@@ -33,7 +34,7 @@ def _run(obj, x0, h, sweeps, pk: bool, graph=False):
         torch.cuda.synchronize()
         return eng, terms
     finally:
-        os.environ.pop("BD3MG_NO_PK", None)
+        os.environ.pop("BD3MG_PK", None)
 
 
 def _problem(k, nx, ny, nz, seed, kz=None):
@@ -49,6 +50,10 @@ def _problem(k, nx, ny, nz, seed, kz=None):
 
 
 def _same(a, b):
+    """Iterate, memory store, snapshot and StepInfo bit for bit; recorder
+    terms bit for bit except the data term (and f): the persistent sweep's
+    residual tiles are 64 x 32 (4 CTAs per SM), so its sum of r^2 groups the
+    pixels differently."""
     ea, ta = a
     eb, tb = b
     assert torch.equal(ea.x, eb.x)
@@ -56,7 +61,8 @@ def _same(a, b):
     assert torch.equal(ea.snap, eb.snap)
     assert torch.equal(ea.info, eb.info)
     for u, v in zip(ta, tb):
-        assert torch.equal(u, v)
+        assert torch.equal(u[[1, 2, 3, 5, 6]], v[[1, 2, 3, 5, 6]])
+        torch.testing.assert_close(u[[0, 4]], v[[0, 4]], rtol=1e-13, atol=0)
 
 
 @pytest.mark.parametrize("k,nx,ny,nz,h", [(5, 64, 64, 24, 8), (3, 70, 45, 22, 4), (7, 64, 50, 40, 8),
@@ -99,9 +105,9 @@ def test_persistent_sweep_sharded_mirrors_bitwise(world):
     outs = []
     for pk in (True, False):
         if pk:
-            os.environ.pop("BD3MG_NO_PK", None)
+            os.environ["BD3MG_PK"] = "1"
         else:
-            os.environ["BD3MG_NO_PK"] = "1"
+            os.environ.pop("BD3MG_PK", None)
         try:
             shards = [ShardedJacobi(obj, x0, h, torch.float64, rank=r, world=world, halo="p2p") for r in range(world)]
             bases = {r: s.peer.ptr for r, s in enumerate(shards)}
@@ -115,7 +121,7 @@ def test_persistent_sweep_sharded_mirrors_bitwise(world):
             for s in shards:
                 s.close()
         finally:
-            os.environ.pop("BD3MG_NO_PK", None)
+            os.environ.pop("BD3MG_PK", None)
     assert torch.equal(outs[0], outs[1])
     single, _ = _run(obj, x0, h, 4, pk=True)
     assert torch.equal(outs[0], single.x)
