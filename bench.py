@@ -515,6 +515,9 @@ def main():
         if one_gpu:
             dist.init_process_group("gloo")
         else:
+            # communicator setup is logged (NCCL INFO, init subsystem) so the rank count can be checked
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
     cfg = bench_config(args, world)
     dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
@@ -605,6 +608,16 @@ def main():
         extra["roofline"], extra["operators"] = roofline(obj, cfg, dtype, torch, N, D, blur)
     if not args.quick:
         extra["e2e"] = e2e(obj, cfg, x0, args, world, rank, torch, N, D, eng)
+    if args.mode == "jacobi" and not args.quick and not one_gpu and os.environ.get("BD3MG_BENCH_NO_C5") != "1":
+        # north_star's scaling target: >= 0.8 efficiency at 8 GPUs on the LARGEST config, strong-scaled; the
+        # driver's SCALE run calls this script at N = 1, 2, 4, 8, so every line carries the C5-strong number
+        if world > 1:
+            dist.barrier()
+        if hasattr(eng, "close"):
+            eng.close()
+        del eng
+        torch.cuda.empty_cache()
+        extra["c5_strong"] = c5_strong(world, rank, dist, torch, args)
     if not args.quick and rank == 0 and world == 1:
         extra["variants"] = {"hd-cache": variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush),
                              "hd-incremental": variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur,
@@ -634,6 +647,77 @@ def main():
 
 
 # ---------------------------------------------------------------------------
+def c5_strong(world, rank, dist, torch, args, sweeps=3):
+    """BASELINE C5 (1024x1024x512 fp32, PSF 9x9x21, 8 blocks of 64 planes)
+    split over the N ranks (strong scaling: the same volume at every N), the
+    block-Jacobi sweep with update-kernel NVLink halo stores; 1 eager + 1
+    captured warm-up sweep, `sweeps` timed, max over ranks.  The inputs are
+    seeded synthetic fields built per rank for its local slab only (the
+    sweep's work does not depend on the values), so the setup stays seconds
+    at 2 GB per field."""
+    from paper_2002_02328_b200 import blur, configs, objective, runtime
+    cfg = configs.CONFIGS["C5"]
+    dims = cfg.dims
+    psf = blur.depth_variant_stack(dims, cfg.kdims, cfg.sigma_xy, cfg.sigma_z)
+    params = objective.RegParams(lam=cfg.lam, eta=cfg.eta, kappa=cfg.kappa, delta=cfg.delta)
+    nz = dims.nz
+    B = -(-nz // cfg.block_height)
+    y = np.zeros(dims.shape)  # lazily committed pages: only the local rows are touched below
+    x0 = np.zeros(dims.shape)
+    if world > 1:
+        from paper_2002_02328_b200.distributed import SlabLayout, ShardedJacobi
+        lay = SlabLayout.build(nz, cfg.kdims[2], cfg.block_height, world)
+        l_lo, l_hi = lay.local(rank)
+    else:
+        l_lo, l_hi = 0, nz - 1
+    rng = np.random.Generator(np.random.Philox(7 + rank))
+    for z0 in range(l_lo, l_hi + 1, 32):  # plane chunks: bounded temporaries
+        z1 = min(l_hi + 1, z0 + 32)
+        x0[z0:z1] = rng.random((z1 - z0,) + dims.shape[1:], dtype=np.float32)
+        y[z0:z1] = rng.random((z1 - z0,) + dims.shape[1:], dtype=np.float32)
+    obj = objective.Objective(psf, y, params)
+    if world > 1:
+        eng = ShardedJacobi(obj, x0, cfg.block_height, torch.float32, halo="p2p")
+    else:
+        eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, torch.float32)
+    del x0
+    eng.sweep()
+    eng.capture()
+    eng.sweep()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(sweeps):
+        eng.sweep()
+    b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = a.elapsed_time(b)
+    per_rank = [ms]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        allr = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allr, t)
+        per_rank = [float(v.item()) for v in allr]
+    t_max = max(per_rank)
+    eng.check()
+    fl = blur.flops_jacobi_sweep(dims, cfg.kdims, [runtime.scheduler.SliceBlock(lo, min(lo + cfg.block_height - 1,
+                                                                                          nz - 1))
+                                                   for lo in range(0, nz, cfg.block_height)])
+    if hasattr(eng, "close"):
+        eng.close()
+    return {"metric": "BD3MG block-iterations/sec (C5 1024x1024x512 fp32, PSF 9x9x21, 8 blocks x 64 planes, "
+                      "block-Jacobi sweeps, strong scaling)",
+            "value": sweeps * B / (t_max / 1e3), "unit": UNIT, "ms_per_step": t_max / sweeps, "steps": sweeps,
+            "warmup": 2, "scaling": "strong", "ranks": world, "per_rank_ms_per_step": [v / sweeps for v in per_rank],
+            "correlation_tflops": fl / (t_max / sweeps / 1e3) / 1e12,
+            "halo": "p2p update-kernel NVLink stores" if world > 1 else "none (one GPU)",
+            "data": "seeded uniform fields per local slab (throughput does not depend on the values)"}
+
+
 def variant_hd_cache(obj, cfg, x0, dtype, args, torch, runtime, blur, flush, incremental=False):
     """Secondary numbers: the "hd-cache" variant (H E_S d_mem kept from the
     previous visit; one forward correlation per Gram instead of two) and
