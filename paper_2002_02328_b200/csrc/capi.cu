@@ -596,7 +596,27 @@ struct StepOpts {
   T* r_full = nullptr;         // variant "hd-incremental": r = Hx - y kept across calls (plane 0 = r_full_z0)
   int64_t r_full_z0 = 0;
   bool r_refresh = false;      // recompute r_full exactly in this call
+  // recorder terms fused into the gradient correlation (M_GRADF): snapshot rows [rec_lo, rec_hi] (rolled)
+  // and the stencil sums written to rec_sums[0..4] (the sweep's sums + 1)
+  bool rec_gradf = false;
+  T* rec_snap = nullptr;
+  double* rec_sums = nullptr;
+  bool side_forked = false;    // the caller forked the side stream (ss->ev[0]) before this call
 };
+
+// The gradient correlation with the regulariser gradient fused into its
+// epilogue (M_GRADF: no separate stencil pass) where it exists: fp64, square
+// 3 / 5 / 7 / 9 taps, TMA-staged rows.
+template <typename T>
+bool gradf_ok(const bd3mg_geom_t* g) {
+  // opt-in (BD3MG_GRADF=1): correct and bitwise, but measured slower at C2 (445 vs 424 us per sweep): the
+  // epilogue's stencil math and L2 round trips sit on the correlation's critical path, while the separate
+  // stencil mostly overlaps the residual correlation on the side stream
+  const char* on = getenv("BD3MG_GRADF");
+  const bool off = getenv("BD3MG_NO_GRADF") != nullptr || !on || on[0] == '0';
+  return !off && sizeof(T) == 8 && g->kx == g->ky && (g->kx == 3 || g->kx == 5 || g->kx == 7 || g->kx == 9) &&
+         st_use_tma<T>(g->nx);
+}
 
 // Small stencil grids (one block of a cyclic / asynchronous step): each
 // block's z-march is cut into chunks of c planes so a block alone fills ~2
@@ -678,10 +698,12 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   }
   std::vector<T*> gb(nt), wb(nt), grb(nt);
   const bool pre = opt.greg != nullptr;
+  const bool gradf = gradf_ok<T>(g);  // regulariser gradient in the gradient correlation's epilogue
+  if (opt.rec_gradf && !gradf) return fail(BD3MG_EINVAL, "fused recorder needs the fused gradient");
   for (int t = 0; t < nt; ++t) {
     gb[t] = ws.take<T>(h[t] * plane);
-    wb[t] = pre ? opt.omega[t] : ws.take<T>(h[t] * plane);
-    grb[t] = pre ? opt.greg[t] : ws.take<T>(h[t] * plane);
+    wb[t] = (pre && opt.omega) ? opt.omega[t] : ws.take<T>(h[t] * plane);
+    grb[t] = pre ? opt.greg[t] : (gradf ? nullptr : ws.take<T>(h[t] * plane));
   }
   long long gram_work = 0;
   for (int t = 0; t < nt; ++t) gram_work += ohi[t] - olo[t] + 1;
@@ -715,6 +737,12 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   (void)gram_work;
   const long long conv_part_rows = std::max<long long>(std::max(resid_rows, gram_rows), kSumsqCtas);
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
+  double* rsq_parts = (opt.resid_sq && opt.ss) ? ws.take<double>((size_t)std::max<long long>(resid_rows, 1)) : nullptr;
+  bool rsq_forked = false;  // the residual's reduction goes to the side stream
+  std::pair<long long, long long> rsq_range{0, 0};
+  long long grad_rows = 0;  // recorder partial rows of the fused gradient (one per GRADF CTA)
+  for (int t = 0; t < nt; ++t) grad_rows += conv_rows<T>(g, M_GRAD, h[t]);
+  double* eparts_g = opt.rec_gradf ? ws.take<double>((size_t)grad_rows * kGradfNV) : nullptr;
   long long hsum = 0;
   for (int t = 0; t < nt; ++t) hsum += h[t];
   // one partial row per (job, tile); a z-chunked block is several jobs
@@ -746,7 +774,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   };
   // (0) block steps with a side stream (mg_steps): the regulariser gradient
   // needs x only, so it runs next to the residual correlation
-  const bool greg_side = opt.ss && !pre;
+  const bool greg_side = opt.ss && !pre && !gradf;
   if (greg_side) {
     CU(hop(s, opt.ss->side, opt.ss->ev[0]));
     int rc = greg_launch(opt.ss->side);
@@ -778,22 +806,36 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       j.dst0 = (shared ? rb[0] : rb[t]) + (rjobs[t].first - (shared ? u_lo : olo[t])) * plane;
       j.sub = y + rjobs[t].first * plane;
     }
+    // with a side stream the residual's partial rows get their own buffer and the recorder's reduction of
+    // them runs on the side stream, off the correlations' critical path (joined before the solve)
+    const bool rsq_side = opt.resid_sq && opt.ss && rec_job >= 0;
+    if (rsq_side) a.partials = rsq_parts;
     CU(conv_launch<T>(M_RESID, false, a, 0, s));
     launched();
     if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
       if (rec_job >= 0) {
         const long long tl = conv_tiles<T>(g, M_RESID);
         const long long b0 = (long long)a.jobs[rec_job].work_begin * tl;
-        CU(reduce(cparts, 1, {{b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)}}, opt.resid_sq, 1, s));
+        if (rsq_side) {  // enqueued below, after the side stream's stencil is joined
+          rsq_range = {b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)};
+          rsq_forked = true;
+        } else {
+          CU(reduce(cparts, 1, {{b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)}}, opt.resid_sq, 1, s));
+        }
       } else {
         CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
       }
     }
   }
-  // join the recorder / regulariser-gradient stencil of the side stream
-  if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
+  // join the recorder / regulariser-gradient stencil of the side stream (when one was forked: by the
+  // sweep before this call, or above)
+  if (opt.ss && (greg_side || opt.side_forked)) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
+  if (rsq_forked) {  // the recorder's data term next to the gradient correlation
+    CU(hop(s, opt.ss->side, opt.ss->ev[7]));
+    CU(reduce(rsq_parts, 1, {rsq_range}, opt.resid_sq, 1, opt.ss->side));
+  }
   // (2) regulariser gradient + omega (tiled stencil), then g = H^T r + it
-  if (!pre && !greg_side) {
+  if (!pre && !greg_side && !gradf) {
     int rc = greg_launch(s);
     if (rc) return rc;
   }
@@ -808,6 +850,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   const long long tl_reg = z_tiles<T>(g);
   std::vector<int> rg_begin(nt), rg_end(nt);  // regulariser-Gram jobs of each block
   int rg_jobs = 0;
+  long long grad_row0 = 0;  // first recorder row of the current part's fused-gradient launch
   if (parts == 2) CU(hop(s, opt.ss->side2, opt.ss->ev[4]));  // fork after RESID / greg
   for (int part = 0; part < parts; ++part) {
     const int t0 = part == 0 ? 0 : nt / 2, t1 = (parts == 1 || part == 1) ? nt : nt / 2;
@@ -821,9 +864,16 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
         j.src0 = rb[t]; j.src_z0 = r_z0[t]; j.src_nz = (int)r_n[t];
         j.dst0 = gb[t]; j.sub = grb[t];
         j.out_lo = (int)tasks[t].z_lo; j.nout = (int)h[t];
+        if (gradf) {  // regulariser gradient (+ recorder terms) from the iterate tile in the epilogue
+          j.xg = (const T*)tasks[t].frag; j.xg_z0 = tasks[t].frag_z0; j.xg_nz = (int)tasks[t].nzf;
+          j.omega = wb[t];
+          j.snap = (opt.rec_gradf && opt.rec_snap) ? opt.rec_snap + (tasks[t].z_lo - opt.rec_lo) * plane : nullptr;
+          j.eparts = opt.rec_gradf ? eparts_g + (size_t)grad_row0 * kGradfNV : nullptr;  // rows: this launch's CTAs
+        }
       }
-      CU(conv_launch<T>(M_GRAD, true, a, 0, sp));
+      CU(conv_launch<T>(gradf ? M_GRADF : M_GRAD, true, a, 0, sp));
       launched();
+      for (int t = t0; t < t1; ++t) grad_row0 += conv_rows<T>(g, M_GRAD, h[t]);
     }
     // regulariser Gram terms on the side stream, concurrent with the Gram correlation
     cudaStream_t s3 = sp;
@@ -885,6 +935,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   }
   if (parts == 2) CU(hop(opt.ss->side2, s, opt.ss->ev[6]));  // join the second chain
   if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[3]));  // join the side stream
+  if (opt.rec_gradf)  // the recorder's stencil sums from the fused gradient's partial rows
+    CU(reduce(eparts_g, kGradfNV, {{0, grad_rows}}, opt.rec_sums, kGradfNV, s));
   // (5)+(6) per-block reductions and the 2x2 solves, one CTA per block
   {
     SolveArgs sa;
@@ -1490,14 +1542,30 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   opt.fin_sums = sums;  // the update launch writes the recorder terms
   opt.fin_terms = terms;
 #endif
+  // recorder terms + snapshot roll fused into the gradient correlation (no stencil pass)
+  const bool rec_gradf = fused && gradf_ok<T>(g);
+  if (rec_gradf) {
+    opt.greg = nullptr;
+    opt.omega = nullptr;
+    opt.rec_gradf = true;
+    opt.rec_snap = (T*)sw->snap;
+    opt.rec_sums = sums + 1;
+  }
   SideStream* ss = nullptr;
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
-  if (!ws.measure) {
+  if (!ws.measure && rec_gradf) {
+    if (!ws.ok()) return ws_fail(ws);
+    if (!getenv("BD3MG_NO_SIDE_STREAM")) {
+      CU(side_stream(s, &ss));
+      opt.ss = ss;
+    }
+  } else if (!ws.measure) {
     if (!ws.ok()) return ws_fail(ws);
     if (fused && !getenv("BD3MG_NO_SIDE_STREAM")) {
       CU(side_stream(s, &ss));
       opt.ss = ss;
       CU(hop(s, ss->side, ss->ev[0]));  // fork: the stencil runs next to the residual correlation
+      opt.side_forked = true;
       s1 = ss->side;
     }
     // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll

@@ -93,6 +93,11 @@ cudaError_t launch_tiled(ConvArgs<T>& p, int total_work, cudaStream_t s) {
     if (ok && Cfg::NIN == 2) ok = encode_tmap(&jb.tmap1, jb.src1, f64, p.nx, p.ny, jb.src_nz, Cfg::PITCH, Cfg::BOXH);
     jb.use_tma = (ok && !no_tma) ? 1 : 0;
     jb.epi_tma = 0;
+    if constexpr (MODE == M_GRADF) {  // the iterate tile with its halo: same box as the taps
+      if (!jb.use_tma || !jb.xg || !encode_tmap(&jb.tmap1, jb.xg, f64, p.nx, p.ny, jb.xg_nz, Cfg::PITCH, Cfg::BOXH))
+        return cudaErrorInvalidValue;  // the fused regulariser gradient needs TMA staging
+      jb.epi_tma = 1;
+    }
     if constexpr ((MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC) && Cfg::NIN == 1 && sizeof(T) == 8) {
       static const bool no_epi = getenv("BD3MG_NO_EPI_TMA") != nullptr;
       if (jb.use_tma && jb.sub && !no_epi)

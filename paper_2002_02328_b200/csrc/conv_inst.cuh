@@ -44,6 +44,17 @@ cudaError_t conv_launch(int mode, bool adj, ConvArgs<T>& p, int total_work, cuda
   switch (mode) {
     case M_STORE: return launch_mode<T, M_STORE, true>(p, total_work, s);
     case M_GRAD: return launch_mode<T, M_GRAD, true>(p, total_work, s);
+    case M_GRADF:  // fp64 tiled shapes only (the caller checks conv_gradf_ok)
+      if constexpr (sizeof(T) == 8) {
+        switch (p.ky == p.kx ? p.ky : 0) {
+          case 3: return launch_tiled<T, 3, M_GRADF, true>(p, total_work, s);
+          case 5: return launch_tiled<T, 5, M_GRADF, true>(p, total_work, s);
+          case 7: return launch_tiled<T, 7, M_GRADF, true>(p, total_work, s);
+          case 9: return launch_tiled<T, 9, M_GRADF, true>(p, total_work, s);
+          default: return cudaErrorInvalidValue;
+        }
+      }
+      return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }
 }

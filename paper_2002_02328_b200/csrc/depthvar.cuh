@@ -42,6 +42,9 @@ enum ConvMode : int {
   M_GRAMC = 5,  // dst0 = acc0 (H E_S g); partial: acc0^2, acc0*c, c^2 with c = sub[o] (cached H E_S d)
   M_GRAM2P = 6, // M_GRAM2 as two single-input passes over one tile ring (input 1, then input 0):
                 // the same tile, sums and partials bit for bit, half the staging smem
+  M_GRADF = 7,  // (adjoint) dst0 = acc + greg with the regulariser gradient computed in the epilogue from
+                // the iterate tile (TMA-staged into the freed ring buffer): greg_tile's arithmetic, omega
+                // stored, optionally the recorder terms + snapshot roll (no separate stencil pass)
 };
 
 constexpr int kMaxJobs = 32;
@@ -54,8 +57,10 @@ struct alignas(64) ConvJob {
   const T* src1;        // second fragment (M_GRAM2), same geometry
   T* dst0;              // output rows; row 0 is global depth out_lo
   const T* sub;         // M_RESID: rows aligned with dst0
-  const T* xg;          // M_GRAD: iterate fragment (plane 0 = depth xg_z0)
-  T* omega;             // M_GRAD: rows aligned with dst0
+  const T* xg;          // M_GRADF: iterate fragment (plane 0 = depth xg_z0, xg_nz planes; tmap1 maps it)
+  T* omega;             // M_GRADF: omega rows aligned with dst0
+  T* snap;              // M_GRADF: recorder snapshot rows aligned with dst0 (rolled), or null
+  double* eparts;       // M_GRADF: recorder partial rows (one per CTA, kEvalNV), or null (no recorder)
   long long src_z0;
   long long xg_z0;
   int src_nz, xg_nz;
@@ -76,6 +81,7 @@ struct ConvGeom {
   int ny, nx;
   long long plane;      // ny*nx
   int nz_global;        // global depth (axial far-face rule)
+  double two_eta, lam, two_kappa, delta2, x_min, x_max;  // regulariser (M_GRADF epilogue)
 };
 
 template <typename T>
@@ -84,7 +90,6 @@ struct ConvArgs : ConvGeom<T> {
   int tiles_x, tiles_y;
   int raster_group;     // tiles per rasterisation group (0: plain x, y, z order); see cta_pos
   double* partials;     // [gridDim.z * tiles_y * tiles_x][NV]
-  double two_eta, lam, two_kappa, delta2, x_min, x_max;
   const double* gate;   // optional: the launch is a no-op while *gate != 0 (device-side loops, krylov.cuh)
   ConvJob<T> jobs[kMaxJobs];
 };
@@ -173,6 +178,11 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 #ifndef BD3MG_RY1
 #define BD3MG_RY1 16  // rows per thread of the single-input modes
 #endif
+#ifndef BD3MG_WY1
+#define BD3MG_WY1 4   // warps per CTA of the single-input modes (tile height WY1 * RY1); measured on B200
+                      // at C2: 8 warps x 8 rows (same 64 x 64 tile) ran H in 99.5-117 us against 80 us
+#endif
+
 template <typename T, int KY_, int KX_, int MODE, int RYO = 0>
 struct ConvCfg {
   static constexpr bool DUAL = (MODE == M_GRAM2);
@@ -183,7 +193,8 @@ struct ConvCfg {
   // outputs per thread in y; dual-input rows measured on B200: 8 (fp64), 4 (fp32); the two-pass
   // Gram keeps the dual-input tile (same pixels per CTA, so the same partial sums)
   static constexpr int RY = RYO > 0 ? RYO : (DUAL || TWOPASS) ? (sizeof(T) == 8 ? BD3MG_RY2 : 4) : BD3MG_RY1;
-  static constexpr int WX = 32, WY = 4;             // a warp spans one row group
+  static constexpr int WX = 32;                     // a warp spans one row group
+  static constexpr int WY = (DUAL || TWOPASS || RYO > 0) ? 4 : BD3MG_WY1;  // warps per CTA
   static constexpr int NT = WX * WY;
   static constexpr int TX = WX * RX, TY = WY * RY;
   // TMA boxes must start on a 16-byte boundary in x (measured: odd-element
@@ -284,10 +295,181 @@ struct TileIO {
   TileSrc<T> in0, in1;          // in1: second input (M_GRAM2; M_GRAM2P runs it as the first pass)
   T* dst;                       // output plane (row y at dst + y*nx), or null
   const T* sub;                 // epilogue operand plane, same alignment, or null
-  const CUtensorMap* tm_epi;    // epilogue operand TMA (TX x TY box at (x0, y0, epi_z)), or null
+  const CUtensorMap* tm_epi;    // epilogue operand TMA (TX x TY box at (x0, y0, epi_z)), or null;
+                                //   M_GRADF: the iterate map (correlation box, halo origin)
   int epi_z;
   bool use_tma;
+  // M_GRADF: iterate fragment (axial neighbours read through L2), outputs
+  const T* xf;
+  long long xf_z0;
+  int xf_nz;
+  T* omega;                     // omega plane (row y at omega + y*nx)
+  T* snap;                      // snapshot plane or null
+  double* epart;                // recorder partials (kEvalNV) or null
 };
+
+constexpr int kGradfNV = 5;     // recorder sums of M_GRADF: box, tv, axial, |x-snap|^2, |snap|^2
+
+// M_GRADF epilogue: g = H^T r + greg for the thread's RY x RX outputs, with
+// greg computed here from the staged iterate tile xt (plane zo, origin
+// (x0 - RXA, y0 - RYH), pitch PITCH) exactly as greg_tile computes it
+// (stencil_tma.cuh; reference objective.py:130-137, :175-186): omega, the
+// weighted differences, their adjoints (left / upper neighbours by a lane
+// shuffle, the warp above through shared memory, the tile edges from the
+// halo), the box and axial terms (planes zo -+ 1 through L2).  Optionally the
+// recorder terms of eval_f and the snapshot roll.
+template <typename T, typename Cfg>
+BD3MG_D void gradf_epilogue(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0, int y0, const T* xt,
+                            T (&acc)[Cfg::RY][Cfg::RX], double* red_s, T* scratch) {
+  using V = typename Vec16<T>::type;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, RXA = Cfg::RXA, RYH = Cfg::RYH, PITCH = Cfg::PITCH;
+  constexpr int TX = Cfg::TX;
+  static_assert(RX == Cfg::VEC, "one 16-byte vector per thread row");
+  const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
+  const int lane = threadIdx.x & 31;
+  const int nx = p.nx, ny = p.ny;
+  const T d2 = (T)p.delta2, two_eta = (T)p.two_eta, lam = (T)p.lam, two_kappa = (T)p.two_kappa;
+  const T xmin = (T)p.x_min, xmax = (T)p.x_max;
+  auto X = [&](int ly, int lx) { return xt[(ly + RYH) * PITCH + lx + RXA]; };
+  // omega / weighted differences at tile-local (ly, lx); zero outside the volume (greg_tile's halo rule)
+  auto wxy = [&](int ly, int lx, T& w, T& px, T& py, T& sq) {
+    const int y = y0 + ly, x = x0 + lx;
+    const T c = X(ly, lx);
+    const T dx = (x < nx - 1) ? sub_rn(X(ly, lx + 1), c) : T(0);
+    const T dy = (y < ny - 1) ? sub_rn(X(ly + 1, lx), c) : T(0);
+    sq = add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), d2);
+    w = rsqrt(sq);
+    px = mul_rn(w, dx);
+    py = mul_rn(w, dy);
+  };
+  auto in_vol = [&](int ly, int lx) {
+    const int y = y0 + ly, x = x0 + lx;
+    return y >= 0 && x >= 0 && y < ny && x < nx;
+  };
+  // py of the row above each warp's first row: the warp above's last row (shared memory) or the halo row
+  // (scratch: the other ring buffer, free after the tap walk)
+  T (*s_lastpy)[TX] = reinterpret_cast<T (*)[TX]>(scratch);
+  {
+    const int lyl = ty * RY + RY - 1;
+#pragma unroll
+    for (int i = 0; i < RX; ++i) {
+      T w, px, py, sq;
+      wxy(lyl, tx * RX + i, w, px, py, sq);
+      s_lastpy[ty][tx * RX + i] = py;
+    }
+  }
+  __syncthreads();
+  const long long plane = p.plane;
+  const bool has_m = zo >= 1, has_p = zo < p.nz_global - 1;
+  const T* xm_p = has_m ? io.xf + (long long)(zo - 1 - io.xf_z0) * plane : nullptr;
+  const T* xp_p = has_p ? io.xf + (long long)(zo + 1 - io.xf_z0) * plane : nullptr;
+  double ev[kGradfNV] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const bool eval = io.epart != nullptr;
+  T pym[RX];
+#pragma unroll
+  for (int i = 0; i < RX; ++i) {
+    const int lx = tx * RX + i;
+    if (ty > 0) {
+      pym[i] = s_lastpy[ty - 1][lx];
+    } else {
+      T w, px, py, sq;
+      py = T(0);
+      if (in_vol(-1, lx)) wxy(-1, lx, w, px, py, sq);
+      pym[i] = py;
+    }
+  }
+  const int xt0 = x0 + tx * RX;
+  const bool vec_row = (nx % RX) == 0 && xt0 + RX <= nx;
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int ly = ty * RY + r, y = y0 + ly;
+    T w[RX], px[RX], py[RX], sq[RX];
+#pragma unroll
+    for (int i = 0; i < RX; ++i) wxy(ly, tx * RX + i, w[i], px[i], py[i], sq[i]);
+    // left neighbour's weighted x-difference: lane - 1 (every lane shuffles), lane 0 from the halo
+    T pxl = __shfl_up_sync(0xffffffffu, px[RX - 1], 1);
+    if (lane == 0) {
+      T ww, pxx, pyy, sqq;
+      pxx = T(0);
+      if (in_vol(ly, tx * RX - 1)) wxy(ly, tx * RX - 1, ww, pxx, pyy, sqq);
+      pxl = pxx;
+    }
+    const long long o = (long long)y * nx + xt0;
+    T xm[RX], xp[RX], sn[RX];
+    if (y < ny) {
+      if (vec_row) {
+        if (has_m) { const V v = __ldcg(reinterpret_cast<const V*>(xm_p + o)); const T* q = reinterpret_cast<const T*>(&v);
+#pragma unroll
+          for (int i = 0; i < RX; ++i) xm[i] = q[i]; }
+        if (has_p) { const V v = __ldcg(reinterpret_cast<const V*>(xp_p + o)); const T* q = reinterpret_cast<const T*>(&v);
+#pragma unroll
+          for (int i = 0; i < RX; ++i) xp[i] = q[i]; }
+        if (eval && io.snap) { const V v = __ldcg(reinterpret_cast<const V*>(io.snap + o)); const T* q = reinterpret_cast<const T*>(&v);
+#pragma unroll
+          for (int i = 0; i < RX; ++i) sn[i] = q[i]; }
+      } else {
+#pragma unroll
+        for (int i = 0; i < RX; ++i) {
+          const bool in = xt0 + i < nx;
+          xm[i] = (has_m && in) ? __ldcg(xm_p + o + i) : T(0);
+          xp[i] = (has_p && in) ? __ldcg(xp_p + o + i) : T(0);
+          sn[i] = (eval && io.snap && in) ? __ldcg(io.snap + o + i) : T(0);
+        }
+      }
+    }
+    T gout[RX], wout[RX], xout[RX];
+#pragma unroll
+    for (int i = 0; i < RX; ++i) {
+      const int lx = tx * RX + i, x = x0 + lx;
+      const T pxm = (i > 0) ? px[i - 1] : pxl;
+      const T xc = X(ly, lx);
+      const T clipped = xc < xmin ? xmin : (xc > xmax ? xmax : xc);
+      const T box = mul_rn(two_eta, sub_rn(xc, clipped));
+      const T tvx = (nx == 1) ? T(0) : sub_rn(pxm, px[i]);
+      const T tvy = (ny == 1) ? T(0) : sub_rn(pym[i], py[i]);
+      const T xzp = has_p ? xp[i] : T(0);
+      const T dzm = has_m ? sub_rn(xc, xm[i]) : T(0);
+      const T dzp = has_p ? sub_rn(xzp, xc) : T(0);
+      const T greg = add_rn(add_rn(box, mul_rn(lam, add_rn(tvx, tvy))), mul_rn(two_kappa, sub_rn(dzm, dzp)));
+      gout[i] = add_rn(acc[r][i], greg);
+      wout[i] = w[i];
+      xout[i] = xc;
+      if (eval && y < ny && x < nx) {
+        const double e = (double)xc - (double)clipped;
+        ev[0] += e * e;
+        ev[1] += (double)sq[i] * (double)w[i];
+        if (has_p) ev[2] += ((double)xzp - (double)xc) * ((double)xzp - (double)xc);
+        if (io.snap) {
+          ev[3] += ((double)xc - (double)sn[i]) * ((double)xc - (double)sn[i]);
+          ev[4] += (double)sn[i] * (double)sn[i];
+        }
+      }
+      pym[i] = py[i];
+    }
+    if (y < ny) {
+      if (vec_row) {
+        *reinterpret_cast<V*>(io.dst + o) = *reinterpret_cast<const V*>(gout);
+        *reinterpret_cast<V*>(io.omega + o) = *reinterpret_cast<const V*>(wout);
+        if (eval && io.snap) *reinterpret_cast<V*>(io.snap + o) = *reinterpret_cast<const V*>(xout);
+      } else {
+#pragma unroll
+        for (int i = 0; i < RX; ++i)
+          if (xt0 + i < nx) {
+            io.dst[o + i] = gout[i];
+            io.omega[o + i] = wout[i];
+            if (eval && io.snap) io.snap[o + i] = xout[i];
+          }
+      }
+    }
+  }
+  if (eval) {
+    cta_reduce<kGradfNV, Cfg::NT>(ev, red_s);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < kGradfNV; ++k) io.epart[k] = ev[k];
+    }
+  }
+}
 
 // One TY x TX output tile of output plane zo: the kz-tap walk over the staged
 // input planes (double-buffered TMA ring, mbarrier completion), the register-
@@ -375,16 +557,26 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
   // RESID / GRAD: the epilogue operand tile (y rows or the regulariser
   // gradient) is loaded by TMA into the tile buffer the last tap plane frees,
   // while that plane computes; the epilogue then reads it from shared memory
-  constexpr bool kEpiTma = (MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC) && NIN == 1 && sizeof(T) == 8;
-  const bool epi_tma = kEpiTma && tma && io.tm_epi != nullptr && nstep > 0;
+  constexpr bool kEpiTma =
+      (MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC || MODE == M_GRADF) && NIN == 1 && sizeof(T) == 8;
+  const bool epi_tma = kEpiTma && tma && io.tm_epi != nullptr && (nstep > 0 || MODE == M_GRADF);
+  if (MODE == M_GRADF && nstep == 0 && epi_tma && threadIdx.x == 0) {  // no tap in range: stage the iterate now
+    mbar_expect_tx(&mbar[1], (uint32_t)Cfg::BOX_BYTES);
+    tma_load_3d(tiles + 1 * NIN * Cfg::TILE, io.tm_epi, x0 - RXA, y0 - RYH, io.epi_z, &mbar[1]);
+  }
   uint32_t phase = 0;  // bit b = parity of buffer b
   int buf = 0;
   for (int st = 0; st < nstep; ++st) {
     if (st < nstep - 1) {
       issue(st + 1, buf ^ 1);
     } else if (epi_tma && threadIdx.x == 0) {
-      mbar_expect_tx(&mbar[buf ^ 1], (uint32_t)(Cfg::TX * Cfg::TY * sizeof(T)));
-      tma_load_3d(tiles + (buf ^ 1) * NIN * Cfg::TILE, io.tm_epi, x0, y0, io.epi_z, &mbar[buf ^ 1]);
+      if constexpr (MODE == M_GRADF) {  // the iterate plane zo with its halo (same box as the taps)
+        mbar_expect_tx(&mbar[buf ^ 1], (uint32_t)Cfg::BOX_BYTES);
+        tma_load_3d(tiles + (buf ^ 1) * NIN * Cfg::TILE, io.tm_epi, x0 - RXA, y0 - RYH, io.epi_z, &mbar[buf ^ 1]);
+      } else {
+        mbar_expect_tx(&mbar[buf ^ 1], (uint32_t)(Cfg::TX * Cfg::TY * sizeof(T)));
+        tma_load_3d(tiles + (buf ^ 1) * NIN * Cfg::TILE, io.tm_epi, x0, y0, io.epi_z, &mbar[buf ^ 1]);
+      }
     }
     if constexpr (kEpiLoad) {
       if (st == s_pf && vec_io && io.sub && threadIdx.x < Cfg::TY) {
@@ -451,6 +643,10 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
   // ---- epilogue -----------------------------------------------------------
   const T* etile = tiles + buf * NIN * Cfg::TILE;  // the buffer the last plane left free
   if (epi_tma) mbar_wait(&mbar[buf], (phase >> buf) & 1u);
+  if constexpr (MODE == M_GRADF) {
+    gradf_epilogue<T, Cfg>(p, io, zo, x0, y0, etile, acc[0], red_s, tiles + (buf ^ 1) * NIN * Cfg::TILE);
+    return;
+  }
   constexpr int NV = Cfg::NV;
   double part[NV > 0 ? NV : 1];
 #pragma unroll
@@ -560,6 +756,14 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
   io.tm_epi = job.epi_tma ? &job.tmap1 : nullptr;
   io.epi_z = zo - job.out_lo;
   io.use_tma = job.use_tma != 0;
+  io.xf = nullptr; io.xf_z0 = 0; io.xf_nz = 0; io.omega = nullptr; io.snap = nullptr; io.epart = nullptr;
+  if constexpr (MODE == M_GRADF) {
+    io.epi_z = (int)(zo - job.xg_z0);  // the iterate map (tmap1) spans the fragment xg
+    io.xf = job.xg; io.xf_z0 = job.xg_z0; io.xf_nz = job.xg_nz;
+    io.omega = job.omega + orow;
+    io.snap = job.snap ? job.snap + orow : nullptr;
+    io.epart = job.eparts ? job.eparts + pos.cta * kGradfNV : nullptr;
+  }
   constexpr int NV = Cfg::NV;
   conv_tile<T, KY, KX, MODE, ADJ>(p, io, zo, pos.tx * Cfg::TX, pos.ty * Cfg::TY,
                                   NV > 0 ? p.partials + pos.cta * NV : nullptr, sbase);

@@ -64,8 +64,14 @@ constexpr int kPkMaxSeg = 1280;
 #define BD3MG_PK_RY 8
 #endif
 constexpr int kPkRY = BD3MG_PK_RY;
+// 4 slots cap the registers at 128 and the kernel then spills; measured on
+// B200: spilled values were corrupted across items (tests/test_gpu_sweep_pk.py
+// fails at 4, passes at 3), so 3 is the default
+#ifndef BD3MG_PK_SLOTS
+#define BD3MG_PK_SLOTS 3
+#endif
 template <typename T, int K>
-constexpr int pk_slots_per_sm() { return (sizeof(T) == 8 && K >= 9) ? 2 : (K >= 7 ? 3 : 4); }
+constexpr int pk_slots_per_sm() { return (sizeof(T) == 8 && K >= 9) ? 2 : (K >= 7 ? 3 : BD3MG_PK_SLOTS); }
 
 // counter layout (ints): [0] ticket, [1] RED arrivals, then per block
 // greg / grad / rg / gram / solve, then per residual plane
