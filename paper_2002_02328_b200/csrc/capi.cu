@@ -737,7 +737,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   (void)gram_work;
   const long long conv_part_rows = std::max<long long>(std::max(resid_rows, gram_rows), kSumsqCtas);
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
-  double* rsq_parts = (opt.resid_sq && opt.ss) ? ws.take<double>((size_t)std::max<long long>(resid_rows, 1)) : nullptr;
+  // (sized whether or not a side stream is used: workspace sizing runs without one)
+  double* rsq_parts = opt.resid_sq ? ws.take<double>((size_t)std::max<long long>(resid_rows, 1)) : nullptr;
   bool rsq_forked = false;  // the residual's reduction goes to the side stream
   std::pair<long long, long long> rsq_range{0, 0};
   long long grad_rows = 0;  // recorder partial rows of the fused gradient (one per GRADF CTA)
