@@ -887,8 +887,20 @@ def roofline(obj, cfg, dtype, torch, N, D, blur):
         traffic = json.load(open(ROOT / "profiles" / "ncu_traffic.json"))[cfg.name]["traffic_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         pass
-    roof = {"bound": "fp64_fma" if dtype == torch.float64 else "fp32_fma", "kernel": "conv_tiled_kernel (H, full volume)",
+    # nominal FMA-pipe peak at the sampled max SM clock: 148 SMs x {64 DFMA | 128 FFMA} x 2 flop x f_max
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    f_max = None
+    try:
+        f_max = json.load(open(ROOT / "MEASURED_PEAKS.json"))["sm_max_mhz"] * 1e6
+    except (OSError, KeyError, ValueError):
+        f_max = 1.965e9
+    nominal = sms * (64 if dtype == torch.float64 else 128) * 2 * f_max / 1e12
+    kname = "conv_tiled_kernel" if dtype == torch.float64 else "conv_rz2_kernel (two output planes, FFMA2)"
+    roof = {"bound": "fp64_fma" if dtype == torch.float64 else "fp32_fma", "kernel": f"{kname} (H, full volume)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_nominal": nominal, "frac_nominal": achieved / nominal,
+            "peak_nominal_source": f"{sms} SMs x {64 if dtype == torch.float64 else 128} FMA/clk x 2 x "
+                                   f"{f_max / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
             "peak_source": "measured: bd3mg_fma_probe (dense FMA chains) on this GPU, this run "
                            "(MEASURED_PEAKS.json has no FP64/FP32 entry)",
             "bound_note": "FMA-pipe bound, not hbm/tensor: the depth-variant correlation is a direct convolution "

@@ -116,3 +116,31 @@ def test_pipelined_session_sweep_bitwise(h, pinned, dt):
         np.testing.assert_allclose(terms[:5], ref[:5], rtol=1e-13 if dt == "f64" else 1e-6)
     assert np.array_equal(x, eng.x.double().cpu().numpy())
     hp.close()
+
+
+def test_host_handle_serialises_concurrent_worker_threads(c1obj):
+    """The reference's live engine calls its core from several worker
+    threads at once (runtime.py:188-200).  Calls on one HostProblem handle
+    share its stream and buffers, so the library serialises them (per-handle
+    mutex): 8 threads x 6 calls each must give exactly the sequential
+    results (concurrent calls used to race on the uploads)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2002_02328_b200 import blur
+    from paper_2002_02328_b200.host import HostProblem
+    from paper_2002_02328_b200.volume import SliceBlock
+    obj, x0, cfg = c1obj
+    hp = HostProblem(obj)
+    rng = np.random.default_rng(7)
+    jobs = []
+    for i in range(48):
+        blk = (SliceBlock(0, 7), SliceBlock(8, 15), SliceBlock(16, 23))[i % 3]
+        s = blur.slab_support(obj.psf, blk)
+        xs = x0[s.z_lo:s.z_hi + 1] * (1.0 + 0.01 * i)
+        jobs.append((xs, s.z_lo, blk, 0.01 * rng.standard_normal(blk.count(obj.dims))))
+    want = [hp.mg_direction(*j) for j in jobs]
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        got = list(pool.map(lambda j: hp.mg_direction(*j), jobs))
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+    hp.close()
