@@ -179,6 +179,9 @@ int bd3mg_cg_solve(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const void* kern
  * block << 32 | z << 16 | aux).  Copies the last sweep's records (after a
  * device synchronise); *n_out = items of that sweep. */
 int bd3mg_pk_trace(void* host, int64_t max_items, int64_t* n_out);
+/* Persistent sweeps launched in this process (BD3MG_PK=1 selects them where
+ * they apply; otherwise the multi-kernel sweep runs, with the same results). */
+long long bd3mg_pk_launches(void);
 
 /* `iters` power-iteration steps on H^T H over the full volume (reference
  * objective.py:358-366): v <- H^T H v / |H^T H v| in place; norms_out

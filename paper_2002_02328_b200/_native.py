@@ -29,6 +29,7 @@ EXPORTS = (
     "bd3mg_eval_f_ws_bytes", "bd3mg_eval_f", "bd3mg_eval_rows_ws_bytes", "bd3mg_eval_rows",
     "bd3mg_omega_rows", "bd3mg_majorant_apply_ws_bytes", "bd3mg_majorant_apply",
     "bd3mg_cg_solve_ws_bytes", "bd3mg_cg_solve", "bd3mg_power_hth_ws_bytes", "bd3mg_power_hth", "bd3mg_pk_trace",
+    "bd3mg_pk_launches",
     "bd3mg_mg_steps_ws_bytes", "bd3mg_mg_steps", "bd3mg_apply_increment",
     "bd3mg_jacobi_sweep_ws_bytes", "bd3mg_jacobi_cache_elems", "bd3mg_jacobi_sweep",
     "bd3mg_jacobi_sweep_mirrored", "bd3mg_jacobi_sweep_incremental", "bd3mg_mg_steps_incremental_ws_bytes",
@@ -120,6 +121,7 @@ def _load() -> C.CDLL:
     lib.bd3mg_cg_solve_ws_bytes.restype = _sz
     lib.bd3mg_cg_solve.argtypes = [G, R, _vp, _vp, _vp, _i64, _i64, C.c_double, C.c_int32, _vp, _vp, _vp, _sz, _vp]
     lib.bd3mg_pk_trace.argtypes = [_vp, _i64, C.POINTER(C.c_int64)]
+    lib.bd3mg_pk_launches.restype = C.c_longlong
     lib.bd3mg_power_hth_ws_bytes.argtypes = [G]
     lib.bd3mg_power_hth_ws_bytes.restype = _sz
     lib.bd3mg_power_hth.argtypes = [G, _vp, _vp, C.c_int32, _vp, _vp, _vp, _sz, _vp]

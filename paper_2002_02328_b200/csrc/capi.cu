@@ -1106,6 +1106,7 @@ PkTrace& pk_trace() {
   static PkTrace t;
   return t;
 }
+std::atomic<long long> g_pk_launches{0};  // persistent sweeps launched (bd3mg_pk_launches)
 
 struct PkGroup {
   int type, b, z, aux;
@@ -1453,6 +1454,7 @@ int pk_sweep(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, const T* y
     CU(cudaMemsetAsync(ctr, 0, sizeof(int) * pk_ctr_count((int)P), s));
     CU(pk_launch(a, Kk, s, nullptr));
     launched();
+    g_pk_launches.fetch_add(1);
     return BD3MG_OK;
   }
 }
@@ -1934,6 +1936,8 @@ int bd3mg_power_hth(const bd3mg_geom_t* g, const void* kernels, void* v, int32_t
                     power_hth_impl<float>(g, (const float*)kernels, (float*)v, iters, norms_out, state_out, ws,
                                           (cudaStream_t)stream));
 }
+
+long long bd3mg_pk_launches(void) { return g_pk_launches.load(); }
 
 int bd3mg_pk_trace(void* host, int64_t max_items, int64_t* n_out) {
   PkTrace& tr = pk_trace();

@@ -56,7 +56,7 @@ struct PkSeg {
   uint8_t type, b;
 };
 
-constexpr int kPkMaxSeg = 1280;
+constexpr int kPkMaxSeg = 1700;
 // rows per thread of the residual / gradient tiles: 8 (64 x 32 tiles, like
 // the Gram) halves the staging ring, so 4 CTAs share an SM -- three keep the
 // FMA pipe fed while the fourth runs a memory-bound item

@@ -22,9 +22,12 @@ def _run(obj, x0, h, sweeps, pk: bool, graph=False):
         os.environ["BD3MG_PK"] = "1"
     else:
         os.environ.pop("BD3MG_PK", None)
+    from paper_2002_02328_b200 import _native as N
+    n0 = N.lib.bd3mg_pk_launches()
     try:
         eng = runtime.JacobiSweeper(obj, x0, h, torch.float64)
         eng.sweep()
+        assert (N.lib.bd3mg_pk_launches() > n0) == pk  # the persistent kernel ran exactly when asked
         if graph:
             eng.capture()
         terms = []
@@ -109,6 +112,8 @@ def test_persistent_sweep_sharded_mirrors_bitwise(world):
         else:
             os.environ.pop("BD3MG_PK", None)
         try:
+            from paper_2002_02328_b200 import _native as N
+            n0 = N.lib.bd3mg_pk_launches()
             shards = [ShardedJacobi(obj, x0, h, torch.float64, rank=r, world=world, halo="p2p") for r in range(world)]
             bases = {r: s.peer.ptr for r, s in enumerate(shards)}
             for s in shards:
@@ -117,6 +122,7 @@ def test_persistent_sweep_sharded_mirrors_bitwise(world):
                 for s in shards:
                     s.local_sweep()
             torch.cuda.synchronize()
+            assert (N.lib.bd3mg_pk_launches() > n0) == pk
             outs.append(torch.cat([s.x[s.o_lo - s.l_lo:s.o_hi - s.l_lo + 1] for s in shards]).clone())
             for s in shards:
                 s.close()
