@@ -553,10 +553,19 @@ int power_hth_impl(const bd3mg_geom_t* g, const T* K, T* v, int iters, double* n
 // runs its HBM-bound stencils next to the FMA-bound correlations.  Event
 // record / wait is legal inside CUDA-graph capture (the side stream joins the
 // capture and is joined back before the sweep returns).
+constexpr int kMaxParts = 4;  // GRAD -> GRAM -> solve -> update chains of a batched step
 struct SideStream {
-  cudaStream_t side = nullptr;
-  cudaStream_t side2 = nullptr;  // second half of the blocks' GRAD -> GRAM chain
-  cudaEvent_t ev[8] = {};
+  // The block scheduler dispatches concurrent kernels of equal priority in launch order: a later
+  // kernel's CTAs start only when the earlier kernel has none left to dispatch, i.e. in its last wave
+  // (measured with scripts/sweep_timeline.py), so the streams overlap tails, not whole kernels.
+  // BD3MG_SIDE_PRIO=hi gives the stencil stream a higher priority: eager launches then run the stencils
+  // right after their producers, but torch's graph instantiation ignores node priorities and the sweep is
+  // work-conserving either way (measured: +-1%), so equal priorities stay the default.
+  cudaStream_t side = nullptr;             // stencils, recorder reductions
+  cudaStream_t chain[kMaxParts - 1] = {};  // streams of the chains after the first (which stays on the caller's)
+  cudaEvent_t ev[8 + 5 * kMaxParts] = {};
+  // events 8..: per chain p  fork (8+5p), regulariser-Gram fork (9+5p), its join (10+5p), chain join (11+5p),
+  // tail fork (12+5p)
 };
 cudaError_t side_stream(cudaStream_t main, SideStream** out) {
   static std::mutex mu;
@@ -567,9 +576,15 @@ cudaError_t side_stream(cudaStream_t main, SideStream** out) {
   std::lock_guard<std::mutex> lock(mu);
   SideStream& ss = cache[{dev, main}];
   if (!ss.side) {
-    e = cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ss.side2, cudaStreamNonBlocking);
-    for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
+    int least = 0, greatest = 0;
+    (void)cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const char* pr = getenv("BD3MG_SIDE_PRIO");
+    const int prio = (pr && pr[0] == 'h') ? greatest : 0;
+    e = cudaStreamCreateWithPriority(&ss.side, cudaStreamNonBlocking, prio);
+    for (int i = 0; i < kMaxParts - 1 && e == cudaSuccess; ++i)
+      e = cudaStreamCreateWithFlags(&ss.chain[i], cudaStreamNonBlocking);
+    for (int i = 0; i < 8 + 5 * kMaxParts && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
   *out = &ss;
@@ -840,23 +855,108 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     int rc = greg_launch(s);
     if (rc) return rc;
   }
-  // (2b)-(4) per half of the blocks: g = H^T r + greg, then the regulariser
-  // Gram terms (side stream) and the data Gram.  With a side stream the two
-  // halves run as two GRAD -> GRAM chains on two streams, so each kernel's
-  // last wave overlaps the other chain's work instead of idling SMs.
-  // measured: +1% at C2 fp64, -4% at C2 fp32 (the fp32 chains are short), so fp64 only
-  const int parts = (opt.ss && nt >= 4 && sizeof(T) == 8 && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
+  // (2b)-(7) The blocks are cut into `parts` groups, each a chain GRAD -> (regulariser Gram on the side
+  // stream | data Gram) -> solve -> update on its own stream.  The correlations of one chain fill the last
+  // waves of another's instead of idling SMs (measured: +1% at C2 fp64 with two chains; -4% at C2 fp32,
+  // whose chains are short, so fp64 only), and an earlier chain's HBM-bound solve + update run under a
+  // later chain's FMA-bound Gram correlation instead of after it.  A block's update touches only its own
+  // rows of x and d_mem, and no later kernel of another chain reads those (the Gram inputs are the
+  // chain's own g and d rows), so the chains are independent once the residual is formed.
+  // BD3MG_PARTS=n overrides (1: one chain, the pre-split layout).
+  static const int parts_env = getenv("BD3MG_PARTS") ? atoi(getenv("BD3MG_PARTS")) : 0;
+  int parts = (opt.ss && nt >= 4 && sizeof(T) == 8 && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
+  if (parts > 1 && parts_env > 0) parts = std::min(std::min(parts_env, kMaxParts), nt);
+  // the fused-gradient recorder (opt-in) reduces its sums over all chains before the update: one tail
+  const bool chain_tails = parts > 1 && !opt.rec_gradf;
   std::vector<std::pair<long long, long long>> granges(nt);
   long long gram_row0 = 0;  // first partial row of the current part's Gram launch
   const long long tl_reg = z_tiles<T>(g);
   std::vector<int> rg_begin(nt), rg_end(nt);  // regulariser-Gram jobs of each block
   int rg_jobs = 0;
   long long grad_row0 = 0;  // first recorder row of the current part's fused-gradient launch
-  if (parts == 2) CU(hop(s, opt.ss->side2, opt.ss->ev[4]));  // fork after RESID / greg
+  // mirrors: every row must be updated by this call (checked over all blocks before any chain launches)
+  for (int j = 0; j < opt.nmirrors; ++j) {
+    const bd3mg_mirror_t& M = opt.mirrors[j];
+    int64_t covered = 0;
+    for (int t = 0; t < nt; ++t) {
+      const int64_t lo = std::max<int64_t>(M.z_lo, tasks[t].z_lo), hi = std::min<int64_t>(M.z_hi, tasks[t].z_hi);
+      if (lo > hi) continue;
+      if (!tasks[t].x_rows) return fail(BD3MG_EINVAL, "mirrored rows need an in-place update");
+      covered += hi - lo + 1;
+    }
+    if (covered != M.z_hi - M.z_lo + 1)
+      return fail(BD3MG_EINVAL, "mirror rows [%lld, %lld] are not all updated by this call", (long long)M.z_lo,
+                  (long long)M.z_hi);
+  }
+  // (5)+(6) per-block reductions and the 2x2 solves of blocks [t0, t1), one CTA per block
+  auto launch_solve = [&](int t0, int t1, cudaStream_t st) -> int {
+    SolveArgs sa;
+    memset(&sa, 0, sizeof(sa));
+    sa.nblocks = t1 - t0;
+    sa.two_eta = 2.0 * r->eta; sa.lam = r->lam; sa.two_kappa = 2.0 * r->kappa;
+    sa.prune_tol = kPruneTol; sa.pinv_tol = kPinvTol;
+    sa.nv_gram = gmode == M_GRAM1 ? 1 : 3;
+    const long long tl = z_tiles<T>(g);
+    for (int t = t0; t < t1; ++t) {
+      sa.has_d[t - t0] = tasks[t].d_mem != nullptr;
+      sa.g_begin[t - t0] = granges[t].first; sa.g_end[t - t0] = granges[t].second;
+      sa.r_begin[t - t0] = rg_begin[t] * tl; sa.r_end[t - t0] = rg_end[t] * tl;
+    }
+    reduce_solve_kernel<<<t1 - t0, kEwNT, 0, st>>>(sa, cparts, rparts, info_out + (size_t)t0 * kInfoNV); launched();
+    CU(cudaGetLastError());
+    return BD3MG_OK;
+  };
+  // (7) increments / in-place update of blocks [t0, t1); `fin`: this launch also writes the recorder terms
+  auto launch_update = [&](int t0, int t1, bool fin, cudaStream_t st) -> int {
+#ifndef BD3MG_EXP_SKIP_UPDATE
+    UpdArgs<T> ua;
+    memset(&ua, 0, sizeof(ua));
+    ua.nblocks = t1 - t0;
+    if (fin) { ua.fin_sums = opt.fin_sums; ua.fin_terms = opt.fin_terms; }
+    ua.fin_eta = r->eta; ua.fin_lam = r->lam; ua.fin_kappa = r->kappa;
+    int mc = 1;
+    for (int t = t0; t < t1; ++t) {
+      UpdBlock<T>& B = ua.blk[t - t0];
+      B.g = gb[t]; B.d = (const T*)tasks[t].d_mem; B.inc_out = (T*)tasks[t].inc_out;
+      B.x = (T*)tasks[t].x_rows; B.dmem = (T*)tasks[t].dmem_rows;
+      B.n = h[t] * plane;
+      B.ctas = (int)std::max<int64_t>(1, std::min<int64_t>((B.n + 4 * kEwNT - 1) / (4 * kEwNT), 1024));
+      mc = std::max(mc, B.ctas);
+    }
+    double* info_p = info_out + (size_t)t0 * kInfoNV;
+    // split each mirror into per-block element ranges of the in-place update
+    MirArgs<T, kMaxMirSegs> ma;
+    memset(&ma, 0, sizeof(ma));
+    for (int j = 0; j < opt.nmirrors; ++j) {
+      const bd3mg_mirror_t& M = opt.mirrors[j];
+      for (int t = t0; t < t1; ++t) {
+        const int64_t lo = std::max<int64_t>(M.z_lo, tasks[t].z_lo), hi = std::min<int64_t>(M.z_hi, tasks[t].z_hi);
+        if (lo > hi) continue;
+        if (ma.n == kMaxMirSegs) return fail(BD3MG_EINVAL, "more than %d mirror segments", kMaxMirSegs);
+        MirSeg<T>& S = ma.s[ma.n++];
+        S.blk = t - t0;
+        S.a = (lo - tasks[t].z_lo) * plane;
+        S.b = (hi - tasks[t].z_lo + 1) * plane;
+        S.dst = (T*)M.dst + (lo - M.z_lo) * plane;
+      }
+    }
+    if (ma.n == 0) {
+      update_kernel<T, 0><<<dim3(mc, t1 - t0), kEwNT, 0, st>>>(ua, MirArgs<T, 0>{0, {}}, info_p); launched();
+    } else {
+      update_kernel<T, kMaxMirSegs><<<dim3(mc, t1 - t0), kEwNT, 0, st>>>(ua, ma, info_p); launched();
+    }
+    CU(cudaGetLastError());
+#else
+    (void)t0; (void)t1; (void)fin; (void)st;
+#endif
+    return BD3MG_OK;
+  };
+  for (int part = 1; part < parts; ++part)  // fork after RESID / greg
+    CU(hop(s, opt.ss->chain[part - 1], opt.ss->ev[8 + 5 * part]));
   for (int part = 0; part < parts; ++part) {
-    const int t0 = part == 0 ? 0 : nt / 2, t1 = (parts == 1 || part == 1) ? nt : nt / 2;
+    const int t0 = (int)((long long)nt * part / parts), t1 = (int)((long long)nt * (part + 1) / parts);
     const int np = t1 - t0;
-    cudaStream_t sp = part == 0 ? s : opt.ss->side2;
+    cudaStream_t sp = part == 0 ? s : opt.ss->chain[part - 1];
     {
       ConvArgs<T> a = base_args<T>(g, r, K);
       a.njobs = np;
@@ -879,7 +979,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     // regulariser Gram terms on the side stream, concurrent with the Gram correlation
     cudaStream_t s3 = sp;
     if (opt.ss) {
-      CU(hop(sp, opt.ss->side, opt.ss->ev[part == 0 ? 2 : 5]));
+      CU(hop(sp, opt.ss->side, opt.ss->ev[9 + 5 * part]));
       s3 = opt.ss->side;
     }
     {
@@ -933,74 +1033,26 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       }
       gram_row0 += rows;
     }
+    if (chain_tails) {
+      // this chain's solve + update as soon as its own sums are in: the side stream has run the
+      // recorder's reductions and this chain's regulariser Gram by the event recorded here
+      CU(hop(opt.ss->side, sp, opt.ss->ev[10 + 5 * part]));
+      int rc = launch_solve(t0, t1, sp);
+      if (rc) return rc;
+      rc = launch_update(t0, t1, part == 0, sp);
+      if (rc) return rc;
+    }
   }
-  if (parts == 2) CU(hop(opt.ss->side2, s, opt.ss->ev[6]));  // join the second chain
+  for (int part = 1; part < parts; ++part)  // join the later chains
+    CU(hop(opt.ss->chain[part - 1], s, opt.ss->ev[11 + 5 * part]));
   if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[3]));  // join the side stream
   if (opt.rec_gradf)  // the recorder's stencil sums from the fused gradient's partial rows
     CU(reduce(eparts_g, kGradfNV, {{0, grad_rows}}, opt.rec_sums, kGradfNV, s));
-  // (5)+(6) per-block reductions and the 2x2 solves, one CTA per block
-  {
-    SolveArgs sa;
-    memset(&sa, 0, sizeof(sa));
-    sa.nblocks = nt;
-    sa.two_eta = 2.0 * r->eta; sa.lam = r->lam; sa.two_kappa = 2.0 * r->kappa;
-    sa.prune_tol = kPruneTol; sa.pinv_tol = kPinvTol;
-    sa.nv_gram = gmode == M_GRAM1 ? 1 : 3;
-    const long long tl = z_tiles<T>(g);
-    for (int t = 0; t < nt; ++t) {
-      sa.has_d[t] = tasks[t].d_mem != nullptr;
-      sa.g_begin[t] = granges[t].first; sa.g_end[t] = granges[t].second;
-      sa.r_begin[t] = rg_begin[t] * tl; sa.r_end[t] = rg_end[t] * tl;
-    }
-    reduce_solve_kernel<<<nt, kEwNT, 0, s>>>(sa, cparts, rparts, info_out); launched();
-    CU(cudaGetLastError());
-  }
-  // (7) increments / in-place update
-  {
-    UpdArgs<T> ua;
-    memset(&ua, 0, sizeof(ua));
-    ua.nblocks = nt;
-    ua.fin_sums = opt.fin_sums; ua.fin_terms = opt.fin_terms;
-    ua.fin_eta = r->eta; ua.fin_lam = r->lam; ua.fin_kappa = r->kappa;
-    int mc = 1;
-    for (int t = 0; t < nt; ++t) {
-      UpdBlock<T>& B = ua.blk[t];
-      B.g = gb[t]; B.d = (const T*)tasks[t].d_mem; B.inc_out = (T*)tasks[t].inc_out;
-      B.x = (T*)tasks[t].x_rows; B.dmem = (T*)tasks[t].dmem_rows;
-      B.n = h[t] * plane;
-      B.ctas = (int)std::max<int64_t>(1, std::min<int64_t>((B.n + 4 * kEwNT - 1) / (4 * kEwNT), 1024));
-      mc = std::max(mc, B.ctas);
-    }
-#ifndef BD3MG_EXP_SKIP_UPDATE
-    if (opt.nmirrors == 0) {
-      update_kernel<T, 0><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, MirArgs<T, 0>{0, {}}, info_out); launched();
-    } else {
-      // split each mirror into per-block element ranges of the in-place update
-      MirArgs<T, kMaxMirSegs> ma;
-      memset(&ma, 0, sizeof(ma));
-      for (int j = 0; j < opt.nmirrors; ++j) {
-        const bd3mg_mirror_t& M = opt.mirrors[j];
-        int64_t covered = 0;
-        for (int t = 0; t < nt; ++t) {
-          const int64_t lo = std::max<int64_t>(M.z_lo, tasks[t].z_lo), hi = std::min<int64_t>(M.z_hi, tasks[t].z_hi);
-          if (lo > hi) continue;
-          if (!tasks[t].x_rows) return fail(BD3MG_EINVAL, "mirrored rows need an in-place update");
-          if (ma.n == kMaxMirSegs) return fail(BD3MG_EINVAL, "more than %d mirror segments", kMaxMirSegs);
-          MirSeg<T>& S = ma.s[ma.n++];
-          S.blk = t;
-          S.a = (lo - tasks[t].z_lo) * plane;
-          S.b = (hi - tasks[t].z_lo + 1) * plane;
-          S.dst = (T*)M.dst + (lo - M.z_lo) * plane;
-          covered += hi - lo + 1;
-        }
-        if (covered != M.z_hi - M.z_lo + 1)
-          return fail(BD3MG_EINVAL, "mirror rows [%lld, %lld] are not all updated by this call", (long long)M.z_lo,
-                      (long long)M.z_hi);
-      }
-      update_kernel<T, kMaxMirSegs><<<dim3(mc, nt), kEwNT, 0, s>>>(ua, ma, info_out); launched();
-    }
-#endif
-    CU(cudaGetLastError());
+  if (!chain_tails) {
+    int rc = launch_solve(0, nt, s);
+    if (rc) return rc;
+    rc = launch_update(0, nt, true, s);
+    if (rc) return rc;
   }
   // (8) cached H E_S d_mem for the next visit (variant "hd-cache"), and the
   // maintained residual (variant "hd-incremental")
