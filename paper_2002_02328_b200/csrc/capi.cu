@@ -633,6 +633,18 @@ bool gradf_ok(const bd3mg_geom_t* g) {
          st_use_tma<T>(g->nx);
 }
 
+// The regulariser Gram terms computed by the dual-input Gram correlation in
+// front of its tap walk (rg_center, depthvar.cuh) instead of a separate
+// reg_gram stencil pass: fp64, square 3 / 5 / 7 / 9 taps, rows of whole
+// 16-byte chunks.  BD3MG_NO_RGF=1 keeps the separate pass (the persistent
+// sweep's bitwise twin).
+template <typename T>
+bool rgf_ok(const bd3mg_geom_t* g, int gmode) {
+  const bool off = getenv("BD3MG_NO_RGF") != nullptr;
+  return !off && sizeof(T) == 8 && gmode == M_GRAM2 && conv_tiled_shape(g->ky, g->kx) &&
+         !conv_rz2<T>(g->ky, g->kx, M_GRAM2) && (g->nx * (long long)sizeof(T)) % 16 == 0;
+}
+
 // Small stencil grids (one block of a cyclic / asynchronous step): each
 // block's z-march is cut into chunks of c planes so a block alone fills ~2
 // CTAs per SM (the march is a serial chain of TMA round trips per CTA).  c
@@ -767,7 +779,10 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     const int64_t c = stencil_chunk<T>(g, h[t]);
     rg_total += (h[t] + c - 1) / c;
   }
-  const long long reg_rows = rg_total * z_tiles<T>(g);
+  // fused into the Gram correlation: one partial row per (block plane, Gram tile)
+  const bool rgf = rgf_ok<T>(g, gmode);
+  const long long rgf_tiles = rgf ? conv_tiles<T>(g, M_GRAM2) : 0;
+  const long long reg_rows = rgf ? hsum * rgf_tiles : rg_total * z_tiles<T>(g);
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return ws_fail(ws);
@@ -900,7 +915,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     for (int t = t0; t < t1; ++t) {
       sa.has_d[t - t0] = tasks[t].d_mem != nullptr;
       sa.g_begin[t - t0] = granges[t].first; sa.g_end[t - t0] = granges[t].second;
-      sa.r_begin[t - t0] = rg_begin[t] * tl; sa.r_end[t - t0] = rg_end[t] * tl;
+      sa.r_begin[t - t0] = rgf ? rg_begin[t] : rg_begin[t] * tl;
+      sa.r_end[t - t0] = rgf ? rg_end[t] : rg_end[t] * tl;
     }
     reduce_solve_kernel<<<t1 - t0, kEwNT, 0, st>>>(sa, cparts, rparts, info_out + (size_t)t0 * kInfoNV); launched();
     CU(cudaGetLastError());
@@ -977,12 +993,19 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       for (int t = t0; t < t1; ++t) grad_row0 += conv_rows<T>(g, M_GRAD, h[t]);
     }
     // regulariser Gram terms on the side stream, concurrent with the Gram correlation
+    // (or inside the Gram correlation itself: rgf)
     cudaStream_t s3 = sp;
-    if (opt.ss) {
+    if (rgf) {
+      for (int t = t0; t < t1; ++t) {
+        rg_begin[t] = rg_jobs;  // in partial rows, not jobs
+        rg_jobs += (int)(h[t] * rgf_tiles);
+        rg_end[t] = rg_jobs;
+      }
+    } else if (opt.ss) {
       CU(hop(sp, opt.ss->side, opt.ss->ev[9 + 5 * part]));
       s3 = opt.ss->side;
     }
-    {
+    if (!rgf) {
       StArgs<T> sa = st_args<T>(g, r);
       sa.partials = rparts + (size_t)rg_jobs * tl_reg * kRegNV;  // job-major rows after the earlier parts
       std::vector<StJob<T>> jobs;
@@ -1018,6 +1041,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
         j.src0 = gb[t];
         j.src1 = tasks[t].d_mem ? (const T*)tasks[t].d_mem : gb[t];
         if (cached) { j.sub = opt.hd[t]; j.dst0 = hgb[t]; }
+        if (rgf) { j.omega = wb[t]; j.eparts = rparts + (size_t)rg_begin[t] * kRegNV; }
         j.src_z0 = tasks[t].z_lo; j.src_nz = (int)h[t];
         j.out_lo = (int)olo[t]; j.nout = (int)(ohi[t] - olo[t] + 1);
       }

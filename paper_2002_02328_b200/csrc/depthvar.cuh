@@ -29,6 +29,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bd3mg {
@@ -48,6 +50,7 @@ enum ConvMode : int {
 };
 
 constexpr int kMaxJobs = 32;
+constexpr int kRgNV = 12;  // regulariser-Gram sums per partial row (= kRegNV, stencil.cuh)
 
 template <typename T>
 struct alignas(64) ConvJob {
@@ -58,9 +61,12 @@ struct alignas(64) ConvJob {
   T* dst0;              // output rows; row 0 is global depth out_lo
   const T* sub;         // M_RESID: rows aligned with dst0
   const T* xg;          // M_GRADF: iterate fragment (plane 0 = depth xg_z0, xg_nz planes; tmap1 maps it)
-  T* omega;             // M_GRADF: omega rows aligned with dst0
+  T* omega;             // M_GRADF: omega rows aligned with dst0; M_GRAM2 (fp64): omega rows of the block
+                        //   (row 0 = src_z0) -- the regulariser Gram terms are then computed by the tiles
+                        //   whose output plane lies inside the block (no separate reg_gram pass), or null
   T* snap;              // M_GRADF: recorder snapshot rows aligned with dst0 (rolled), or null
-  double* eparts;       // M_GRADF: recorder partial rows (one per CTA, kEvalNV), or null (no recorder)
+  double* eparts;       // M_GRADF: recorder partial rows (one per CTA, kEvalNV), or null (no recorder);
+                        //   M_GRAM2 with omega: regulariser-Gram partial rows, kRgNV per (block plane, tile)
   long long src_z0;
   long long xg_z0;
   int src_nz, xg_nz;
@@ -217,10 +223,15 @@ struct ConvCfg {
   static constexpr int NV = ModeNV<MODE>::value;
   static constexpr size_t TILE_BYTES = (size_t)TILE * sizeof(T);  // 128-byte aligned buffer stride
   static constexpr size_t BOX_BYTES = (size_t)BOX * sizeof(T);
+  // fp64 dual-input Gram: the regulariser Gram terms of the block are computed before the tap walk
+  // (rg_center); their omega tile (TX x TY, cp.async-staged) and the reduction scratch follow the
+  // barriers.  The dual-input tile runs 2 CTAs per SM (shared-memory bound), so these 17 KB are free.
+  static constexpr bool RGF = DUAL && sizeof(T) == 8;
+  static constexpr size_t RG_BYTES = RGF ? (size_t)TX * TY * sizeof(T) + (NT / 32) * kRgNV * sizeof(double) : 0;
   BD3MG_HD static size_t coef_bytes(int kz) { return ((size_t)kz * KY * KX * sizeof(T) + 127) & ~size_t(127); }
   // bytes conv_tile uses from its 128-byte aligned base
   static size_t layout_bytes(int kz) {
-    return coef_bytes(kz) + 2 * NIN * TILE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double);
+    return coef_bytes(kz) + 2 * NIN * TILE_BYTES + 2 * sizeof(uint64_t) + 8 * (NT / 32) * sizeof(double) + RG_BYTES;
   }
   static size_t smem_bytes(int kz) { return layout_bytes(kz) + 128; }
 };
@@ -300,12 +311,14 @@ struct TileIO {
   int epi_z;
   bool use_tma;
   // M_GRADF: iterate fragment (axial neighbours read through L2), outputs
-  const T* xf;
-  long long xf_z0;
-  int xf_nz;
-  T* omega;                     // omega plane (row y at omega + y*nx)
-  T* snap;                      // snapshot plane or null
-  double* epart;                // recorder partials (kEvalNV) or null
+  const T* xf = nullptr;
+  long long xf_z0 = 0;
+  int xf_nz = 0;
+  T* omega = nullptr;           // omega plane (row y at omega + y*nx); M_GRAM2: the block's omega plane zo
+                                //   (the tile then adds the regulariser Gram terms, rg_center), or null
+  T* snap = nullptr;            // snapshot plane or null
+  double* epart = nullptr;      // recorder partials (kEvalNV) or null; M_GRAM2: the tile's kRgNV sums
+  bool rg_has_d = false;        // M_GRAM2 + omega: the block has a memory column (in1 is d, not g again)
 };
 
 constexpr int kGradfNV = 5;     // recorder sums of M_GRADF: box, tv, axial, |x-snap|^2, |snap|^2
@@ -471,6 +484,126 @@ BD3MG_D void gradf_epilogue(const ConvGeom<T>& p, const TileIO<T>& io, int zo, i
   }
 }
 
+// Regulariser Gram terms of one block plane, computed by the dual-input Gram
+// tile whose output plane zo lies inside the block [blo, bhi].  Such a tile
+// starts its tap walk at the centre tap, so the first two staged planes are
+// plane zo (g0, d0) and, when zo < bhi, plane zo + 1 (g1, d1) of g and d: they
+// hold every neighbour the forward differences need; omega comes from the
+// tile's cp.async-staged copy `ws` (TX x TY).  Term by term this is
+// reg_gram_tile (stencil_tma.cuh; reference objective.py:262-274,
+// directions.py:80-85) for the columns [-g, d] embedded on the block:
+// v[0..2] column norms, [3..5] omega-weighted TV terms, [6..8] axial terms,
+// [9] g.d, [10] nonzeros of g, [11] non-finite entries of g; the CTA's sums go
+// to part_out (thread 0).  Out-of-volume pixels of the staged tiles and of
+// the omega tile are zero, so they add nothing; only the far-face rules of the
+// differences need masks.  Every FP64 instruction here competes with the
+// correlation for the FP64 pipe, so the flags are counted on the integer pipe.
+// The row loop is kept rolled: ptxas budgets the kernel's uniform registers
+// over all of its code, and the tap walk needs them for its coefficients (DFMA
+// with a uniform operand; with the coefficients in vector registers the walk
+// runs 15% slower -- measured).
+#ifndef BD3MG_RG_UNROLL
+#define BD3MG_RG_UNROLL 1  // rows of rg_center's loop unrolled together (code size vs latency hiding, see below)
+#endif
+constexpr int kRgUnroll = BD3MG_RG_UNROLL;
+template <typename T, typename Cfg>
+__device__ __noinline__ void rg_center(int nx, int ny, int nz_global, int zo, int x0, int y0, int blo, int bhi,
+                                       bool has_d, const T* g0, const T* d0, const T* g1, const T* d1, const T* ws,
+                                       double* red, double* part_out) {
+  using V = typename Vec16<T>::type;
+  constexpr int RX = Cfg::RX, RY = Cfg::RY, PITCH = Cfg::PITCH;
+  static_assert(RX == 2 && sizeof(T) == 8, "fp64 tile: one 16-byte vector per thread row");
+  const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
+  const int xa = x0 + tx * RX;                     // the thread's two columns xa, xa + 1
+  const bool mx0 = xa < nx - 1, mx1 = xa + 1 < nx - 1;
+  const int q0 = (ty * RY + Cfg::RYH) * PITCH + tx * RX + Cfg::RXA;
+  const bool next = zo < bhi, far = !next && bhi < nz_global - 1, first = zo == blo && blo >= 1;
+  double v[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) v[k] = 0.0;
+  int nnz = 0, nnf = 0;
+  // row r of the thread: columns xa, xa + 1 and the right neighbour xa + 2
+  T gc[3], dc[3];
+  {
+    const V a = *reinterpret_cast<const V*>(g0 + q0);
+    gc[0] = a.x; gc[1] = a.y; gc[2] = g0[q0 + 2];
+    dc[0] = dc[1] = dc[2] = T(0);
+    if (has_d) {
+      const V b = *reinterpret_cast<const V*>(d0 + q0);
+      dc[0] = b.x; dc[1] = b.y; dc[2] = d0[q0 + 2];
+    }
+  }
+#pragma unroll kRgUnroll
+  for (int r = 0; r < RY; ++r) {
+    const int ly = ty * RY + r, y = y0 + ly;
+    const bool my = y < ny - 1;
+    const int q = q0 + (r + 1) * PITCH;
+    T gn[3], dn[3];  // the row below
+    {
+      const V a = *reinterpret_cast<const V*>(g0 + q);
+      gn[0] = a.x; gn[1] = a.y; gn[2] = g0[q + 2];
+      dn[0] = dn[1] = dn[2] = T(0);
+      if (has_d) {
+        const V b = *reinterpret_cast<const V*>(d0 + q);
+        dn[0] = b.x; dn[1] = b.y; dn[2] = d0[q + 2];
+      }
+    }
+    const V wv = *reinterpret_cast<const V*>(ws + ly * Cfg::TX + tx * RX);
+    V g1v = {T(0), T(0)}, d1v = {T(0), T(0)};
+    if (next) {
+      g1v = *reinterpret_cast<const V*>(g1 + q - PITCH);
+      if (has_d) d1v = *reinterpret_cast<const V*>(d1 + q - PITCH);
+    }
+#pragma unroll
+    for (int i = 0; i < RX; ++i) {
+      const T g = gc[i], d = dc[i];
+      const double w = i == 0 ? wv.x : wv.y;
+      const bool mx = i == 0 ? mx0 : mx1;
+      // columns b0 = -g, b1 = d
+      v[0] += g * g;
+      v[1] -= g * d;
+      v[2] += d * d;
+      const double dx0 = mx ? sub_rn(g, gc[i + 1]) : 0.0;   // -(g[x+1] - g)
+      const double dy0 = my ? sub_rn(g, gn[i]) : 0.0;
+      const double dx1 = mx ? sub_rn(dc[i + 1], d) : 0.0;
+      const double dy1 = my ? sub_rn(dn[i], d) : 0.0;
+      v[3] += w * (dx0 * dx0 + dy0 * dy0);
+      v[4] += w * (dx0 * dx1 + dy0 * dy1);
+      v[5] += w * (dx1 * dx1 + dy1 * dy1);
+      // axial row zo of the block-embedded vectors
+      double z0v = 0.0, z1v = 0.0;
+      if (next) {
+        z0v = g - (i == 0 ? g1v.x : g1v.y);
+        z1v = (i == 0 ? d1v.x : d1v.y) - d;
+      } else if (far) {
+        z0v = g;      // -b0
+        z1v = -d;     // -b1
+      }
+      v[6] += z0v * z0v;
+      v[7] += z0v * z1v;
+      v[8] += z1v * z1v;
+      // flags on the integer pipe: g != 0 (either zero sign), g non-finite (exponent all ones)
+      const unsigned hi = (unsigned)__double2hiint(g) & 0x7fffffffu, lo = (unsigned)__double2loint(g);
+      nnz += (hi | lo) != 0u;
+      nnf += hi >= 0x7ff00000u;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { gc[k] = gn[k]; dc[k] = dn[k]; }
+  }
+  double o[kRgNV];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) o[k] = v[k];
+  if (first) { o[6] += v[0]; o[7] += v[1]; o[8] += v[2]; }  // the row above the block: (b - 0)^2
+  o[9] = -v[1];  // g.d: every product is the exact negation of (-g).d
+  o[10] = (double)nnz;
+  o[11] = (double)nnf;
+  cta_reduce<kRgNV, Cfg::NT>(o, red);
+  if (threadIdx.x == 0 && part_out) {
+#pragma unroll
+    for (int k = 0; k < kRgNV; ++k) part_out[k] = o[k];
+  }
+}
+
 // One TY x TX output tile of output plane zo: the kz-tap walk over the staged
 // input planes (double-buffered TMA ring, mbarrier completion), the register-
 // tiled FMA loop, and the mode's epilogue; `part` receives the CTA's NV
@@ -493,6 +626,9 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
   uint64_t* mbar_l = reinterpret_cast<uint64_t*>(sbase + 2 * NIN * Cfg::TILE_BYTES + Cfg::coef_bytes(p.kz));
   double* red_s = reinterpret_cast<double*>(mbar_l + 2);
   uint64_t* mbar = bars ? bars : mbar_l;  // persistent kernel: barriers at a fixed location
+  // fused regulariser Gram (fp64 dual-input tile whose output plane lies inside the block)
+  constexpr bool kRgf = Cfg::RGF && MODE == M_GRAM2;
+  const bool rg_here = kRgf && io.omega != nullptr;
 
   const int tx = threadIdx.x % Cfg::WX, ty = threadIdx.x / Cfg::WX;
   const int rz = (p.kz - 1) / 2;
@@ -503,6 +639,13 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
   const int a_lo = (int)max(0LL, zlo_in - zo + rz);
   const int a_hi = (int)min((long long)p.kz - 1, zhi_in - zo + rz);
   const int ntap = a_hi - a_lo + 1;
+  // A tile that also computes the regulariser Gram terms walks its taps so that the centre comes last:
+  // a_lo .. rz - 1 upwards, then a_hi .. rz downwards.  The two ring buffers then still hold planes
+  // zo + 1 and zo of g and d when the walk ends -- every neighbour those terms need -- and the extra work
+  // sits behind the walk (rg_center, called from the epilogue), not inside it.  (The order only regroups
+  // the roundings of sums that feed the 2 x 2 Gram; every batching of a block uses the same order.)
+  const int n_lo = rg_here ? rz - a_lo : ntap;
+  auto tap_of = [&](int step) { return step < n_lo ? a_lo + step : a_hi - (step - n_lo); };
   // steps of the walk: the taps (two-pass Gram: the taps over input 1, then over input 0)
   const int nstep = TWOPASS ? 2 * ntap : ntap;
 
@@ -517,7 +660,7 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
   auto issue = [&](int step, int b) {
     T* dst = tiles + b * NIN * Cfg::TILE;
     const bool second = TWOPASS && step < ntap;  // pass 0 of the two-pass Gram reads input 1
-    const int a = a_lo + (TWOPASS && step >= ntap ? step - ntap : step);
+    const int a = kRgf ? tap_of(step) : a_lo + (TWOPASS && step >= ntap ? step - ntap : step);
     const int zi = zo + a - rz;
     const TileSrc<T>& in = second ? io.in1 : io.in0;
     if (tma) {
@@ -548,6 +691,19 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
 #pragma unroll
     for (int i = 0; i < RX; ++i) accp[r][i] = T(0);
 
+  if constexpr (kRgf) {
+    if (rg_here) {  // each thread stages its own omega values (RY rows x 16 bytes)
+      T* rg_w = reinterpret_cast<T*>(red_s + 8 * (Cfg::NT / 32));  // omega tile, TX x TY
+      const int xw = x0 + tx * RX;
+#pragma unroll 1
+      for (int r = 0; r < RY; ++r) {
+        const int ly = ty * RY + r, y = y0 + ly;
+        const bool ok = y < p.ny && xw + RX <= p.nx;
+        cp_async<16>(rg_w + ly * Cfg::TX + tx * RX, ok ? io.omega + (long long)y * p.nx + xw : io.omega, ok);
+      }
+      cp_async_commit();
+    }
+  }
   if (nstep > 0) issue(0, 0);
   // the epilogue operand rows of this tile are pulled into L2 two taps before
   // the end, so the epilogue's loads do not wait on DRAM
@@ -603,7 +759,7 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
       else cp_async_wait<0>();
       __syncthreads();
     }
-    const int a = a_lo + (TWOPASS && st >= ntap ? st - ntap : st);
+    const int a = kRgf ? tap_of(st) : a_lo + (TWOPASS && st >= ntap ? st - ntap : st);
     const T* cs = coef_s + a * (KY * KX);
     const T* tb = tiles + buf * NIN * Cfg::TILE + (ty * RY) * Cfg::PITCH + tx * RX;
 #pragma unroll
@@ -727,6 +883,20 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
     }
   }
   }  // !vec_here
+  if constexpr (kRgf) {
+    // (after the Gram products above: only the three partial sums stay live across the call)
+    if (rg_here) {
+      const T* t0 = tiles + (buf ^ 1) * NIN * Cfg::TILE;  // the last step: the centre plane zo
+      const T* t1 = tiles + buf * NIN * Cfg::TILE;        // the step before: plane zo + 1 (when zo < bhi)
+      cp_async_wait<0>();                                 // the omega tile
+      T* rg_w = reinterpret_cast<T*>(red_s + 8 * (Cfg::NT / 32));
+#ifndef BD3MG_EXP_RGF_NOCALL
+      rg_center<T, Cfg>(p.nx, p.ny, p.nz_global, zo, x0, y0, (int)zlo_in, (int)zhi_in, io.rg_has_d, t0,
+                        t0 + Cfg::TILE, t1, t1 + Cfg::TILE, rg_w, reinterpret_cast<double*>(rg_w + Cfg::TX * Cfg::TY),
+                        io.epart);
+#endif
+    }
+  }
   if constexpr (NV > 0) {
     cta_reduce<NV, Cfg::NT>(part, red_s);
     if (threadIdx.x == 0 && part_out) {
@@ -763,6 +933,15 @@ __global__ void __launch_bounds__(ConvCfg<T, KY, KX, MODE>::NT)
     io.omega = job.omega + orow;
     io.snap = job.snap ? job.snap + orow : nullptr;
     io.epart = job.eparts ? job.eparts + pos.cta * kGradfNV : nullptr;
+  }
+  if constexpr (MODE == M_GRAM2 && Cfg::RGF) {
+    // the block's regulariser Gram terms ride on the tiles whose output plane lies inside the block
+    if (job.omega && zo >= job.src_z0 && zo < job.src_z0 + job.src_nz) {
+      const long long brow = zo - job.src_z0;
+      io.omega = job.omega + brow * p.plane;
+      io.epart = job.eparts + (brow * ((long long)gridDim.x * gridDim.y) + (long long)pos.ty * gridDim.x + pos.tx) * kRgNV;
+      io.rg_has_d = job.src1 != job.src0;
+    }
   }
   constexpr int NV = Cfg::NV;
   conv_tile<T, KY, KX, MODE, ADJ>(p, io, zo, pos.tx * Cfg::TX, pos.ty * Cfg::TY,

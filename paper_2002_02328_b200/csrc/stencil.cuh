@@ -22,6 +22,7 @@ constexpr int kTS = 32;                 // tile edge (pixels)
 constexpr int kStNT = 256;              // threads: 32 (x) x 8 (y); 4 rows per thread
 constexpr int kStRows = kTS / (kStNT / kTS);
 constexpr int kRegNV = 12;              // sums produced per block by reg_gram
+static_assert(kRegNV == kRgNV, "the fused regulariser Gram (depthvar.cuh, rg_center) writes the same rows");
 constexpr int kEvalNV = 5;              // box, tv, axial, |x-snap|^2, |snap|^2
 
 template <typename T>

@@ -22,6 +22,9 @@ def _run(obj, x0, h, sweeps, pk: bool, graph=False):
         os.environ["BD3MG_PK"] = "1"
     else:
         os.environ.pop("BD3MG_PK", None)
+    # the bitwise twin of the persistent sweep is the multi-kernel sweep with the separate regulariser-Gram
+    # stencil (the default multi-kernel sweep folds those sums into the Gram correlation: other groupings)
+    os.environ["BD3MG_NO_RGF"] = "1"
     from paper_2002_02328_b200 import _native as N
     n0 = N.lib.bd3mg_pk_launches()
     try:
@@ -38,6 +41,7 @@ def _run(obj, x0, h, sweeps, pk: bool, graph=False):
         return eng, terms
     finally:
         os.environ.pop("BD3MG_PK", None)
+        os.environ.pop("BD3MG_NO_RGF", None)
 
 
 def _problem(k, nx, ny, nz, seed, kz=None):
@@ -111,6 +115,7 @@ def test_persistent_sweep_sharded_mirrors_bitwise(world):
             os.environ["BD3MG_PK"] = "1"
         else:
             os.environ.pop("BD3MG_PK", None)
+        os.environ["BD3MG_NO_RGF"] = "1"  # see _run
         try:
             from paper_2002_02328_b200 import _native as N
             n0 = N.lib.bd3mg_pk_launches()
@@ -128,6 +133,7 @@ def test_persistent_sweep_sharded_mirrors_bitwise(world):
                 s.close()
         finally:
             os.environ.pop("BD3MG_PK", None)
+            os.environ.pop("BD3MG_NO_RGF", None)
     assert torch.equal(outs[0], outs[1])
     single, _ = _run(obj, x0, h, 4, pk=True)
     assert torch.equal(outs[0], single.x)
