@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <queue>
 #include <type_traits>
@@ -563,9 +564,9 @@ struct SideStream {
   // work-conserving either way (measured: +-1%), so equal priorities stay the default.
   cudaStream_t side = nullptr;             // stencils, recorder reductions
   cudaStream_t chain[kMaxParts - 1] = {};  // streams of the chains after the first (which stays on the caller's)
-  cudaEvent_t ev[8 + 5 * kMaxParts] = {};
+  cudaEvent_t ev[8 + 6 * kMaxParts] = {};
   // events 8..: per chain p  fork (8+5p), regulariser-Gram fork (9+5p), its join (10+5p), chain join (11+5p),
-  // tail fork (12+5p)
+  // tail fork (12+5p); then kMaxParts "chain's regulariser gradient ready" events
 };
 cudaError_t side_stream(cudaStream_t main, SideStream** out) {
   static std::mutex mu;
@@ -583,7 +584,7 @@ cudaError_t side_stream(cudaStream_t main, SideStream** out) {
     e = cudaStreamCreateWithPriority(&ss.side, cudaStreamNonBlocking, prio);
     for (int i = 0; i < kMaxParts - 1 && e == cudaSuccess; ++i)
       e = cudaStreamCreateWithFlags(&ss.chain[i], cudaStreamNonBlocking);
-    for (int i = 0; i < 8 + 5 * kMaxParts && e == cudaSuccess; ++i)
+    for (int i = 0; i < 8 + 6 * kMaxParts && e == cudaSuccess; ++i)
       e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
@@ -593,6 +594,16 @@ cudaError_t side_stream(cudaStream_t main, SideStream** out) {
 inline cudaError_t hop(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
   cudaError_t e = cudaEventRecord(ev, from);
   return e == cudaSuccess ? cudaStreamWaitEvent(to, ev, 0) : e;
+}
+
+// Number of GRAD -> Gram -> solve -> update chains of a batched step of nt blocks (mg_steps_chunk);
+// chain p covers blocks [nt * p / parts, nt * (p + 1) / parts).
+template <typename T>
+int chain_parts(bool side_stream, int nt) {
+  static const int parts_env = getenv("BD3MG_PARTS") ? atoi(getenv("BD3MG_PARTS")) : 0;
+  int parts = (side_stream && nt >= 4 && sizeof(T) == 8 && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
+  if (parts > 1 && parts_env > 0) parts = std::min(std::min(parts_env, kMaxParts), nt);
+  return parts;
 }
 
 // Options of the batched step used by the sweep driver.
@@ -617,6 +628,10 @@ struct StepOpts {
   T* rec_snap = nullptr;
   double* rec_sums = nullptr;
   bool side_forked = false;    // the caller forked the side stream (ss->ev[0]) before this call
+  std::function<int()> after_resid;  // side-stream work of the caller, enqueued right after the residual launch
+  // per-chain regulariser gradient: chain p's gradient correlation waits for chain_ready[p] only (events the
+  // caller records on the side stream after that chain's stencil), not for the whole side stream
+  const cudaEvent_t* chain_ready = nullptr;
 };
 
 // The gradient correlation with the regulariser gradient fused into its
@@ -843,6 +858,10 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     if (rsq_side) a.partials = rsq_parts;
     CU(conv_launch<T>(M_RESID, false, a, 0, s));
     launched();
+    if (opt.after_resid) {
+      const int rc = opt.after_resid();
+      if (rc) return rc;
+    }
     if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
       if (rec_job >= 0) {
         const long long tl = conv_tiles<T>(g, M_RESID);
@@ -860,7 +879,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   }
   // join the recorder / regulariser-gradient stencil of the side stream (when one was forked: by the
   // sweep before this call, or above)
-  if (opt.ss && (greg_side || opt.side_forked)) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
+  if (opt.ss && (greg_side || opt.side_forked) && !opt.chain_ready) CU(hop(opt.ss->side, s, opt.ss->ev[1]));
   if (rsq_forked) {  // the recorder's data term next to the gradient correlation
     CU(hop(s, opt.ss->side, opt.ss->ev[7]));
     CU(reduce(rsq_parts, 1, {rsq_range}, opt.resid_sq, 1, opt.ss->side));
@@ -878,9 +897,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   // rows of x and d_mem, and no later kernel of another chain reads those (the Gram inputs are the
   // chain's own g and d rows), so the chains are independent once the residual is formed.
   // BD3MG_PARTS=n overrides (1: one chain, the pre-split layout).
-  static const int parts_env = getenv("BD3MG_PARTS") ? atoi(getenv("BD3MG_PARTS")) : 0;
-  int parts = (opt.ss && nt >= 4 && sizeof(T) == 8 && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
-  if (parts > 1 && parts_env > 0) parts = std::min(std::min(parts_env, kMaxParts), nt);
+  const int parts = chain_parts<T>(opt.ss != nullptr, nt);
   // the fused-gradient recorder (opt-in) reduces its sums over all chains before the update: one tail
   const bool chain_tails = parts > 1 && !opt.rec_gradf;
   std::vector<std::pair<long long, long long>> granges(nt);
@@ -969,6 +986,9 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   };
   for (int part = 1; part < parts; ++part)  // fork after RESID / greg
     CU(hop(s, opt.ss->chain[part - 1], opt.ss->ev[8 + 5 * part]));
+  if (opt.chain_ready)  // each chain waits for its own blocks' regulariser gradient
+    for (int part = 0; part < parts; ++part)
+      CU(cudaStreamWaitEvent(part == 0 ? s : opt.ss->chain[part - 1], opt.chain_ready[part], 0));
   for (int part = 0; part < parts; ++part) {
     const int t0 = (int)((long long)nt * part / parts), t1 = (int)((long long)nt * (part + 1) / parts);
     const int np = t1 - t0;
@@ -1632,6 +1652,9 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   }
   SideStream* ss = nullptr;
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
+  // (function scope: the step below may run the stencil launches through opt.after_resid)
+  const cudaEvent_t* chain_events = nullptr;
+  std::function<int()> side_work;
   if (!ws.measure && rec_gradf) {
     if (!ws.ok()) return ws_fail(ws);
     if (!getenv("BD3MG_NO_SIDE_STREAM")) {
@@ -1648,6 +1671,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
       s1 = ss->side;
     }
     // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll
+    side_work = [&, s1]() -> int {
     if (!rec) {
       CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s1));
     } else {
@@ -1663,8 +1687,23 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
           J.out0 = grb[b]; J.out1 = wb[b];
         }
 #ifndef BD3MG_EXP_SKIP_GREG
-        int rc = launch_greg<T>(e, true, s1);
-        if (rc) return rc;
+        if (chain_events) {
+          // one stencil launch per chain of the block step (partial rows stay job-major), an event after each
+          const int parts = chain_parts<T>(true, nb);
+          for (int part = 0; part < parts; ++part) {
+            const int b0 = (int)((long long)nb * part / parts), b1 = (int)((long long)nb * (part + 1) / parts);
+            StArgs<T> ep = e;
+            ep.njobs = b1 - b0;
+            for (int b = b0; b < b1; ++b) ep.jobs[b - b0] = e.jobs[b];
+            ep.partials = eparts + (size_t)b0 * z_tiles<T>(g) * kEvalNV;
+            int rc = launch_greg<T>(ep, true, s1);
+            if (rc) return rc;
+            CU(cudaEventRecord(chain_events[part], s1));
+          }
+        } else {
+          int rc = launch_greg<T>(e, true, s1);
+          if (rc) return rc;
+        }
 #endif
       } else {
         e.njobs = 1;
@@ -1676,6 +1715,28 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
       if (sw->snap && !fused)  // fused: the stencil rolled the snapshot as it read it
         CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
                            cudaMemcpyDeviceToDevice, s1));
+    }
+      return BD3MG_OK;
+    };
+    // The stencil is enqueued right AFTER the residual correlation's launch: the block scheduler serves
+    // equal-priority kernels in launch order, so the correlation's CTAs go first and the stencil fills its
+    // last wave instead of holding every SM for the sweep's first 27 us; and it is launched once per chain
+    // of the block step, so the first chain's gradient correlation starts as soon as its own blocks'
+    // regulariser gradient is there (C2 fp64: 409 -> 406 us; fp32, one chain: 1% slower at C2, neutral at
+    // C3, so fp64 only).  BD3MG_GREG_AFTER=0: the stencil first.
+    static const bool greg_after = [] {
+      const char* e = getenv("BD3MG_GREG_AFTER");
+      return e ? e[0] != '0' : true;
+    }();
+    if (greg_after && sizeof(T) == 8 && opt.side_forked && !(r_full && !r_refresh)) {
+      opt.after_resid = side_work;
+      if (fused && rec && chain_parts<T>(true, nb) > 1 && !getenv("BD3MG_NO_CHAIN_GREG")) {
+        chain_events = ss->ev + 8 + 5 * kMaxParts;  // kMaxParts events after the chain events
+        opt.chain_ready = chain_events;
+      }
+    } else {
+      const int rc0 = side_work();
+      if (rc0) return rc0;
     }
   }
   // (2) the fused block steps at the anchor (x, dmem updated in place)
