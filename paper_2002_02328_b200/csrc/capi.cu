@@ -600,7 +600,8 @@ inline cudaError_t hop(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
 // chain p covers blocks [nt * p / parts, nt * (p + 1) / parts).
 template <typename T>
 int chain_parts(bool side_stream, int nt) {
-  static const int parts_env = getenv("BD3MG_PARTS") ? atoi(getenv("BD3MG_PARTS")) : 0;
+  const char* pe = getenv("BD3MG_PARTS");  // (read per call: the tests switch it)
+  const int parts_env = pe ? atoi(pe) : 0;
   int parts = (side_stream && nt >= 4 && sizeof(T) == 8 && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
   if (parts > 1 && parts_env > 0) parts = std::min(std::min(parts_env, kMaxParts), nt);
   return parts;
@@ -1724,10 +1725,8 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     // of the block step, so the first chain's gradient correlation starts as soon as its own blocks'
     // regulariser gradient is there (C2 fp64: 409 -> 406 us; fp32, one chain: 1% slower at C2, neutral at
     // C3, so fp64 only).  BD3MG_GREG_AFTER=0: the stencil first.
-    static const bool greg_after = [] {
-      const char* e = getenv("BD3MG_GREG_AFTER");
-      return e ? e[0] != '0' : true;
-    }();
+    const char* ga = getenv("BD3MG_GREG_AFTER");  // (read per call: the tests switch it)
+    const bool greg_after = ga ? ga[0] != '0' : true;
     if (greg_after && sizeof(T) == 8 && opt.side_forked && !(r_full && !r_refresh)) {
       opt.after_resid = side_work;
       if (fused && rec && chain_parts<T>(true, nb) > 1 && !getenv("BD3MG_NO_CHAIN_GREG")) {

@@ -340,3 +340,64 @@ def test_cyclic_incremental_ragged_blocks():
         assert abs(a.f() - b.f()) <= 1e-11 * abs(a.f())
     xa, xb = a.x.cpu().numpy(), b.x.cpu().numpy()
     assert np.linalg.norm(xa - xb) <= 1e-10 * np.linalg.norm(xa)
+
+
+def _sweeps_with_env(env, sweeps=3, dtype=torch.float64, cfg_name="C1", graph=False):
+    """x, d_mem, StepInfo and recorder terms after `sweeps` block-Jacobi sweeps with `env` set."""
+    import os
+    from paper_2002_02328_b200 import configs, objective, runtime
+    cfg = configs.CONFIGS[cfg_name]
+    psf, truth, y, x0, params = configs.make_problem(cfg)
+    obj = objective.Objective(psf, y, params)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        eng = runtime.JacobiSweeper(obj, x0, 4 if cfg_name == "C1" else cfg.block_height, dtype)
+        terms = []
+        eng.sweep()
+        if graph:
+            eng.capture()
+        for _ in range(sweeps - 1):
+            eng.sweep()
+            terms.append(eng.terms.clone())
+        torch.cuda.synchronize()
+        return eng.x.clone(), eng.prev.clone(), eng.info.clone(), terms
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_chain_layouts_are_bitwise_equal(graph):
+    """The GRAD -> Gram -> solve -> update chains of the batched step (1 to 4
+    chains, per-chain regulariser-gradient launches enqueued before or after
+    the residual correlation) only reorder independent launches: iterate,
+    memory store, StepInfo and recorder terms must not change by a bit."""
+    ref = _sweeps_with_env({"BD3MG_PARTS": "1", "BD3MG_GREG_AFTER": "0"}, graph=graph)
+    for env in ({"BD3MG_PARTS": "2", "BD3MG_GREG_AFTER": "0"}, {"BD3MG_PARTS": "2", "BD3MG_GREG_AFTER": "1"},
+                {"BD3MG_PARTS": "3", "BD3MG_GREG_AFTER": "1"}, {"BD3MG_PARTS": "4", "BD3MG_GREG_AFTER": "1"}, {}):
+        got = _sweeps_with_env(env, graph=graph)
+        assert torch.equal(got[0], ref[0]), env
+        assert torch.equal(got[1], ref[1]), env
+        assert torch.equal(got[2], ref[2]), env
+        for u, v in zip(got[3], ref[3]):
+            assert torch.equal(u, v), env
+
+
+def test_fused_regulariser_gram_matches_the_stencil():
+    """The regulariser Gram terms computed by the Gram correlation's tiles
+    (rg_center, the default) against the separate reg_gram stencil
+    (BD3MG_NO_RGF=1): same sums in another grouping -- Gram entries, rhs and
+    coefficients to 1e-12, iterates to 1e-11 after three sweeps; the flags
+    (column mask, status) exactly."""
+    a = _sweeps_with_env({})
+    b = _sweeps_with_env({"BD3MG_NO_RGF": "1"})
+    ia, ib = a[2].cpu().numpy(), b[2].cpu().numpy()
+    np.testing.assert_allclose(ia[:, :7], ib[:, :7], rtol=1e-11, atol=1e-300)
+    assert np.array_equal(ia[:, [7, 8, 12]], ib[:, [7, 8, 12]])
+    xa, xb = a[0].cpu().numpy(), b[0].cpu().numpy()
+    assert np.linalg.norm(xa - xb) <= 1e-11 * np.linalg.norm(xb)
+    assert not np.array_equal(ia[:, :3], ib[:, :3]) or np.array_equal(xa, xb)
