@@ -796,9 +796,14 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     rg_total += (h[t] + c - 1) / c;
   }
   // fused into the Gram correlation: one partial row per (block plane, Gram tile)
-  const bool rgf = rgf_ok<T>(g, gmode);
+  // (only with TMA staging: every d_mem block must be 16-byte aligned like the workspace rows)
+  bool rgf = rgf_ok<T>(g, gmode) && !getenv("BD3MG_NO_TMA");
+  for (int t = 0; t < nt && rgf; ++t)
+    if (tasks[t].d_mem && (reinterpret_cast<uintptr_t>(tasks[t].d_mem) & 15)) rgf = false;
   const long long rgf_tiles = rgf ? conv_tiles<T>(g, M_GRAM2) : 0;
-  const long long reg_rows = rgf ? hsum * rgf_tiles : rg_total * z_tiles<T>(g);
+  // (sized for either path: the choice may differ between the sizing call and the launch)
+  const long long reg_rows = std::max<long long>(rgf_ok<T>(g, gmode) ? hsum * conv_tiles<T>(g, M_GRAM2) : 0,
+                                                 rg_total * z_tiles<T>(g));
   double* rparts = ws.take<double>((size_t)reg_rows * kRegNV);
   if (ws.measure) return BD3MG_OK;
   if (!ws.ok()) return ws_fail(ws);

@@ -184,6 +184,9 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 #ifndef BD3MG_RY1
 #define BD3MG_RY1 16  // rows per thread of the single-input modes
 #endif
+#ifndef BD3MG_EARLY_ISSUE
+#define BD3MG_EARLY_ISSUE 1  // first TMA load of a tile before its coefficient staging (conv_tile)
+#endif
 #ifndef BD3MG_WY1
 #define BD3MG_WY1 4   // warps per CTA of the single-input modes (tile height WY1 * RY1); measured on B200
                       // at C2: 8 warps x 8 rows (same 64 x 64 tile) ran H in 99.5-117 us against 80 us
@@ -654,8 +657,6 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
     mbar_init(&mbar[1], 1);
     fence_mbar_init();
   }
-  stage_coefs<T, ADJ>(p, zo, coef_s, Cfg::NT);
-  __syncthreads();
 
   auto issue = [&](int step, int b) {
     T* dst = tiles + b * NIN * Cfg::TILE;
@@ -677,6 +678,15 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
       cp_async_commit();
     }
   };
+
+  // One tile per CTA (no barriers handed in): the first plane's TMA load is issued before the
+  // coefficients are staged, so its latency overlaps their global loads and the barrier below.
+  // (The persistent kernel's tiles follow one another in a CTA: its previous tile's epilogue may
+  // still read the ring, so there the load waits for the barrier.)
+  const bool early = BD3MG_EARLY_ISSUE && tma && bars == nullptr && nstep > 0;
+  if (early) issue(0, 0);
+  stage_coefs<T, ADJ>(p, zo, coef_s, Cfg::NT);
+  __syncthreads();
 
   T acc[NIN][RY][RX];
 #pragma unroll
@@ -704,7 +714,7 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
       cp_async_commit();
     }
   }
-  if (nstep > 0) issue(0, 0);
+  if (nstep > 0 && !early) issue(0, 0);
   // the epilogue operand rows of this tile are pulled into L2 two taps before
   // the end, so the epilogue's loads do not wait on DRAM
   constexpr bool kEpiLoad = MODE == M_RESID || MODE == M_GRAD || MODE == M_GRAMC;
