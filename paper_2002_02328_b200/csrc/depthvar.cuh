@@ -112,20 +112,39 @@ struct CtaPos {
   long long cta;
 };
 BD3MG_D CtaPos cta_pos(int group) {
-  const long long nx = gridDim.x, ny = gridDim.y, nz = gridDim.z, T = nx * ny;
-  const long long L = blockIdx.x + nx * (blockIdx.y + ny * (long long)blockIdx.z);
+  // (32-bit arithmetic where the grid allows: a 64-bit division is a ~100-instruction subroutine, and
+  // every thread of every CTA runs these before its first load)
+  const unsigned nx = gridDim.x, ny = gridDim.y, nz = gridDim.z, T = nx * ny;
+  const unsigned long long total = (unsigned long long)T * nz;
+  if (total < (1ull << 31) && (unsigned long long)nx * ny < (1ull << 31)) {
+    const unsigned L = blockIdx.x + nx * (blockIdx.y + ny * blockIdx.z);
+    unsigned t, z;
+    if (group <= 0 || (unsigned)group >= T) {
+      t = blockIdx.x + nx * blockIdx.y;
+      z = blockIdx.z;
+    } else {
+      const unsigned G = (unsigned)group, g = L / (G * nz), full = T / G;
+      const unsigned gg = g < full ? G : T - full * G;
+      const unsigned rem = L - g * G * nz;
+      z = rem / gg;
+      t = g * G + rem % gg;
+    }
+    return {(int)(t % nx), (int)(t / nx), (int)z, (long long)z * T + t};
+  }
+  const long long nxl = gridDim.x, nyl = gridDim.y, nzl = gridDim.z, Tl = nxl * nyl;
+  const long long L = blockIdx.x + nxl * (blockIdx.y + nyl * (long long)blockIdx.z);
   long long t, z;
-  if (group <= 0 || group >= T) {
-    t = L % T;
-    z = L / T;
+  if (group <= 0 || group >= Tl) {
+    t = L % Tl;
+    z = L / Tl;
   } else {
-    const long long g = L / ((long long)group * nz), full = T / group;
-    const long long gg = g < full ? group : T - full * group;
-    const long long rem = L - g * group * nz;
+    const long long g = L / ((long long)group * nzl), full = Tl / group;
+    const long long gg = g < full ? group : Tl - full * group;
+    const long long rem = L - g * group * nzl;
     z = rem / gg;
     t = g * group + rem % gg;
   }
-  return {(int)(t % nx), (int)(t / nx), (int)z, z * T + t};
+  return {(int)(t % nxl), (int)(t / nxl), (int)z, z * Tl + t};
 }
 
 template <int MODE>
@@ -653,6 +672,8 @@ BD3MG_D void conv_tile(const ConvGeom<T>& p, const TileIO<T>& io, int zo, int x0
   const int nstep = TWOPASS ? 2 * ntap : ntap;
 
   if (tma && threadIdx.x == 0) {
+    tma_prefetch_desc(io.in0.tm);  // the descriptor fetch overlaps the barrier set-up
+    if constexpr (NIN == 2 || TWOPASS) tma_prefetch_desc(io.in1.tm);
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     fence_mbar_init();
