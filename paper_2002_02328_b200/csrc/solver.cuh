@@ -159,18 +159,78 @@ static __device__ void solve_one(const SolveArgs& p, int j, const double* D, con
 }
 
 // One CTA per block: reduce its conv and regulariser partial rows (same
-// deterministic order as reduce_rows_kernel), then the 2x2 solve.
+// deterministic order per value as reduce_rows_kernel: fixed stride classes
+// per thread, warp butterfly, warps in order), then the 2x2 solve.  Both row
+// sets are summed in ONE pass -- their loads are issued together and all 15
+// values share the butterfly and the barrier -- because this launch sits on
+// the critical path of every block step and is pure latency.
 static __global__ void __launch_bounds__(kEwNT) reduce_solve_kernel(const __grid_constant__ SolveArgs p,
                                                              const double* __restrict__ gram_rows,
                                                              const double* __restrict__ reg_rows,
                                                              double* __restrict__ info) {
-  __shared__ double s[kRedMaxNV][kEwNT / 32];
+  constexpr int NW = kEwNT / 32, NG = 3, NR = kRegNV;
+  __shared__ double s[NG + NR][NW];
   const int j = blockIdx.x;
-  double D[kRedMaxNV], R[kRedMaxNV];
-  cta_sum_rows(gram_rows, p.nv_gram, p.g_begin[j], p.g_end[j], s, D);
-  if (p.nv_gram < 3) { D[1] = 0.0; D[2] = 0.0; }
-  cta_sum_rows(reg_rows, kRegNV, p.r_begin[j], p.r_end[j], s, R);
-  if (threadIdx.x == 0) solve_one(p, j, D, R, info + j * kInfoNV);
+  const int nvg = p.nv_gram;
+  double aD[NG], aR[NR];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) aD[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) aR[k] = 0.0;
+  long long rg = p.g_begin[j] + threadIdx.x, rr = p.r_begin[j] + threadIdx.x;
+  const long long eg = p.g_end[j], er = p.r_end[j];
+  while (rg < eg || rr < er) {
+    double vD[NG], vR[NR];
+    const bool hg = rg < eg, hr = rr < er;
+#pragma unroll
+    for (int k = 0; k < NG; ++k) vD[k] = (hg && k < nvg) ? gram_rows[rg * nvg + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) vR[k] = hr ? reg_rows[rr * NR + k] : 0.0;
+    if (hg) {
+#pragma unroll
+      for (int k = 0; k < NG; ++k)
+        if (k < nvg) aD[k] += vD[k];
+    }
+    if (hr) {
+#pragma unroll
+      for (int k = 0; k < NR; ++k) aR[k] += vR[k];
+    }
+    rg += kEwNT;
+    rr += kEwNT;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NG; ++k) aD[k] += __shfl_xor_sync(0xffffffffu, aD[k], off);
+#pragma unroll
+    for (int k = 0; k < NR; ++k) aR[k] += __shfl_xor_sync(0xffffffffu, aR[k], off);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NG; ++k) s[k][warp] = aD[k];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) s[NG + k][warp] = aR[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double D[kRedMaxNV], R[kRedMaxNV];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      double t = s[k][0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) t += s[k][w];
+      D[k] = k < nvg ? t : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      double t = s[NG + k][0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) t += s[NG + k][w];
+      R[k] = t;
+    }
+    solve_one(p, j, D, R, info + j * kInfoNV);
+  }
 }
 
 // ---------------------------------------------------------------------------
