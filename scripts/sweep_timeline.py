@@ -1,5 +1,5 @@
 """Kernel timeline of graph-replayed block-Jacobi sweeps (torch.profiler / CUPTI):
-    python scripts/sweep_timeline.py C2 [sweeps]
+    python scripts/sweep_timeline.py C2 [sweeps] [jacobi|cyclic]
 Prints, per kernel of the last replayed sweep, start / end relative to the sweep's first kernel and the
 stream it ran on: shows what actually overlaps inside the captured graph (ncu serialises launches)."""
 import sys
@@ -16,7 +16,8 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 dt = torch.float64 if cfg.dtype == "f64" else torch.float32
 psf, truth, y, x0, params = configs.make_problem(cfg)
 obj = objective.Objective(psf, y, params)
-eng = runtime.JacobiSweeper(obj, x0, cfg.block_height, dt)
+mode = sys.argv[3] if len(sys.argv) > 3 else "jacobi"
+eng = (runtime.CyclicSweeper if mode == "cyclic" else runtime.JacobiSweeper)(obj, x0, cfg.block_height, dt)
 import os
 eng.sweep()
 if not os.environ.get("TIMELINE_EAGER"):
