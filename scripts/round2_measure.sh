@@ -5,7 +5,7 @@ set -u
 O=gpurun_out/r2
 mkdir -p $O
 run() { tag=$1; shift; timeout 900 python bench.py "$@" > $O/bench_$tag.log 2>&1; grep '^{' $O/bench_$tag.log | tail -1 > $O/bench_$tag.json; echo "$tag rc=$?"; }
-run C2 --config C2
+( time run C2 --config C2 ) 2>&1 | tail -4
 run C2f32 --config C2f32
 run C3 --config C3
 run C4 --config C4
