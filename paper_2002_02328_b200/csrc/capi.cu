@@ -166,8 +166,9 @@ long long z_tiles(const bd3mg_geom_t* g) {
 }
 
 // Regulariser gradient (+ omega, + recorder terms when `eval`) of every job.
+constexpr size_t kGregPad = 8192;  // see launch_greg
 template <typename T>
-int launch_greg(StArgs<T>& a, bool eval, cudaStream_t s) {
+int launch_greg(StArgs<T>& a, bool eval, cudaStream_t s, size_t pad_hint = 0) {
   if (a.njobs == 0) return BD3MG_OK;
   if (!st_use_tma<T>(a.nx)) {
     CU(st_launch_z<T>(eval ? greg_z_kernel<T, true> : greg_z_kernel<T, false>, a, greg_z_smem<T>(), s));
@@ -184,8 +185,15 @@ int launch_greg(StArgs<T>& a, bool eval, cudaStream_t s) {
       return fail(BD3MG_EINVAL, "greg: TMA descriptor rejected (job %d)", j);
   }
   auto kern = eval ? greg_t_kernel<T, true> : greg_t_kernel<T, false>;
-  CU(ensure_smem_attr(kern, G::smem()));
-  kern<<<dim3((a.nx + kTmX - 1) / kTmX, (a.ny + kTmY - 1) / kTmY, a.njobs), kTmNT, G::smem(), s>>>(a, tm);
+  // pad_hint: extra dynamic shared memory per CTA of the sweep's recorder stencil (fp64, when it runs in
+  // the last wave of a residual correlation: the sweep passes kGregPad): 8 KB more make it 33 KB,
+  // so at most four of its CTAs (not five or six) share an SM with a 76.7 KB correlation CTA of the
+  // residual correlation's last wave, in which this stencil runs.  Measured at C2: 395.5 -> 390.0 us per
+  // sweep (4 KB: 396, 14 KB: 398, 24 KB: 398-399, 50 KB: 402).  BD3MG_ST_PAD=<bytes> overrides.
+  static const long pad_env = getenv("BD3MG_ST_PAD") ? atol(getenv("BD3MG_ST_PAD")) : -1;
+  const size_t pad = pad_env >= 0 ? (size_t)pad_env : pad_hint;
+  CU(ensure_smem_attr(kern, G::smem() + pad + 49 * 1024));
+  kern<<<dim3((a.nx + kTmX - 1) / kTmX, (a.ny + kTmY - 1) / kTmY, a.njobs), kTmNT, G::smem() + pad, s>>>(a, tm);
   launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
@@ -1702,7 +1710,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
             ep.njobs = b1 - b0;
             for (int b = b0; b < b1; ++b) ep.jobs[b - b0] = e.jobs[b];
             ep.partials = eparts + (size_t)b0 * z_tiles<T>(g) * kEvalNV;
-            int rc = launch_greg<T>(ep, true, s1);
+            int rc = launch_greg<T>(ep, true, s1, kGregPad);
             if (rc) return rc;
             CU(cudaEventRecord(chain_events[part], s1));
           }
