@@ -185,8 +185,8 @@ int launch_greg(StArgs<T>& a, bool eval, cudaStream_t s, size_t pad_hint = 0) {
       return fail(BD3MG_EINVAL, "greg: TMA descriptor rejected (job %d)", j);
   }
   auto kern = eval ? greg_t_kernel<T, true> : greg_t_kernel<T, false>;
-  // pad_hint: extra dynamic shared memory per CTA of the sweep's recorder stencil (fp64, when it runs in
-  // the last wave of a residual correlation: the sweep passes kGregPad): 8 KB more make it 33 KB,
+  // pad_hint: extra dynamic shared memory per CTA of the sweep's recorder stencil (when it runs next to a
+  // residual correlation: the sweep passes kGregPad).  In fp64, 8 KB more make it 33 KB,
   // so at most four of its CTAs (not five or six) share an SM with a 76.7 KB correlation CTA of the
   // residual correlation's last wave, in which this stencil runs.  Measured at C2: 395.5 -> 390.0 us per
   // sweep (4 KB: 396, 14 KB: 398, 24 KB: 398-399, 50 KB: 402).  BD3MG_ST_PAD=<bytes> overrides.
@@ -1715,7 +1715,10 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
             CU(cudaEventRecord(chain_events[part], s1));
           }
         } else {
-          int rc = launch_greg<T>(e, true, s1);
+          // (next to the residual correlation on the side stream: the same residency bound, measured at
+          // fp32 too -- C2 fp32 282.9 -> 279.1 us, C3 3784 -> 3770 us)
+          const bool beside_resid = s1 != s && !(r_full && !r_refresh);
+          int rc = launch_greg<T>(e, true, s1, beside_resid ? kGregPad : 0);
           if (rc) return rc;
         }
 #endif
