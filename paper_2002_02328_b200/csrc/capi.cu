@@ -218,8 +218,13 @@ int launch_reg_gram(StArgs<T>& a, cudaStream_t s) {
         (J.b && !encode_tmap(&tm.b[j], J.b, sizeof(T) == 8, a.nx, a.ny, h, G::BW, G::BH)))
       return fail(BD3MG_EINVAL, "reg_gram: TMA descriptor rejected (job %d)", j);
   }
-  CU(ensure_smem_attr(reg_gram_t_kernel<T>, G::smem()));
-  reg_gram_t_kernel<T><<<dim3((a.nx + kTmX - 1) / kTmX, (a.ny + kTmY - 1) / kTmY, a.njobs), kTmNT, G::smem(), s>>>(a, tm);
+  // extra dynamic shared memory per CTA, as for the recorder stencil (launch_greg): measured for the fp32
+  // sweeps, where this stencil runs next to the Gram correlation (C2 fp32 278.8 -> 277.6 us, C3 3769 ->
+  // 3753 us at +8 KB; +16 KB and more are slower).  BD3MG_RG_PAD=<bytes> overrides.
+  static const long pad_env = getenv("BD3MG_RG_PAD") ? atol(getenv("BD3MG_RG_PAD")) : -1;
+  const size_t pad = pad_env >= 0 ? (size_t)pad_env : (sizeof(T) == 4 ? kGregPad : 0);
+  CU(ensure_smem_attr(reg_gram_t_kernel<T>, G::smem() + pad + 49 * 1024));
+  reg_gram_t_kernel<T><<<dim3((a.nx + kTmX - 1) / kTmX, (a.ny + kTmY - 1) / kTmY, a.njobs), kTmNT, G::smem() + pad, s>>>(a, tm);
   launched();
   CU(cudaGetLastError());
   return BD3MG_OK;
