@@ -642,7 +642,10 @@ struct StepOpts {
   T* rec_snap = nullptr;
   double* rec_sums = nullptr;
   bool side_forked = false;    // the caller forked the side stream (ss->ev[0]) before this call
-  std::function<int()> after_resid;  // side-stream work of the caller, enqueued right after the residual launch
+  // side-stream work of the caller, enqueued right after the residual launch(es): phase -1 = all of it;
+  // with the residual launched per chain (below), phase 0 = the first chain's share (after the first
+  // launch), phase 1 = the rest (after the second)
+  std::function<int(int)> after_resid;
   // per-chain regulariser gradient: chain p's gradient correlation waits for chain_ready[p] only (events the
   // caller records on the side stream after that chain's stencil), not for the whole side stream
   const cudaEvent_t* chain_ready = nullptr;
@@ -796,6 +799,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   // (sized whether or not a side stream is used: workspace sizing runs without one)
   double* rsq_parts = opt.resid_sq ? ws.take<double>((size_t)std::max<long long>(resid_rows, 1)) : nullptr;
   bool rsq_forked = false;  // the residual's reduction goes to the side stream
+  bool resid_split = false;  // the residual went out per chain: the first chain runs on a chain stream
   std::pair<long long, long long> rsq_range{0, 0};
   long long grad_rows = 0;  // recorder partial rows of the fused gradient (one per GRADF CTA)
   for (int t = 0; t < nt; ++t) grad_rows += conv_rows<T>(g, M_GRAD, h[t]);
@@ -875,16 +879,51 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     // them runs on the side stream, off the correlations' critical path (joined before the solve)
     const bool rsq_side = opt.resid_sq && opt.ss && rec_job >= 0;
     if (rsq_side) a.partials = rsq_parts;
-    CU(conv_launch<T>(M_RESID, false, a, 0, s));
-    launched();
-    if (opt.after_resid) {
-      const int rc = opt.after_resid();
-      if (rc) return rc;
+    // Two chains with per-chain stencils (the fp64 Jacobi sweep): the residual is launched per chain as
+    // well -- first the rows the first chain's gradient needs, [u_lo, ohi of its last block], then the
+    // rest -- with the first chain's stencil enqueued between the two.  The first chain's gradient
+    // correlation then starts when ITS rows and ITS stencil are done, under the second launch, instead of
+    // after the whole residual and the stencil's run in its last wave.  Partial rows keep the order of the
+    // single launch (plane-major), so the recorder's sum has the same bits.
+    int zsplit = -1;
+    if (opt.chain_ready && opt.after_resid && shared && rjobs.size() == 1 &&
+        chain_parts<T>(opt.ss != nullptr, nt) == 2 && !getenv("BD3MG_NO_RESID_SPLIT")) {
+      const int tA = (int)((long long)nt * 1 / 2) - 1;  // last block of the first chain
+      if (ohi[tA] < u_hi && ohi[tA] >= u_lo) zsplit = (int)ohi[tA];
     }
+    long long resid_b0 = 0;  // first partial row of the recorder job
+    if (zsplit >= 0) {
+      const long long tl = conv_tiles<T>(g, M_RESID);
+      ConvArgs<T> a1 = a, a2 = a;
+      a1.jobs[0].nout = zsplit - (int)rjobs[0].first + 1;
+      a2.jobs[0].out_lo = zsplit + 1;
+      a2.jobs[0].nout = (int)(rjobs[0].first + rjobs[0].second) - (zsplit + 1);
+      a2.jobs[0].dst0 = a.jobs[0].dst0 + (long long)a1.jobs[0].nout * plane;
+      a2.jobs[0].sub = a.jobs[0].sub + (long long)a1.jobs[0].nout * plane;
+      a2.partials = a.partials + (size_t)conv_rows<T>(g, M_RESID, a1.jobs[0].nout);
+      CU(conv_launch<T>(M_RESID, false, a1, 0, s));
+      launched();
+      CU(cudaEventRecord(opt.ss->ev[2], s));  // the first chain's residual rows are done
+      int rc = opt.after_resid(0);
+      if (rc) return rc;
+      CU(conv_launch<T>(M_RESID, false, a2, 0, s));
+      launched();
+      rc = opt.after_resid(1);
+      if (rc) return rc;
+      (void)tl;
+    } else {
+      CU(conv_launch<T>(M_RESID, false, a, 0, s));
+      launched();
+      if (opt.after_resid) {
+        const int rc = opt.after_resid(-1);
+        if (rc) return rc;
+      }
+      if (rec_job >= 0) resid_b0 = (long long)a.jobs[rec_job].work_begin * conv_tiles<T>(g, M_RESID);
+    }
+    resid_split = zsplit >= 0;
     if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
       if (rec_job >= 0) {
-        const long long tl = conv_tiles<T>(g, M_RESID);
-        const long long b0 = (long long)a.jobs[rec_job].work_begin * tl;
+        const long long b0 = resid_b0;
         if (rsq_side) {  // enqueued below, after the side stream's stencil is joined
           rsq_range = {b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)};
           rsq_forked = true;
@@ -1003,15 +1042,25 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
 #endif
     return BD3MG_OK;
   };
-  for (int part = 1; part < parts; ++part)  // fork after RESID / greg
-    CU(hop(s, opt.ss->chain[part - 1], opt.ss->ev[8 + 5 * part]));
+  // stream of a chain: the first stays on the caller's stream -- except with the per-chain residual,
+  // where the caller's stream still carries the second residual launch: then the first chain moves to a
+  // chain stream (it waits for its residual rows only) and the second stays on the caller's
+  auto stream_of = [&](int part) -> cudaStream_t {
+    if (resid_split) return part == 0 ? opt.ss->chain[0] : s;
+    return part == 0 ? s : opt.ss->chain[part - 1];
+  };
+  if (resid_split) {
+    CU(cudaStreamWaitEvent(opt.ss->chain[0], opt.ss->ev[2], 0));
+  } else {
+    for (int part = 1; part < parts; ++part)  // fork after RESID / greg
+      CU(hop(s, opt.ss->chain[part - 1], opt.ss->ev[8 + 5 * part]));
+  }
   if (opt.chain_ready)  // each chain waits for its own blocks' regulariser gradient
-    for (int part = 0; part < parts; ++part)
-      CU(cudaStreamWaitEvent(part == 0 ? s : opt.ss->chain[part - 1], opt.chain_ready[part], 0));
+    for (int part = 0; part < parts; ++part) CU(cudaStreamWaitEvent(stream_of(part), opt.chain_ready[part], 0));
   for (int part = 0; part < parts; ++part) {
     const int t0 = (int)((long long)nt * part / parts), t1 = (int)((long long)nt * (part + 1) / parts);
     const int np = t1 - t0;
-    cudaStream_t sp = part == 0 ? s : opt.ss->chain[part - 1];
+    cudaStream_t sp = stream_of(part);
     {
       ConvArgs<T> a = base_args<T>(g, r, K);
       a.njobs = np;
@@ -1106,8 +1155,8 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       if (rc) return rc;
     }
   }
-  for (int part = 1; part < parts; ++part)  // join the later chains
-    CU(hop(opt.ss->chain[part - 1], s, opt.ss->ev[11 + 5 * part]));
+  for (int part = 0; part < parts; ++part)  // join the chains that ran on chain streams
+    if (stream_of(part) != s) CU(hop(stream_of(part), s, opt.ss->ev[11 + 5 * part]));
   if (opt.ss) CU(hop(opt.ss->side, s, opt.ss->ev[3]));  // join the side stream
   if (opt.rec_gradf)  // the recorder's stencil sums from the fused gradient's partial rows
     CU(reduce(eparts_g, kGradfNV, {{0, grad_rows}}, opt.rec_sums, kGradfNV, s));
@@ -1673,7 +1722,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
   cudaStream_t s1 = s;  // stream of the recorder / regulariser-gradient stencil
   // (function scope: the step below may run the stencil launches through opt.after_resid)
   const cudaEvent_t* chain_events = nullptr;
-  std::function<int()> side_work;
+  std::function<int(int)> side_work;
   if (!ws.measure && rec_gradf) {
     if (!ws.ok()) return ws_fail(ws);
     if (!getenv("BD3MG_NO_SIDE_STREAM")) {
@@ -1690,8 +1739,9 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
       s1 = ss->side;
     }
     // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll
-    side_work = [&, s1]() -> int {
+    side_work = [&, s1](int phase) -> int {
     if (!rec) {
+      if (phase == 0) return BD3MG_OK;
       CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s1));
     } else {
       StArgs<T> e = st_args<T>(g, r);
@@ -1710,6 +1760,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
           // one stencil launch per chain of the block step (partial rows stay job-major), an event after each
           const int parts = chain_parts<T>(true, nb);
           for (int part = 0; part < parts; ++part) {
+            if ((phase == 0 && part != 0) || (phase == 1 && part == 0)) continue;
             const int b0 = (int)((long long)nb * part / parts), b1 = (int)((long long)nb * (part + 1) / parts);
             StArgs<T> ep = e;
             ep.njobs = b1 - b0;
@@ -1733,6 +1784,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
         e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
         CU(st_launch<T>(eval_kernel<T>, e, s1));
       }
+      if (phase == 0) return BD3MG_OK;  // (the reduction follows the last stencil launch)
       CU(reduce(eparts, kEvalNV, {{0, fused ? nb * z_tiles<T>(g) : nrec * st_tiles(g)}}, sums + 1, kEvalNV, s1));
       if (sw->snap && !fused)  // fused: the stencil rolled the snapshot as it read it
         CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
@@ -1755,7 +1807,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
         opt.chain_ready = chain_events;
       }
     } else {
-      const int rc0 = side_work();
+      const int rc0 = side_work(-1);
       if (rc0) return rc0;
     }
   }
