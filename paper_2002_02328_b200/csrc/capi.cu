@@ -643,8 +643,8 @@ struct StepOpts {
   double* rec_sums = nullptr;
   bool side_forked = false;    // the caller forked the side stream (ss->ev[0]) before this call
   // side-stream work of the caller, enqueued right after the residual launch(es): phase -1 = all of it;
-  // with the residual launched per chain (below), phase 0 = the first chain's share (after the first
-  // launch), phase 1 = the rest (after the second)
+  // with the residual launched per chain (below), phase k = chain k's share (after launch k; the last
+  // phase also closes the recorder's reduction)
   std::function<int(int)> after_resid;
   // per-chain regulariser gradient: chain p's gradient correlation waits for chain_ready[p] only (events the
   // caller records on the side stream after that chain's stencil), not for the whole side stream
@@ -885,32 +885,42 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     // correlation then starts when ITS rows and ITS stencil are done, under the second launch, instead of
     // after the whole residual and the stencil's run in its last wave.  Partial rows keep the order of the
     // single launch (plane-major), so the recorder's sum has the same bits.
-    int zsplit = -1;
-    if (opt.chain_ready && opt.after_resid && shared && rjobs.size() == 1 &&
-        chain_parts<T>(opt.ss != nullptr, nt) == 2 && !getenv("BD3MG_NO_RESID_SPLIT")) {
-      const int tA = (int)((long long)nt * 1 / 2) - 1;  // last block of the first chain
-      if (ohi[tA] < u_hi && ohi[tA] >= u_lo) zsplit = (int)ohi[tA];
+    // (any number of chains: launch k covers the rows up to chain k's last gradient row that the earlier
+    // launches have not produced; the last chain stays on the caller's stream)
+    std::vector<int> zend;  // last residual row of each launch
+    const int nchains = chain_parts<T>(opt.ss != nullptr, nt);
+    if (opt.chain_ready && opt.after_resid && shared && rjobs.size() == 1 && nchains >= 2 && nchains <= 4 &&
+        !getenv("BD3MG_NO_RESID_SPLIT")) {
+      int prev = (int)u_lo - 1;
+      for (int k = 0; k < nchains; ++k) {
+        const int tl_ = (int)((long long)nt * (k + 1) / nchains) - 1;  // last block of chain k
+        const int e = k == nchains - 1 ? (int)u_hi : (int)std::min<int64_t>(ohi[tl_], u_hi);
+        if (e <= prev) { zend.clear(); break; }
+        zend.push_back(e);
+        prev = e;
+      }
+      if (!zend.empty() && zend.back() != (int)u_hi) zend.clear();
     }
     long long resid_b0 = 0;  // first partial row of the recorder job
-    if (zsplit >= 0) {
-      const long long tl = conv_tiles<T>(g, M_RESID);
-      ConvArgs<T> a1 = a, a2 = a;
-      a1.jobs[0].nout = zsplit - (int)rjobs[0].first + 1;
-      a2.jobs[0].out_lo = zsplit + 1;
-      a2.jobs[0].nout = (int)(rjobs[0].first + rjobs[0].second) - (zsplit + 1);
-      a2.jobs[0].dst0 = a.jobs[0].dst0 + (long long)a1.jobs[0].nout * plane;
-      a2.jobs[0].sub = a.jobs[0].sub + (long long)a1.jobs[0].nout * plane;
-      a2.partials = a.partials + (size_t)conv_rows<T>(g, M_RESID, a1.jobs[0].nout);
-      CU(conv_launch<T>(M_RESID, false, a1, 0, s));
-      launched();
-      CU(cudaEventRecord(opt.ss->ev[2], s));  // the first chain's residual rows are done
-      int rc = opt.after_resid(0);
-      if (rc) return rc;
-      CU(conv_launch<T>(M_RESID, false, a2, 0, s));
-      launched();
-      rc = opt.after_resid(1);
-      if (rc) return rc;
-      (void)tl;
+    if (!zend.empty()) {
+      cudaEvent_t evr[3] = {opt.ss->ev[2], opt.ss->ev[4], opt.ss->ev[5]};
+      int z0 = (int)rjobs[0].first;
+      size_t prow = 0;
+      for (int k = 0; k < nchains; ++k) {
+        ConvArgs<T> ak = a;
+        ak.jobs[0].out_lo = z0;
+        ak.jobs[0].nout = zend[k] - z0 + 1;
+        ak.jobs[0].dst0 = a.jobs[0].dst0 + (long long)(z0 - (int)rjobs[0].first) * plane;
+        ak.jobs[0].sub = a.jobs[0].sub + (long long)(z0 - (int)rjobs[0].first) * plane;
+        ak.partials = a.partials + prow;
+        CU(conv_launch<T>(M_RESID, false, ak, 0, s));
+        launched();
+        if (k < nchains - 1) CU(cudaEventRecord(evr[k], s));  // chain k's residual rows are done
+        const int rc = opt.after_resid(k);
+        if (rc) return rc;
+        prow += (size_t)conv_rows<T>(g, M_RESID, ak.jobs[0].nout);
+        z0 = zend[k] + 1;
+      }
     } else {
       CU(conv_launch<T>(M_RESID, false, a, 0, s));
       launched();
@@ -920,7 +930,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       }
       if (rec_job >= 0) resid_b0 = (long long)a.jobs[rec_job].work_begin * conv_tiles<T>(g, M_RESID);
     }
-    resid_split = zsplit >= 0;
+    resid_split = !zend.empty();
     if (opt.resid_sq) {  // recorder data term of the anchor, before cparts is reused
       if (rec_job >= 0) {
         const long long b0 = resid_b0;
@@ -1046,11 +1056,12 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   // where the caller's stream still carries the second residual launch: then the first chain moves to a
   // chain stream (it waits for its residual rows only) and the second stays on the caller's
   auto stream_of = [&](int part) -> cudaStream_t {
-    if (resid_split) return part == 0 ? opt.ss->chain[0] : s;
+    if (resid_split) return part < parts - 1 ? opt.ss->chain[part] : s;
     return part == 0 ? s : opt.ss->chain[part - 1];
   };
   if (resid_split) {
-    CU(cudaStreamWaitEvent(opt.ss->chain[0], opt.ss->ev[2], 0));
+    cudaEvent_t evr[3] = {opt.ss->ev[2], opt.ss->ev[4], opt.ss->ev[5]};
+    for (int part = 0; part < parts - 1; ++part) CU(cudaStreamWaitEvent(opt.ss->chain[part], evr[part], 0));
   } else {
     for (int part = 1; part < parts; ++part)  // fork after RESID / greg
       CU(hop(s, opt.ss->chain[part - 1], opt.ss->ev[8 + 5 * part]));
@@ -1741,7 +1752,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll
     side_work = [&, s1](int phase) -> int {
     if (!rec) {
-      if (phase == 0) return BD3MG_OK;
+      if (phase >= 0 && phase < chain_parts<T>(true, nb) - 1) return BD3MG_OK;
       CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s1));
     } else {
       StArgs<T> e = st_args<T>(g, r);
@@ -1760,7 +1771,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
           // one stencil launch per chain of the block step (partial rows stay job-major), an event after each
           const int parts = chain_parts<T>(true, nb);
           for (int part = 0; part < parts; ++part) {
-            if ((phase == 0 && part != 0) || (phase == 1 && part == 0)) continue;
+            if (phase >= 0 && part != phase) continue;
             const int b0 = (int)((long long)nb * part / parts), b1 = (int)((long long)nb * (part + 1) / parts);
             StArgs<T> ep = e;
             ep.njobs = b1 - b0;
@@ -1784,7 +1795,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
         e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
         CU(st_launch<T>(eval_kernel<T>, e, s1));
       }
-      if (phase == 0) return BD3MG_OK;  // (the reduction follows the last stencil launch)
+      if (phase >= 0 && phase < chain_parts<T>(true, nb) - 1) return BD3MG_OK;  // (the reduction follows the last stencil launch)
       CU(reduce(eparts, kEvalNV, {{0, fused ? nb * z_tiles<T>(g) : nrec * st_tiles(g)}}, sums + 1, kEvalNV, s1));
       if (sw->snap && !fused)  // fused: the stencil rolled the snapshot as it read it
         CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
