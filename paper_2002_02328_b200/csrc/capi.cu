@@ -611,11 +611,15 @@ inline cudaError_t hop(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
 
 // Number of GRAD -> Gram -> solve -> update chains of a batched step of nt blocks (mg_steps_chunk);
 // chain p covers blocks [nt * p / parts, nt * (p + 1) / parts).
+// fp32: chains where the launches are short enough for their tails to matter -- measured with the
+// per-chain residual and stencils: C2 fp32 +9.4%, C3 +0.8%, C4 +0.7%, C5 (2^29 voxels) -0.4% -- so up to
+// 2^27 voxels per step.  `voxels`: rows x plane of the step's blocks.
 template <typename T>
-int chain_parts(bool side_stream, int nt) {
+int chain_parts(bool side_stream, int nt, long long voxels) {
   const char* pe = getenv("BD3MG_PARTS");  // (read per call: the tests switch it)
   const int parts_env = pe ? atoi(pe) : 0;
-  int parts = (side_stream && nt >= 4 && sizeof(T) == 8 && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
+  const bool dtype_ok = sizeof(T) == 8 || (voxels > 0 && voxels <= (1LL << 27) && !getenv("BD3MG_NO_CHAINS_F32"));
+  int parts = (side_stream && nt >= 4 && dtype_ok && !getenv("BD3MG_NO_SPLIT")) ? 2 : 1;
   if (parts > 1 && parts_env > 0) parts = std::min(std::min(parts_env, kMaxParts), nt);
   return parts;
 }
@@ -797,7 +801,10 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   const long long conv_part_rows = std::max<long long>(std::max(resid_rows, gram_rows), kSumsqCtas);
   double* cparts = ws.take<double>((size_t)conv_part_rows * 3);
   // (sized whether or not a side stream is used: workspace sizing runs without one)
-  double* rsq_parts = opt.resid_sq ? ws.take<double>((size_t)std::max<long long>(resid_rows, 1)) : nullptr;
+  // (+ one plane pair of rows per extra launch when the residual goes out per chain in fp32)
+  double* rsq_parts = opt.resid_sq ? ws.take<double>((size_t)std::max<long long>(
+                                         resid_rows + kMaxParts * conv_tiles<T>(g, M_RESID), 1))
+                                   : nullptr;
   bool rsq_forked = false;  // the residual's reduction goes to the side stream
   bool resid_split = false;  // the residual went out per chain: the first chain runs on a chain stream
   std::pair<long long, long long> rsq_range{0, 0};
@@ -888,7 +895,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
     // (any number of chains: launch k covers the rows up to chain k's last gradient row that the earlier
     // launches have not produced; the last chain stays on the caller's stream)
     std::vector<int> zend;  // last residual row of each launch
-    const int nchains = chain_parts<T>(opt.ss != nullptr, nt);
+    const int nchains = chain_parts<T>(opt.ss != nullptr, nt, hsum * plane);
     if (opt.chain_ready && opt.after_resid && shared && rjobs.size() == 1 && nchains >= 2 && nchains <= 4 &&
         !getenv("BD3MG_NO_RESID_SPLIT")) {
       int prev = (int)u_lo - 1;
@@ -902,6 +909,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       if (!zend.empty() && zend.back() != (int)u_hi) zend.clear();
     }
     long long resid_b0 = 0;  // first partial row of the recorder job
+    long long resid_nrows = rec_job >= 0 ? conv_rows<T>(g, M_RESID, rjobs[rec_job].second) : 0;  // and their number
     if (!zend.empty()) {
       cudaEvent_t evr[3] = {opt.ss->ev[2], opt.ss->ev[4], opt.ss->ev[5]};
       int z0 = (int)rjobs[0].first;
@@ -921,6 +929,7 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
         prow += (size_t)conv_rows<T>(g, M_RESID, ak.jobs[0].nout);
         z0 = zend[k] + 1;
       }
+      resid_nrows = (long long)prow;  // (the two-plane kernels round every launch up to whole plane pairs)
     } else {
       CU(conv_launch<T>(M_RESID, false, a, 0, s));
       launched();
@@ -935,10 +944,10 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
       if (rec_job >= 0) {
         const long long b0 = resid_b0;
         if (rsq_side) {  // enqueued below, after the side stream's stencil is joined
-          rsq_range = {b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)};
+          rsq_range = {b0, b0 + resid_nrows};
           rsq_forked = true;
         } else {
-          CU(reduce(cparts, 1, {{b0, b0 + conv_rows<T>(g, M_RESID, rjobs[rec_job].second)}}, opt.resid_sq, 1, s));
+          CU(reduce(cparts, 1, {{b0, b0 + resid_nrows}}, opt.resid_sq, 1, s));
         }
       } else {
         CU(cudaMemsetAsync(opt.resid_sq, 0, sizeof(double), s));
@@ -959,13 +968,13 @@ int mg_steps_chunk(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, cons
   }
   // (2b)-(7) The blocks are cut into `parts` groups, each a chain GRAD -> (regulariser Gram on the side
   // stream | data Gram) -> solve -> update on its own stream.  The correlations of one chain fill the last
-  // waves of another's instead of idling SMs (measured: +1% at C2 fp64 with two chains; -4% at C2 fp32,
-  // whose chains are short, so fp64 only), and an earlier chain's HBM-bound solve + update run under a
-  // later chain's FMA-bound Gram correlation instead of after it.  A block's update touches only its own
+  // waves of another's instead of idling SMs, and an earlier chain's HBM-bound solve + update run under a
+  // later chain's FMA-bound Gram correlation instead of after it (fp32 steps up to 2^27 voxels as well,
+  // see chain_parts).  A block's update touches only its own
   // rows of x and d_mem, and no later kernel of another chain reads those (the Gram inputs are the
   // chain's own g and d rows), so the chains are independent once the residual is formed.
   // BD3MG_PARTS=n overrides (1: one chain, the pre-split layout).
-  const int parts = chain_parts<T>(opt.ss != nullptr, nt);
+  const int parts = chain_parts<T>(opt.ss != nullptr, nt, hsum * plane);
   // the fused-gradient recorder (opt-in) reduces its sums over all chains before the update: one tail
   const bool chain_tails = parts > 1 && !opt.rec_gradf;
   std::vector<std::pair<long long, long long>> granges(nt);
@@ -1752,7 +1761,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     // (1) recorder pass of the anchor (+ regulariser gradient when fused), snapshot roll
     side_work = [&, s1](int phase) -> int {
     if (!rec) {
-      if (phase >= 0 && phase < chain_parts<T>(true, nb) - 1) return BD3MG_OK;
+      if (phase >= 0 && phase < chain_parts<T>(true, nb, hsum * plane) - 1) return BD3MG_OK;
       CU(cudaMemsetAsync(sums + 1, 0, kEvalNV * sizeof(double), s1));
     } else {
       StArgs<T> e = st_args<T>(g, r);
@@ -1769,7 +1778,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
 #ifndef BD3MG_EXP_SKIP_GREG
         if (chain_events) {
           // one stencil launch per chain of the block step (partial rows stay job-major), an event after each
-          const int parts = chain_parts<T>(true, nb);
+          const int parts = chain_parts<T>(true, nb, hsum * plane);
           for (int part = 0; part < parts; ++part) {
             if (phase >= 0 && part != phase) continue;
             const int b0 = (int)((long long)nb * part / parts), b1 = (int)((long long)nb * (part + 1) / parts);
@@ -1795,7 +1804,7 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
         e.jobs[0].lo = (int)sw->rec_lo; e.jobs[0].hi = (int)sw->rec_hi;
         CU(st_launch<T>(eval_kernel<T>, e, s1));
       }
-      if (phase >= 0 && phase < chain_parts<T>(true, nb) - 1) return BD3MG_OK;  // (the reduction follows the last stencil launch)
+      if (phase >= 0 && phase < chain_parts<T>(true, nb, hsum * plane) - 1) return BD3MG_OK;  // (the reduction follows the last stencil launch)
       CU(reduce(eparts, kEvalNV, {{0, fused ? nb * z_tiles<T>(g) : nrec * st_tiles(g)}}, sums + 1, kEvalNV, s1));
       if (sw->snap && !fused)  // fused: the stencil rolled the snapshot as it read it
         CU(cudaMemcpyAsync(sw->snap, x + (sw->rec_lo - sw->frag_z0) * plane, (size_t)nrec * plane * sizeof(T),
@@ -1811,9 +1820,9 @@ int jacobi_sweep_impl(const bd3mg_geom_t* g, const bd3mg_reg_t* r, const T* K, c
     // C3, so fp64 only).  BD3MG_GREG_AFTER=0: the stencil first.
     const char* ga = getenv("BD3MG_GREG_AFTER");  // (read per call: the tests switch it)
     const bool greg_after = ga ? ga[0] != '0' : true;
-    if (greg_after && sizeof(T) == 8 && opt.side_forked && !(r_full && !r_refresh)) {
+    if (greg_after && chain_parts<T>(true, nb, hsum * plane) > 1 && opt.side_forked && !(r_full && !r_refresh)) {
       opt.after_resid = side_work;
-      if (fused && rec && chain_parts<T>(true, nb) > 1 && !getenv("BD3MG_NO_CHAIN_GREG")) {
+      if (fused && rec && chain_parts<T>(true, nb, hsum * plane) > 1 && !getenv("BD3MG_NO_CHAIN_GREG")) {
         chain_events = ss->ev + 8 + 5 * kMaxParts;  // kMaxParts events after the chain events
         opt.chain_ready = chain_events;
       }

@@ -401,3 +401,18 @@ def test_fused_regulariser_gram_matches_the_stencil():
     xa, xb = a[0].cpu().numpy(), b[0].cpu().numpy()
     assert np.linalg.norm(xa - xb) <= 1e-11 * np.linalg.norm(xb)
     assert not np.array_equal(ia[:, :3], ib[:, :3]) or np.array_equal(xa, xb)
+
+
+def test_chain_layouts_fp32_bitwise_iterates():
+    """fp32 sweeps run in chains too (up to 2^27 voxels per step): iterate,
+    memory store and StepInfo must not depend on the layout by a bit; the
+    recorder's data term regroups (the two-plane kernels pair other planes
+    when the residual goes out per chain), so it is compared to fp32 rounding."""
+    ref = _sweeps_with_env({"BD3MG_NO_CHAINS_F32": "1"}, dtype=torch.float32)
+    for env in ({}, {"BD3MG_PARTS": "3"}, {"BD3MG_GREG_AFTER": "0"}):
+        got = _sweeps_with_env(env, dtype=torch.float32)
+        assert torch.equal(got[0], ref[0]), env
+        assert torch.equal(got[1], ref[1]), env
+        assert torch.equal(got[2], ref[2]), env
+        for u, v in zip(got[3], ref[3]):
+            torch.testing.assert_close(u, v, rtol=1e-6, atol=0)
